@@ -1,0 +1,423 @@
+"""Pins of the CPU oracle against things other than itself (CPU only, -m "not gpu").
+
+Each test fixes the oracle to something the paper or mathematics determines independently:
+hand-derived worked values (tests/golden/spec_examples.json, cited), closed forms, invariants,
+exhaustive brute force on tiny inputs, and special cases that reduce to library routines
+(torch float64 conv2d / max_pool2d / matmul, exact for integers below 2^53).  The tests are
+chosen so that a dropped term, a wrong sign or index, a transposed operand, a wrong padding
+value or a wrong bit order fails at least one of them.
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1808_00209_b200 import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _expand(x):
+    if isinstance(x, str):
+        n, v = x.split("x")
+        return [int(v)] * int(n)
+    return x
+
+
+def popcount(v: int) -> int:
+    return bin(int(v)).count("1")
+
+
+# ----------------------------------------------------------------------------- Eq. (1), (2)
+def test_sign_eq1(orc):
+    """Eq. (1): zero maps to -1."""
+    assert orc.sign(0.0) == -1 and orc.sign(-0.0) == -1
+    assert orc.sign(1e-300) == 1 and orc.sign(3.7) == 1 and orc.sign(-2.0) == -1
+
+
+@pytest.mark.parametrize("case", GOLD["pack"])
+def test_pack_golden(orc, case):
+    x = _expand(case["x"])
+    assert list(orc.pack(np.array(x, np.int8), case["B"])) == case["words"]
+    assert list(orc.unpack(np.array(case["words"], np.uint32), len(x), case["B"])) == x
+
+
+def test_pack_msb_first_matches_alg1_shift(orc):
+    """Alg. 1 line 10: v |= s << (B - 1 - i) -- element i (0-based) of a word is
+    bit B-1-i.  One-hot +1 vectors pin the bit order of Eq. (2) for every B."""
+    for B in (1, 2, 9, 25, 32):
+        for i in range(B):
+            x = -np.ones(B, np.int8)
+            x[i] = 1
+            assert int(orc.pack(x, B)[0]) == 1 << (B - 1 - i)
+
+
+def test_pack_partial_last_word(orc):
+    """Reading R12: D not divisible by B -> the last word holds D mod B elements at the top
+    positions, pad bits 0 (3 channels with B = 32 -> bits 31, 30, 29)."""
+    assert int(orc.pack(np.array([1, 1, 1], np.int8), 32)[0]) == 0xE0000000
+    assert int(orc.pack(np.array([1, -1, 1], np.int8), 32)[0]) == 0xA0000000
+    w = orc.pack(np.ones(40, np.int8), 32)
+    assert list(w) == [0xFFFFFFFF, 0xFF000000]
+
+
+def test_unpack_rejects_pad_bits(orc):
+    with pytest.raises(ValueError):
+        orc.unpack(np.array([0xE0000001], np.uint32), 3, 32)
+    with pytest.raises(ValueError):
+        orc.unpack(np.array([1 << 9], np.uint32), 9, 9)
+
+
+def test_pack_roundtrip_random(orc):
+    rng = np.random.default_rng(1)
+    for B in range(1, 33):
+        for D in (1, B - 1 if B > 1 else 1, B, 3 * B + 1, 97):
+            x = rng.choice(np.array([-1, 1], np.int8), D)
+            assert np.array_equal(orc.unpack(orc.pack(x, B), D, B), x)
+
+
+# ----------------------------------------------------------------------------- Eq. (4) identity
+def _all_pm1(W):
+    return np.array(list(itertools.product([-1, 1], repeat=W)), np.int8)
+
+
+@pytest.mark.parametrize("W", range(1, 9))
+def test_eq4_identity_exhaustive(orc, W):
+    """Eq. (4) PAPER.md:265-267 for every pair of +/-1 vectors of length W <= 8: the oracle's
+    +/-1 dot product equals W - 2 popc(pack(a) XOR pack(b)) with the oracle's own packer."""
+    allv = _all_pm1(W)
+    packed = [int(orc.pack(v, 32)[0]) for v in allv]
+    for i, a in enumerate(allv):
+        dots = orc.dense(a, allv)  # all 2^W dot products with a at once
+        for j in range(len(allv)):
+            assert dots[j] == W - 2 * popcount(packed[i] ^ packed[j])
+
+
+@pytest.mark.parametrize("W", [25, 32, 64, 100])
+def test_eq4_identity_random(orc, W):
+    rng = np.random.default_rng(W)
+    A = rng.choice(np.array([-1, 1], np.int8), (2000, W))
+    Bm = rng.choice(np.array([-1, 1], np.int8), (50, W))
+    pa = [orc.pack(a, 32) for a in A]
+    pb = [orc.pack(b, 32) for b in Bm]
+    for i in range(len(A)):
+        dots = orc.dense(A[i], Bm)
+        for j in range(len(Bm)):
+            pc = sum(popcount(int(u) ^ int(v)) for u, v in zip(pa[i], pb[j]))
+            assert dots[j] == W - 2 * pc
+            assert abs(dots[j]) <= W and (dots[j] - W) % 2 == 0
+
+
+@pytest.mark.parametrize("case", GOLD["xnor_dot"])
+def test_xnor_dot_golden(orc, case):
+    assert orc.dense(np.array(case["a"], np.int8), np.array([case["b"]], np.int8))[0] == case["dot"]
+
+
+def test_weight_pack_golden(orc):
+    case = GOLD["weight_pack"][0]
+    k = np.array(case["kernel3x3"], np.float64).reshape(-1)
+    signs = np.array([orc.sign(v) for v in k], np.int8)
+    assert int(orc.pack(signs, case["B"])[0]) == case["word"]
+
+
+# ----------------------------------------------------------------------------- Eq. (3) binary conv
+def _torch_conv_pm1(x, wt):
+    """Library special case: -1 padding + cross-correlation, float64 (exact)."""
+    k = wt.shape[1]
+    R = (k - 1) // 2
+    xt = torch.from_numpy(x.astype(np.float64)).permute(2, 0, 1)[None]
+    xt = F.pad(xt, (R, R, R, R), value=-1.0)
+    wt_t = torch.from_numpy(wt.astype(np.float64)).permute(0, 3, 1, 2)
+    return F.conv2d(xt, wt_t)[0].permute(1, 2, 0).numpy()
+
+
+@pytest.mark.parametrize("h,w,cin,cout,k", [(3, 3, 1, 1, 3), (4, 4, 2, 3, 3), (5, 5, 3, 2, 5), (5, 7, 1, 4, 5),
+                                            (6, 4, 5, 2, 1), (7, 7, 2, 2, 7), (2, 9, 3, 3, 5)])
+def test_conv_binary_vs_torch(orc, h, w, cin, cout, k):
+    x = synth.numpy(synth.pm1((h, w, cin), 10 + h * w + cin))
+    wt = synth.numpy(synth.pm1((cout, k, k, cin), 20 + k + cout))
+    acc = orc.conv_binary(x, wt)
+    ref = _torch_conv_pm1(x, wt)
+    assert np.array_equal(acc, ref.astype(np.int64))
+
+
+@pytest.mark.parametrize("k,cin,h,w", [(3, 1, 4, 4), (5, 3, 6, 7), (5, 32, 7, 5), (7, 2, 9, 9), (1, 4, 3, 2)])
+def test_conv_binary_closed_form_all_ones(orc, k, cin, h, w):
+    """All-(+1) map and kernel with -1 padding: acc = c_in (2 n_in - K^2), n_in = in-map taps
+    (reading R4: out-of-bounds taps count as -1 and in N = K^2 c_in).  All-(-1) kernel negates."""
+    R = (k - 1) // 2
+    x = np.ones((h, w, cin), np.int8)
+    wt = np.ones((2, k, k, cin), np.int8)
+    wt[1] = -1
+    acc = orc.conv_binary(x, wt)
+    for y in range(h):
+        for xx in range(w):
+            rows = sum(1 for d in range(-R, R + 1) if 0 <= y + d < h)
+            cols = sum(1 for d in range(-R, R + 1) if 0 <= xx + d < w)
+            n_in = rows * cols
+            assert acc[y, xx, 0] == cin * (2 * n_in - k * k)
+            assert acc[y, xx, 1] == -cin * (2 * n_in - k * k)
+    if h > 2 * R and w > 2 * R:
+        assert acc[R, R, 0] == k * k * cin
+
+
+def test_conv_golden(orc):
+    g = {c["name"]: c for c in GOLD["conv"]}
+    c = g["checkerboard_vs_ones_3x3_centre"]
+    x = np.array(c["x"], np.int8)[:, :, None]
+    wt = np.array(c["w"], np.int8)[None, :, :, None]
+    assert orc.conv_binary(x, wt)[c["at"][0], c["at"][1], 0] == c["acc"]
+    c = g["corner_patch_27"]
+    h, w = c["map_hw"]
+    k = c["k"]
+    kernel = orc.unpack(np.array([c["patch_word_B9"]], np.uint32), k * k, k * k).reshape(1, k, k, 1)
+    acc = orc.conv_binary(np.ones((h, w, 1), np.int8), kernel)
+    assert acc[0, 0, 0] == k * k  # the kernel equals the corner patch: perfect match
+    assert np.all(acc <= k * k)
+    c = g["all_ones_k5_c3_interior"]
+    acc = orc.conv_binary(np.ones((7, 7, c["c_in"]), np.int8), np.ones((1, c["k"], c["k"], c["c_in"]), np.int8))
+    assert acc[3, 3, 0] == c["acc_interior"]
+
+
+def test_conv_orientation_not_transposed(orc):
+    """Cross-correlation, not convolution and no (ky,kx) transposition
+    (reading R3): a one-hot kernel at tap (ky,kx) reads x[y+ky-R, x+kx-R]."""
+    rng = np.random.default_rng(5)
+    h, w, k = 6, 7, 3
+    x = rng.choice(np.array([-1, 1], np.int8), (h, w, 1))
+    for ky in range(k):
+        for kx in range(k):
+            # kernel = +1 at (ky,kx), and +1/-1 pairs elsewhere cancel? use c_in=1: sum of 9 terms;
+            # compare the difference of two kernels that differ only at (ky,kx)
+            w1 = np.ones((1, k, k, 1), np.int8)
+            w2 = w1.copy()
+            w2[0, ky, kx, 0] = -1
+            d = (orc.conv_binary(x, w1) - orc.conv_binary(x, w2))[:, :, 0]
+            for y in range(h):
+                for xx in range(w):
+                    yy, xs = y + ky - 1, xx + kx - 1
+                    v = x[yy, xs, 0] if 0 <= yy < h and 0 <= xs < w else -1
+                    assert d[y, xx] == 2 * v
+
+
+def test_conv_parity_and_range(orc):
+    x = synth.numpy(synth.pm1((9, 8, 7), 3))
+    wt = synth.numpy(synth.pm1((5, 3, 3, 7), 4))
+    acc = orc.conv_binary(x, wt)
+    N = 9 * 7
+    assert np.all(np.abs(acc) <= N) and np.all((acc - N) % 2 == 0)
+
+
+def test_conv_fault_injection_localised(orc):
+    """flipping one weight changes only that output channel."""
+    x = synth.numpy(synth.pm1((8, 8, 4), 6))
+    wt = synth.numpy(synth.pm1((6, 3, 3, 4), 7))
+    a0 = orc.conv_binary(x, wt)
+    wt2 = wt.copy()
+    wt2[3, 1, 2, 1] *= -1
+    a1 = orc.conv_binary(x, wt2)
+    diff = np.nonzero(np.any(a0 != a1, axis=(0, 1)))[0]
+    assert list(diff) == [3]
+
+
+# ----------------------------------------------------------------------------- real first layer
+def test_conv_real_vs_torch_zero_pad(orc):
+    x = synth.numpy(synth.images(1, 7, 6, 3, 11))[0].astype(np.float64)
+    wt = synth.numpy(synth.pm1((4, 5, 5, 3), 12))
+    acc = orc.conv_real(x, wt)
+    ref = F.conv2d(torch.from_numpy(x).permute(2, 0, 1)[None], torch.from_numpy(wt.astype(np.float64)).permute(0, 3, 1, 2),
+                   padding=2)[0].permute(1, 2, 0).numpy()
+    assert np.array_equal(acc, ref)
+
+
+def test_conv_real_closed_form(orc):
+    """Constant image v, all-(+1) kernel, zero padding: acc = v c_in n_in (reading R5)."""
+    v, k, cin, h, w = 7.0, 3, 2, 4, 5
+    acc = orc.conv_real(np.full((h, w, cin), v), np.ones((1, k, k, cin), np.int8))
+    for y in range(h):
+        for xx in range(w):
+            n_in = sum(1 for a in (-1, 0, 1) if 0 <= y + a < h) * sum(1 for b in (-1, 0, 1) if 0 <= xx + b < w)
+            assert acc[y, xx, 0] == v * cin * n_in
+    c = GOLD["real_conv"][0]
+    acc = orc.conv_real(np.full((5, 5, 1), c["value"]), np.ones((1, c["k"], c["k"], 1), np.int8))
+    assert acc[2, 2, 0] == c["acc_interior"]
+
+
+# ----------------------------------------------------------------------------- threshold, pool, dense
+def test_binarize_golden(orc):
+    c = GOLD["binarize"][0]
+    b = orc.binarize(np.array([c["acc"]], np.int64).reshape(1, -1)).reshape(-1)
+    assert int(orc.pack(b, 4)[0]) == c["bits_B4"]
+
+
+def test_binarize_threshold_flip(orc):
+    acc = np.array([[-3, 0, 2, 7]], np.int64)
+    assert list(orc.binarize(acc, thr=[2, -1, 2, 6])[0]) == [-1, 1, -1, 1]
+    assert list(orc.binarize(acc, thr=[2, -1, 2, 6], flip=[1, 0, 0, 1])[0]) == [1, 1, -1, -1]
+
+
+def test_maxpool_vs_torch_and_or(orc):
+    x = synth.numpy(synth.pm1((6, 8, 5), 13))
+    y = orc.maxpool2(x)
+    ref = F.max_pool2d(torch.from_numpy(x.astype(np.float64)).permute(2, 0, 1)[None], 2)[0].permute(1, 2, 0).numpy()
+    assert np.array_equal(y, ref.astype(np.int8))
+    for case in GOLD["maxpool"]:
+        b = np.array(case["bits"]).reshape(2, 2, 1) * 2 - 1
+        assert (orc.maxpool2(b.astype(np.int8))[0, 0, 0] + 1) // 2 == case["out"]
+    # OR of packed words == packed max (Table 2 pooling as a bitwise OR)
+    px = orc.pack_channels(x)
+    py = orc.pack_channels(y)
+    por = px[0::2, 0::2] | px[0::2, 1::2] | px[1::2, 0::2] | px[1::2, 1::2]
+    assert np.array_equal(py, por)
+
+
+def test_sign_pool_commute(orc):
+    """sign is monotone: binarize(maxpool_int(acc)) == maxpool(binarize(acc)) (reading R9)."""
+    rng = np.random.default_rng(9)
+    acc = rng.integers(-5, 6, (8, 6, 3)).astype(np.int64)
+    a = orc.maxpool2(orc.binarize(acc))
+    mp = F.max_pool2d(torch.from_numpy(acc.astype(np.float64)).permute(2, 0, 1)[None], 2)[0].permute(1, 2, 0).numpy()
+    b = orc.binarize(mp.astype(np.int64))
+    assert np.array_equal(a, b)
+
+
+def test_dense_vs_matmul(orc):
+    x = synth.numpy(synth.pm1((77,), 14))
+    W = synth.numpy(synth.pm1((9, 77), 15))
+    assert np.array_equal(orc.dense(x, W), W.astype(np.int64) @ x.astype(np.int64))
+    assert orc.dense(x, x[None])[0] == 77 and orc.dense(x, -x[None])[0] == -77
+
+
+@pytest.mark.parametrize("case", GOLD["argmax"])
+def test_argmax_golden(orc, case):
+    assert orc.argmax(case["v"]) == case["cls"]
+
+
+# ----------------------------------------------------------------------------- input binarization
+@pytest.mark.parametrize("case", GOLD["threshold"])
+def test_threshold_golden(orc, case):
+    x = np.full((1, 1, 1), case["x"], np.float64)
+    assert orc.binarize_input(x, orc.THRESH_RGB, [case["T"]])[0, 0, 0] == case["out"]
+
+
+def test_threshold_monotone_in_T(orc):
+    x = synth.numpy(synth.images(1, 5, 5, 3, 21))[0]
+    prev = None
+    for t in range(-260, 10, 7):
+        b = orc.binarize_input(x, orc.THRESH_RGB, [t, t + 1, t - 1])
+        if prev is not None:
+            assert np.all(b >= prev)  # raising T never flips +1 -> -1
+        prev = b
+
+
+@pytest.mark.parametrize("case", GOLD["luma"])
+def test_luma_golden(orc, case):
+    assert orc.luma(*case["rgb"]) == case["y"]
+
+
+def test_gray_threshold(orc):
+    x = np.zeros((1, 2, 3))
+    x[0, 0] = [255, 0, 0]  # luma 76
+    x[0, 1] = [0, 0, 255]  # luma 29
+    assert list(orc.binarize_input(x, orc.THRESH_GRAY, [-50])[0, :, 0]) == [1, -1]
+    assert list(orc.binarize_input(x, orc.THRESH_GRAY, [-76])[0, :, 0]) == [-1, -1]  # 76 - 76 = 0 -> -1
+
+
+@pytest.mark.parametrize("case", GOLD["lbp"])
+def test_lbp_golden(orc, case):
+    g = np.array(case["gray3x3"], np.float64)
+    x = np.repeat(g[:, :, None], 3, axis=2)  # R = G = B = v has luma v
+    out = orc.binarize_input(x, orc.LBP)
+    assert list(out[1, 1]) == case["centre_out"]
+
+
+def test_lbp_orientation_and_border(orc):
+    """Reading R16: channel j <- neighbour n_{3j} clockwise from top-left (TL, R, BL);
+    replicate border (a corner pixel compares against itself for missing neighbours)."""
+    g = np.zeros((3, 3))
+    g[1, 2] = 9  # only R is brighter
+    x = np.repeat(g[:, :, None], 3, axis=2)
+    assert list(orc.binarize_input(x, orc.LBP)[1, 1]) == [-1, 1, -1]
+    g = np.zeros((3, 3))
+    g[2, 0] = 9  # only BL
+    x = np.repeat(g[:, :, None], 3, axis=2)
+    assert list(orc.binarize_input(x, orc.LBP)[1, 1]) == [-1, -1, 1]
+    g = np.arange(9, dtype=np.float64).reshape(3, 3)
+    x = np.repeat(g[:, :, None], 3, axis=2)
+    # top-left corner (0,0): TL/BL clamp to itself or (1,0); R = (0,1) = 1 > 0
+    assert list(orc.binarize_input(x, orc.LBP)[0, 0]) == [-1, 1, 1]
+
+
+# ----------------------------------------------------------------------------- whole network
+def _torch_forward(images, mode, T, layers):
+    """Library composition of the Section 2 pipeline in float64 (independent of the oracle's
+    code): input binarization written with torch ops, conv2d with -1 padding, sign with
+    acc <= 0 -> -1, max_pool2d, HWC flatten, matmul."""
+    def sgn(a):  # Eq. (1): a <= 0 -> -1
+        return (a > 0).double() * 2 - 1
+
+    x = torch.from_numpy(images.astype(np.float64))  # [n,h,w,c]
+    if mode == 1:
+        x = sgn(x + torch.from_numpy(np.asarray(T, np.float32).astype(np.float64)))
+    elif mode == 0:
+        x = sgn(x)
+    x = x.permute(0, 3, 1, 2)
+    flat = None
+    for i, L in enumerate(layers):
+        wt = torch.from_numpy(L["wt"].astype(np.float64))
+        last = i == len(layers) - 1
+        if L["kind"] == "conv":
+            R = (L["k"] - 1) // 2
+            a = F.conv2d(F.pad(x, (R, R, R, R), value=-1.0), wt.permute(0, 3, 1, 2))
+            x = sgn(a)
+            if L.get("pool", 1) == 2:
+                x = F.max_pool2d(x, 2)
+        else:
+            if flat is None:
+                flat = x.permute(0, 2, 3, 1).reshape(x.shape[0], -1)
+            a = flat @ wt.T
+            if last:
+                return a.numpy().astype(np.int64)
+            flat = sgn(a)
+    raise AssertionError
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_forward_vs_torch_composition(orc, mode):
+    spec = dict(h=8, w=8, c=3, layers=[dict(kind="conv", k=3, c_out=4, pool=2), dict(kind="conv", k=5, c_out=6, pool=2),
+                                       dict(kind="dense", l=7), dict(kind="dense", l=5)])
+    layers = synth.make_weights(spec, mode, 100 + mode, small_layers=spec["layers"])
+    layers = [dict(L, wt=synth.numpy(L["wt"])) for L in layers]
+    imgs = synth.numpy(synth.images(4, 8, 8, 3, 30 + mode))
+    T = [-128.0, -100.0, -140.0]
+    net = orc.Net(8, 8, 3, mode, T if mode == 1 else None, layers)
+    logits, cls = net.forward(imgs)
+    ref = _torch_forward(imgs, mode, T, layers)
+    assert np.array_equal(logits, ref)
+    assert list(cls) == [int(np.argmax(r)) for r in ref]
+
+
+def test_forward_equals_layer_composition(orc):
+    """orc_forward == the per-layer oracle functions chained by hand (NONE mode included)."""
+    spec = dict(h=6, w=6, c=3, layers=[dict(kind="conv", k=3, c_out=5, pool=2), dict(kind="dense", l=4)])
+    layers = synth.make_weights(spec, -1, 7, small_layers=spec["layers"])
+    layers = [dict(L, wt=synth.numpy(L["wt"])) for L in layers]
+    img = synth.numpy(synth.images(1, 6, 6, 3, 8))[0].astype(np.float64)
+    net = orc.Net(6, 6, 3, orc.NONE, None, layers)
+    logits, cls = net.forward_one(img)
+    a = orc.conv_real(img, layers[0]["wt"])
+    b = orc.maxpool2(orc.binarize(a))
+    ref = orc.dense(b.reshape(-1), layers[1]["wt"])
+    assert np.array_equal(logits, ref) and cls == orc.argmax(ref)
+
+
+def test_conv_point_equals_full(orc):
+    x = synth.numpy(synth.pm1((7, 9, 5), 40))
+    wt = synth.numpy(synth.pm1((3, 5, 5, 5), 41))
+    acc = orc.conv_binary(x, wt)
+    for (y, xx, o) in [(0, 0, 0), (3, 4, 1), (6, 8, 2), (0, 8, 1), (6, 0, 0)]:
+        assert orc.conv_binary_point(x, wt[o], y, xx) == acc[y, xx, o]
