@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 binarized-CNN forward pass (arXiv 1808.00209) -- the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bnn|reference] [--batch B] [--mode rgb]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A "step" is one pass of the whole hot path (bnn_forward: pack -> conv1+pool -> conv2+pool -> FC1 ->
+FC2 -> FC3 + argmax) over one batch of B synthetic images per GPU (default B = 32768: the
+per-GPU shard of BASELINE config 5, 262144 images over 8 GPUs; weak scaling, B fixed per GPU),
+followed at N > 1 by the NCCL all-gather of the predictions.  Inputs are resident in HBM before
+the timed region; the 906 MB input per GPU is larger than the 126 MB L2, so no L2 flush is needed.
+
+Prints ONE JSON line (rank 0).  `value` = images/s of the whole job (all ranks), timed with CUDA
+events on the forward stream, max over ranks.  `e2e` = the same metric through bnn_forward_host
+(pinned host images -> host logits/classes, copies inside the timed region).  `roofline` = the
+dominant conv kernel's popcount rate (algorithmic popcounts / its CUDA-event time) against the
+POPC pipe peak (16 / clk / SM, measured by tools/probes/pipe_probe.cu) x 148 SMs x max SM clock.
+`cpu_baseline` = the CPU oracle (oracle/) on a bounded sample on the host cores (rank 0, N = 1).
+--impl reference times that oracle alone as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "images/sec at 1/2/4/8 B200; binary conv popc-pipe % and HBM GB/s (ncu)"
+POPC_PER_CLK_SM = 16  # measured on B200: profiles/pipe_probe_r01.txt
+MODES = {"rgb": 1, "gray": 2, "lbp": 3, "none": -1, "sign": 0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="bnn", choices=["bnn", "reference"])
+    ap.add_argument("--batch", type=int, default=32768, help="images per GPU per step")
+    ap.add_argument("--chunk", type=int, default=8192, help="bnn_net max_batch (images per internal chunk)")
+    ap.add_argument("--mode", default="rgb", choices=sorted(MODES))
+    ap.add_argument("--seed", type=int, default=2018)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--check", type=int, default=8, help="sampled images checked against the oracle after timing")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.file,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        rows = [ln.split(",") for ln in open(self.file.name).read().strip().splitlines() if ln.strip()]
+        os.unlink(self.file.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 7:
+                continue
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def conv_popc_per_image(spec, mode):
+    """Algorithmic popcounts per image and per conv layer: H*W*C_out*K^2*ceil(C_in/32),
+    dense patch (ceil(K^2 C_in / 32) words) for the first layer with C_in < 32."""
+    from paper_1808_00209_b200 import synth
+    h, w, c = spec["h"], spec["w"], synth.input_channels(spec["c"], mode)
+    out, macs = [], []
+    for L in spec["layers"]:
+        if L["kind"] == "conv":
+            k, co = L["k"], L["c_out"]
+            words = -(-k * k * c // 32) if c < 32 else k * k * (-(-c // 32))
+            out.append(h * w * co * words)
+            macs.append(h * w * co * k * k * c)
+            c = co
+            h //= L.get("pool", 1)
+            w //= L.get("pool", 1)
+        else:
+            d = h * w * c
+            out.append(L["l"] * (-(-d // 32)))
+            macs.append(L["l"] * d)
+            h, w, c = 1, 1, L["l"]
+    return out, macs
+
+
+def oracle_sample(spec, mode, seconds: float, threads: int, seed: int):
+    """Time the CPU oracle (as it stands) on about `seconds` of work: images/s and images done."""
+    import numpy as np
+    from oracle import oracle as orc
+    from paper_1808_00209_b200 import synth
+    layers = synth.make_weights(spec, mode, seed)
+    T = synth.thresholds(3, seed).numpy() if mode == 1 else (np.array([-127.0], np.float32) if mode == 2 else None)
+    om = {0: orc.SIGN, 1: orc.THRESH_RGB, 2: orc.THRESH_GRAY, 3: orc.LBP, -1: orc.NONE}[mode]
+    net = orc.Net(spec["h"], spec["w"], spec["c"], om, T, [dict(L, wt=L["wt"].numpy()) for L in layers])
+    imgs = synth.images(threads, spec["h"], spec["w"], spec["c"], seed + 1).numpy()
+    done, t0 = 0, time.perf_counter()
+    while True:
+        net.forward(imgs, threads=threads)
+        done += threads
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return done / el, done, el
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------------- reference arm
+def run_reference(a, rank, world):
+    """The reference arm: the CPU oracle on the host cores, same metric/config, each step a bounded
+    sample (one image per core).  Under torchrun only rank 0 works."""
+    if rank != 0:
+        return
+    from paper_1808_00209_b200 import synth
+    spec = synth.VEHICLE
+    mode = MODES[a.mode]
+    cores = host_cores()
+    for _ in range(a.warmup):
+        oracle_sample(spec, mode, 0.0, cores, a.seed)
+    t0 = time.perf_counter()
+    n = 0
+    for _ in range(a.steps):
+        _, d, _ = oracle_sample(spec, mode, 0.0, cores, a.seed)
+        n += d
+    el = time.perf_counter() - t0
+    v = n / el
+    line = {"metric": METRIC, "value": v, "unit": "images/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": el * 1e3 / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "i64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "vehicle classifier (PAPER.md Table 2), %s input binarization; oracle sample of %d "
+                                   "images per step (one per host core)" % (a.mode, cores), "batch_per_step": cores},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle",
+                             "sample": "%d steps x %d images (vehicle net, %s)" % (a.steps, cores, a.mode)},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------- bnn arm
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1808_00209_b200 as bnn
+    from paper_1808_00209_b200 import synth
+
+    assert torch.cuda.is_available(), "bench.py needs a GPU (the CUDA path has no CPU fallback)"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    spec = synth.VEHICLE
+    mode = MODES[a.mode]
+    B = a.batch
+
+    # weights: identical on every rank (same seed), packed on the device by bnn_pack(SIGN)
+    layers = synth.make_weights(spec, mode, a.seed)
+    dl = [dict(L, wt=bnn.pack_weights(L["wt"].to(dev))) for L in layers]
+    T = None
+    if mode == 1:
+        T = synth.thresholds(3, a.seed).to(dev)
+    elif mode == 2:
+        T = torch.tensor([-127.0], device=dev)
+    net = bnn.Net(spec["h"], spec["w"], spec["c"], bnn.U8, mode, T, dl, max_batch=min(a.chunk, B))
+    images = synth.images_chunked(rank * B, B, spec["h"], spec["w"], spec["c"], a.seed + 1, device=dev)
+    L = spec["layers"][-1]["l"]
+    logits = torch.empty((B, L), dtype=torch.int32, device=dev)
+    cls = torch.empty((B,), dtype=torch.int32, device=dev)
+    if world > 1:
+        logits_all = torch.empty((world * B, L), dtype=torch.int32, device=dev)
+        cls_all = torch.empty((world * B,), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        net.forward(images, logits, cls)
+        if world > 1:
+            dist.all_gather_into_tensor(logits_all, logits)
+            dist.all_gather_into_tensor(cls_all, cls)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    net.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    stage_ms, stage_launch = net.profile_read()
+    net.profile(False)
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * B / (ms * 1e-3)
+
+    # ---- roofline of the dominant conv kernel (live CUDA-event times of its launches)
+    popc_img, mac_img = conv_popc_per_image(spec, mode)
+    conv_stages = [i for i, Ly in enumerate(spec["layers"]) if Ly["kind"] == "conv"]
+    dom = max(conv_stages, key=lambda i: stage_ms[i + 1])
+    dom_ms_per_launch = stage_ms[dom + 1] / max(1, stage_launch[dom + 1])
+    imgs_per_launch = B * a.steps / max(1, stage_launch[dom + 1])
+    achieved = popc_img[dom] * imgs_per_launch / (dom_ms_per_launch * 1e-3)
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    peak = POPC_PER_CLK_SM * torch.cuda.get_device_properties(dev).multi_processor_count * sm_max * 1e6
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            k = "layer%d" % dom
+            if k in tj:
+                traffic = tj[k]["dram_bytes_per_launch"] * (imgs_per_launch / tj[k]["images_per_launch"])
+        except (ValueError, KeyError):
+            traffic = None
+    step_ms_total = sum(stage_ms) / a.steps
+    roofline = {"bound": "alu", "pipe": "POPC (16/clk/SM, measured)", "kernel": "layer%d conv (%s)" % (
+        dom, "dense-patch" if dom == 0 else "conv_bin_kernel"), "achieved": achieved / 1e12, "peak": peak / 1e12,
+        "unit": "Tpopc/s", "frac": achieved / peak, "traffic": traffic,
+        "peak_basis": "16 POPC/clk/SM x %d SMs x %.0f MHz (sm max clock)" % (
+            torch.cuda.get_device_properties(dev).multi_processor_count, sm_max),
+        "kernel_share_of_step": stage_ms[dom + 1] / a.steps / step_ms_total if step_ms_total else None,
+        "ms_per_launch": dom_ms_per_launch, "images_per_launch": imgs_per_launch}
+    stages = {("pack" if i == 0 else ("layer%d" % (i - 1) if i <= len(spec["layers"]) else "argmax")):
+              round(stage_ms[i] / a.steps, 4) for i in range(len(stage_ms)) if stage_launch[i]}
+
+    # ---- end to end through bnn_forward_host (pinned host in, host out)
+    e2e = None
+    if not a.no_e2e:
+        h_images = torch.empty(images.shape, dtype=torch.uint8, pin_memory=True)
+        h_images.copy_(images)
+        h_logits = torch.empty((B, L), dtype=torch.int32, pin_memory=True)
+        h_cls = torch.empty((B,), dtype=torch.int32, pin_memory=True)
+        ke = max(3, min(a.steps, 10))
+        net.forward_host(h_images, h_logits, h_cls)  # warm the staging buffers
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            net.forward_host(h_images, h_logits, h_cls)
+        el = (time.perf_counter() - t0) / ke
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        assert torch.equal(h_cls, cls.cpu()), "forward_host disagrees with forward"
+        e2e = {"value": world * B / el, "unit": "images/s", "h2d_bytes_per_step": int(h_images.numel()),
+               "d2h_bytes_per_step": int(h_logits.numel() * 4 + h_cls.numel() * 4), "steps": ke,
+               "timing": "wall clock around the synchronous C-ABI call, max over ranks"}
+
+    # ---- sampled parity against the oracle at this size (not timed)
+    parity = None
+    if a.check > 0 and rank == 0:
+        import numpy as np
+        from oracle import oracle as orc
+        idx = np.linspace(0, B - 1, a.check).astype(int)
+        om = {0: orc.SIGN, 1: orc.THRESH_RGB, 2: orc.THRESH_GRAY, 3: orc.LBP, -1: orc.NONE}[mode]
+        onet = orc.Net(spec["h"], spec["w"], spec["c"], om, None if T is None else T.cpu().numpy(),
+                       [dict(Ly, wt=Ly["wt"].numpy()) for Ly in layers])
+        ref_l, ref_c = onet.forward(images[idx].cpu().numpy(), threads=min(len(idx), host_cores()))
+        ok = bool(np.array_equal(logits[idx].cpu().numpy(), ref_l) and np.array_equal(cls[idx].cpu().numpy(), ref_c))
+        parity = {"images_checked": int(len(idx)), "bit_exact": ok}
+        assert ok, "sampled parity against the oracle FAILED"
+
+    cpu = None
+    if not a.no_cpu and rank == 0 and world == 1:
+        cores = host_cores()
+        v, done, el = oracle_sample(spec, mode, 12.0, cores, a.seed)
+        cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle",
+               "sample": "%d vehicle images (%s), %.1f s on %d threads, one image per thread" % (done, a.mode, el, cores)}
+
+    launches = bnn.forward_launches(net, B) * a.steps
+    tot_mac = sum(mac_img) * B * world
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic",
+            "config": {"workload": "vehicle classifier (PAPER.md Table 2: conv32x5x5+pool, conv32x5x5+pool, FC100, "
+                                   "FC100, FC4), %s input binarization, %d images per GPU per step (config 5 shard: "
+                                   "262144 over 8 GPUs)" % (a.mode, B), "batch_per_gpu": B, "global_batch": B * world,
+                       "chunk": min(a.chunk, B), "input": "u8 96x96x3 uniform, resident in HBM",
+                       "l2": "inputs (%d MB/GPU) larger than L2; no flush" % (B * 27648 // 2 ** 20),
+                       "parallelism": "dp%d (NCCL all-gather of predictions)" % world},
+            "binary_mac_per_s": tot_mac / (ms * 1e-3), "stage_ms_per_step": stages,
+            "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+            "parity": parity}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    net.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -69,6 +69,10 @@ def lib():
         L.bnn_forward_host.restype = i
         L.bnn_forward_launches.argtypes = [vp, i]
         L.bnn_forward_launches.restype = i
+        L.bnn_net_profile.argtypes = [vp, i]
+        L.bnn_net_profile.restype = i
+        L.bnn_net_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), i]
+        L.bnn_net_profile_read.restype = i
         L.bnn_net_destroy.argtypes = [vp]
         L.bnn_net_destroy.restype = None
         _lib = L
@@ -191,6 +195,7 @@ class Net:
         _check(lib().bnn_net_create(h, w, c, in_dtype, mode, _ptr(T), arr, len(layers), max_batch, ctypes.byref(h_)),
                "bnn_net_create")
         self.handle = h_
+        self._n_layers = len(layers)
         self.h, self.w, self.c, self.in_dtype = h, w, c, in_dtype
         self.n_classes = layers[-1]["l"]
         self.device = layers[0]["wt"].device
@@ -221,6 +226,27 @@ class Net:
         _check(lib().bnn_forward_host(self.handle, _ptr(images), n, _ptr(logits), _ptr(cls), _stream(stream)),
                "bnn_forward_host")
         return logits, cls
+
+    def profile(self, enable: bool = True) -> int:
+        """bnn_net_profile: reset and start (or stop) per-stage event timing."""
+        r = lib().bnn_net_profile(self.handle, 1 if enable else 0)
+        if r < 0:
+            _check(-r, "bnn_net_profile")
+        return r
+
+    def profile_read(self):
+        """bnn_net_profile_read -> (ms per stage, launches per stage); stage 0 = pack,
+        i + 1 = layer i, last = argmax."""
+        ns = self.profile_read_count()
+        ms = (ctypes.c_double * ns)()
+        cnt = (ctypes.c_int64 * ns)()
+        r = lib().bnn_net_profile_read(self.handle, ms, cnt, ns)
+        if r < 0:
+            _check(-r, "bnn_net_profile_read")
+        return list(ms), list(cnt)
+
+    def profile_read_count(self) -> int:
+        return self._n_layers + 2
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:

@@ -1,0 +1,665 @@
+// bnn_api.cu -- the C ABI of libbnn.so (include/bnn.h): validation, kernel dispatch and the
+// whole-network orchestration (bnn_net / bnn_forward / bnn_forward_host).
+// Every entry validates before launching, never throws, and reports through bnn_status +
+// the thread-local bnn_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bnn.h"
+#include "k_conv.cuh"
+#include "k_dense.cuh"
+#include "k_pack.cuh"
+
+using namespace bnn;
+
+namespace {
+
+thread_local std::string g_err;
+
+bnn_status fail(bnn_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+bnn_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BNN_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return BNN_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+#define BNN_REQUIRE_ALIGNED(p, name) \
+  do { if ((p) != nullptr && !aligned16(p)) return fail(BNN_E_ALIGN, "%s: pointer not 16-byte aligned", name); } while (0)
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// tuning / test knobs (bnn_set_option)
+int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap conv
+int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
+
+int grid_for(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (int)std::max<int64_t>(1, std::min(b, cap));
+}
+
+int choose_tpc(int64_t total_tiles, bool restage_per_tile) {
+  if (g_opt_tiles_per_cta > 0) return g_opt_tiles_per_cta;
+  if (restage_per_tile) return 1;
+  int64_t target = (int64_t)num_sms() * 8;
+  int64_t tpc = (total_tiles + target - 1) / target;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tpc, 32));
+}
+
+// ---------------------------------------------------------------------------- pack
+bnn_status launch_pack(const void* x, bnn_dtype dt, int n, int h, int w, int c, int mode, const float* T,
+                       uint32_t* y, cudaStream_t s) {
+  const int64_t npix = (int64_t)n * h * w;
+  if (npix == 0) return BNN_OK;
+  if (mode == BNN_THRESH_GRAY || mode == BNN_LBP) {
+    pack_luma_kernel<<<grid_for(npix, 256), 256, 0, s>>>((const uint8_t*)x, n, h, w, mode, T, y);
+    return check_launch("pack_luma_kernel");
+  }
+  if (dt == BNN_U8 && c == 3) {
+    pack_u8c3_kernel<<<grid_for(npix / 4 + 1, 256), 256, 0, s>>>((const uint8_t*)x, npix, mode, T, y);
+    return check_launch("pack_u8c3_kernel");
+  }
+  const int cw = (c + 31) / 32;
+  const int grid = grid_for(npix * cw, 256);
+  switch (dt) {
+    case BNN_U8: pack_generic_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)x, npix, c, cw, mode, T, y); break;
+    case BNN_I8: pack_generic_kernel<int8_t><<<grid, 256, 0, s>>>((const int8_t*)x, npix, c, cw, mode, T, y); break;
+    case BNN_F32: pack_generic_kernel<float><<<grid, 256, 0, s>>>((const float*)x, npix, c, cw, mode, T, y); break;
+    case BNN_I32: pack_generic_kernel<int32_t><<<grid, 256, 0, s>>>((const int32_t*)x, npix, c, cw, mode, T, y); break;
+    default: return fail(BNN_E_ARG, "bnn_pack: bad dtype");
+  }
+  return check_launch("pack_generic_kernel");
+}
+
+// ---------------------------------------------------------------------------- conv
+template <int K, int WY, int WX>
+bnn_status launch_conv_bin_t(ConvArgs A, cudaStream_t s) {
+  constexpr int PR = 2, PC = 8;
+  constexpr int CWC = (K >= 7) ? 4 : 8;
+  constexpr int TH = WY * PR, TW = WX * PC;
+  A.tiles_y = (A.H + TH - 1) / TH;
+  A.tiles_x = (A.W + TW - 1) / TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = choose_tpc(A.total_tiles, A.cw > CWC);
+  const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
+  if (gx > 0x7fffffff) return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: too many tiles");
+  dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
+  conv_bin_kernel<K, PR, PC, WY, WX, CWC><<<grid, WY * WX * 32, 0, s>>>(A);
+  return check_launch("conv_bin_kernel");
+}
+
+template <int K, int WY, int WX>
+bnn_status launch_conv_patch_t(ConvArgs A, cudaStream_t s) {
+  constexpr int PR = 2, PC = 8;
+  constexpr int TH = WY * PR, TW = WX * PC;
+  A.tiles_y = (A.H + TH - 1) / TH;
+  A.tiles_x = (A.W + TW - 1) / TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = choose_tpc(A.total_tiles, false);
+  const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
+  dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
+  conv_patch_kernel<K, PR, PC, WY, WX><<<grid, WY * WX * 32, 0, s>>>(A);
+  return check_launch("conv_patch_kernel");
+}
+
+template <int K, int WY, int WX>
+bnn_status launch_conv_real_u8_t(RealConvArgs A, cudaStream_t s) {
+  constexpr int PR = 2, PC = 8;
+  constexpr int TH = WY * PR, TW = WX * PC;
+  constexpr int IR = TH + K - 1, IC = TW + K - 1;
+  A.tiles_y = (A.H + TH - 1) / TH;
+  A.tiles_x = (A.W + TW - 1) / TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = choose_tpc(A.total_tiles, false);
+  const int nb = K * K * A.c_in, nw = (nb + 3) / 4;
+  const size_t in_bytes = (size_t)((IR * IC * A.c_in + 15) & ~15);
+  const size_t smem = in_bytes + (size_t)nw * TH * TW * 4 + (size_t)nw * 32 * 4;
+  if (smem > 200 * 1024) return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: real first layer k=%d c_in=%d too large", K, A.c_in);
+  auto kfn = conv_real_u8_kernel<K, PR, PC, WY, WX>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
+  dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
+  kfn<<<grid, WY * WX * 32, smem, s>>>(A);
+  return check_launch("conv_real_u8_kernel");
+}
+
+template <int WY, int WX>
+bnn_status dispatch_conv_bin(int k, const ConvArgs& A, bool patch, cudaStream_t s) {
+  if (patch) {
+    switch (k) {
+      case 1: return launch_conv_patch_t<1, WY, WX>(A, s);
+      case 3: return launch_conv_patch_t<3, WY, WX>(A, s);
+      case 5: return launch_conv_patch_t<5, WY, WX>(A, s);
+      case 7: return launch_conv_patch_t<7, WY, WX>(A, s);
+    }
+  } else {
+    switch (k) {
+      case 1: return launch_conv_bin_t<1, WY, WX>(A, s);
+      case 3: return launch_conv_bin_t<3, WY, WX>(A, s);
+      case 5: return launch_conv_bin_t<5, WY, WX>(A, s);
+      case 7: return launch_conv_bin_t<7, WY, WX>(A, s);
+    }
+  }
+  return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: k=%d not supported (1, 3, 5, 7)", k);
+}
+
+template <int WY, int WX>
+bnn_status dispatch_conv_real_u8(int k, const RealConvArgs& A, cudaStream_t s) {
+  switch (k) {
+    case 1: return launch_conv_real_u8_t<1, WY, WX>(A, s);
+    case 3: return launch_conv_real_u8_t<3, WY, WX>(A, s);
+    case 5: return launch_conv_real_u8_t<5, WY, WX>(A, s);
+    case 7: return launch_conv_real_u8_t<7, WY, WX>(A, s);
+  }
+  return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: k=%d not supported (1, 3, 5, 7)", k);
+}
+
+// Is the dense-patch first-layer kernel applicable?  (few input channels, one word/pixel)
+bool use_patch(int c_in, int k) {
+  return g_opt_conv_algo == 0 && c_in < 32 && k > 1 && k * k * c_in <= 256;
+}
+
+bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c_in, const uint32_t* wt, int c_out,
+                       int k, const int32_t* thr, const uint8_t* flip, int pool, uint32_t* y, void* acc,
+                       cudaStream_t s) {
+  if ((int64_t)n * h * w == 0) return BNN_OK;
+  const bool small = (w <= 8 || h <= 8);
+  if (x_dt == BNN_BITS) {
+    ConvArgs A{};
+    A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
+    A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
+    A.cwo = (c_out + 31) / 32; A.pool = pool;
+    const bool patch = use_patch(c_in, k);
+    return small ? dispatch_conv_bin<4, 1>(k, A, patch, s) : dispatch_conv_bin<4, 2>(k, A, patch, s);
+  }
+  RealConvArgs A{};
+  A.x = x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = acc;
+  A.n = n; A.H = h; A.W = w; A.c_in = c_in; A.c_out = c_out; A.cwo = (c_out + 31) / 32; A.pool = pool;
+  if (x_dt == BNN_U8) return small ? dispatch_conv_real_u8<4, 1>(k, A, s) : dispatch_conv_real_u8<4, 2>(k, A, s);
+  // f32
+  const int64_t work = (int64_t)n * (h / pool) * (w / pool) * A.cwo * 32;
+  conv_real_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(A, k);
+  return check_launch("conv_real_f32_kernel");
+}
+
+// ---------------------------------------------------------------------------- dense
+bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,
+                        const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, cudaStream_t s) {
+  if (n == 0) return BNN_OK;
+  DenseArgs A{};
+  A.x = x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = acc;
+  A.cls = (l <= 32) ? cls : nullptr;
+  A.n = n; A.l = l; A.lw = (l + 31) / 32; A.d = d; A.dw = (d + 31) / 32;
+  constexpr int PI = 8, NWARP = 8, DC = 64;
+  dim3 grid((unsigned)((n + PI * NWARP - 1) / (PI * NWARP)), (unsigned)A.lw);
+  dense_kernel<PI, NWARP, DC><<<grid, NWARP * 32, 0, s>>>(A);
+  bnn_status st = check_launch("dense_kernel");
+  if (st != BNN_OK) return st;
+  if (cls != nullptr && l > 32) {
+    argmax_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, s>>>(acc, n, l, cls);
+    return check_launch("argmax_kernel");
+  }
+  return BNN_OK;
+}
+
+}  // namespace
+
+// =============================================================================== public ABI
+extern "C" {
+
+const char* bnn_last_error(void) { return g_err.c_str(); }
+
+int bnn_version(void) { return 100; }
+
+int bnn_set_option(const char* key, int value) {
+  if (key == nullptr) return (int)fail(BNN_E_ARG, "bnn_set_option: null key");
+  if (strcmp(key, "conv_algo") == 0) { g_opt_conv_algo = value; return BNN_OK; }
+  if (strcmp(key, "tiles_per_cta") == 0) { g_opt_tiles_per_cta = value; return BNN_OK; }
+  return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
+}
+
+bnn_status bnn_pack(const void* x, bnn_dtype dt, int n, int h, int w, int c, int mode, const float* T, uint32_t* y,
+                    bnn_stream_t stream) {
+  if (n < 0 || h < 0 || w < 0 || c < 1) return fail(BNN_E_ARG, "bnn_pack: bad sizes n=%d h=%d w=%d c=%d", n, h, w, c);
+  if ((int64_t)n * h * w > 0 && (x == nullptr || y == nullptr)) return fail(BNN_E_ARG, "bnn_pack: null pointer");
+  if (dt != BNN_U8 && dt != BNN_I8 && dt != BNN_F32 && dt != BNN_I32) return fail(BNN_E_ARG, "bnn_pack: bad dtype %d", (int)dt);
+  if (mode < BNN_SIGN || mode > BNN_LBP) return fail(BNN_E_ARG, "bnn_pack: bad mode %d", mode);
+  if ((mode == BNN_THRESH_RGB || mode == BNN_THRESH_GRAY) && T == nullptr)
+    return fail(BNN_E_ARG, "bnn_pack: threshold mode needs T");
+  if ((mode == BNN_THRESH_GRAY || mode == BNN_LBP) && (c != 3 || dt != BNN_U8))
+    return fail(BNN_E_CONFIG, "bnn_pack: GRAY/LBP need u8 input with c == 3");
+  BNN_REQUIRE_ALIGNED(x, "bnn_pack x");
+  BNN_REQUIRE_ALIGNED(y, "bnn_pack y");
+  return launch_pack(x, dt, n, h, w, c, mode, T, y, (cudaStream_t)stream);
+}
+
+bnn_status bnn_conv2d(const void* x, bnn_dtype x_dt, int n, int h, int w, int c_in, const uint32_t* wt, int c_out,
+                      int k, const int32_t* thr, const uint8_t* flip, int pool, uint32_t* y, void* acc,
+                      bnn_stream_t stream) {
+  if (n < 0 || h < 0 || w < 0 || c_in < 1 || c_out < 1) return fail(BNN_E_ARG, "bnn_conv2d: bad sizes");
+  if (k != 1 && k != 3 && k != 5 && k != 7) return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: k=%d not in {1,3,5,7}", k);
+  if (pool != 1 && pool != 2) return fail(BNN_E_ARG, "bnn_conv2d: pool must be 1 or 2");
+  if (pool == 2 && ((h & 1) || (w & 1))) return fail(BNN_E_SHAPE, "bnn_conv2d: pool 2 needs even h, w (got %d x %d)", h, w);
+  if (x_dt != BNN_BITS && x_dt != BNN_U8 && x_dt != BNN_F32) return fail(BNN_E_CONFIG, "bnn_conv2d: x dtype must be BITS, U8 or F32");
+  if (x_dt != BNN_BITS && c_in > 32) return fail(BNN_E_CONFIG, "bnn_conv2d: real first layer needs c_in <= 32");
+  if ((int64_t)n * h * w > 0 && y == nullptr && acc == nullptr) return fail(BNN_E_ARG, "bnn_conv2d: y and acc both null");
+  if ((int64_t)n * h * w > 0 && (x == nullptr || wt == nullptr)) return fail(BNN_E_ARG, "bnn_conv2d: null pointer");
+  BNN_REQUIRE_ALIGNED(x, "bnn_conv2d x");
+  BNN_REQUIRE_ALIGNED(wt, "bnn_conv2d wt");
+  BNN_REQUIRE_ALIGNED(y, "bnn_conv2d y");
+  BNN_REQUIRE_ALIGNED(acc, "bnn_conv2d acc");
+  return launch_conv(x, x_dt, n, h, w, c_in, wt, c_out, k, thr, flip, pool, y, acc, (cudaStream_t)stream);
+}
+
+bnn_status bnn_maxpool(const uint32_t* x, int n, int h, int w, int c, uint32_t* y, bnn_stream_t stream) {
+  if (n < 0 || h < 0 || w < 0 || c < 1) return fail(BNN_E_ARG, "bnn_maxpool: bad sizes");
+  if ((h & 1) || (w & 1)) return fail(BNN_E_SHAPE, "bnn_maxpool: h, w must be even (got %d x %d)", h, w);
+  if ((int64_t)n * h * w > 0 && (x == nullptr || y == nullptr)) return fail(BNN_E_ARG, "bnn_maxpool: null pointer");
+  BNN_REQUIRE_ALIGNED(x, "bnn_maxpool x");
+  BNN_REQUIRE_ALIGNED(y, "bnn_maxpool y");
+  const int cw = (c + 31) / 32;
+  const int64_t total = (int64_t)n * (h / 2) * (w / 2) * cw;
+  if (total == 0) return BNN_OK;
+  maxpool_or_kernel<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(x, n, h, w, cw, y);
+  return check_launch("maxpool_or_kernel");
+}
+
+bnn_status bnn_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,
+                     const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, bnn_stream_t stream) {
+  if (n < 0 || d < 1 || l < 1) return fail(BNN_E_ARG, "bnn_dense: bad sizes");
+  if (n > 0 && (x == nullptr || wt == nullptr)) return fail(BNN_E_ARG, "bnn_dense: null pointer");
+  if (n > 0 && y == nullptr && acc == nullptr && cls == nullptr) return fail(BNN_E_ARG, "bnn_dense: no output");
+  if (cls != nullptr && l > 32 && acc == nullptr) return fail(BNN_E_ARG, "bnn_dense: cls with l > 32 needs acc");
+  if ((d + 31) / 32 > 0x7fffffffLL) return fail(BNN_E_ARG, "bnn_dense: d too large");
+  BNN_REQUIRE_ALIGNED(x, "bnn_dense x");
+  BNN_REQUIRE_ALIGNED(wt, "bnn_dense wt");
+  BNN_REQUIRE_ALIGNED(y, "bnn_dense y");
+  BNN_REQUIRE_ALIGNED(acc, "bnn_dense acc");
+  BNN_REQUIRE_ALIGNED(cls, "bnn_dense cls");
+  return launch_dense(x, n, d, wt, l, thr, flip, y, acc, cls, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+// =============================================================================== network
+struct LayerPlan {
+  int kind, k, c_in, c_out, pool, l;
+  int H, W;          // input spatial dims (conv)
+  int64_t d;         // dense input length
+  bnn_dtype x_dt;    // conv input dtype (BITS, or U8/F32 for a real first layer)
+  const uint32_t* wt;
+  const int32_t* thr;
+  const uint8_t* flip;
+  int64_t out_words_per_img;  // packed output words per image (hidden layers)
+};
+
+struct bnn_net {
+  int h, w, c;
+  bnn_dtype in_dt;
+  int mode;
+  const float* T;
+  int c0;  // channels after input binarization
+  std::vector<LayerPlan> L;
+  int chunk;
+  int64_t img_bytes;
+  int64_t packed_in_words;  // per image
+  int64_t buf_words;        // per image, max over hidden layers
+  uint32_t* packed_in = nullptr;
+  uint32_t* buf[2] = {nullptr, nullptr};
+  int32_t* logits_tmp = nullptr;
+  // host-pipeline resources (lazy)
+  int hchunk = 0;
+  void* d_in[2] = {nullptr, nullptr};
+  int32_t* d_logits[2] = {nullptr, nullptr};
+  int32_t* d_cls[2] = {nullptr, nullptr};
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  // per-stage profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> pending_stage;  // stage of event pair i (events 2i, 2i+1 of the pool)
+  std::vector<double> stage_ms;
+  std::vector<int64_t> stage_launches;
+};
+
+namespace {
+
+void net_free(bnn_net* net) {
+  if (!net) return;
+  cudaFree(net->packed_in);
+  cudaFree(net->buf[0]);
+  cudaFree(net->buf[1]);
+  cudaFree(net->logits_tmp);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(net->d_in[i]);
+    cudaFree(net->d_logits[i]);
+    cudaFree(net->d_cls[i]);
+    if (net->ev_h2d[i]) cudaEventDestroy(net->ev_h2d[i]);
+    if (net->ev_comp[i]) cudaEventDestroy(net->ev_comp[i]);
+    if (net->ev_d2h[i]) cudaEventDestroy(net->ev_d2h[i]);
+  }
+  for (cudaEvent_t e : net->ev_pool) cudaEventDestroy(e);
+  if (net->h2d) cudaStreamDestroy(net->h2d);
+  if (net->d2h) cudaStreamDestroy(net->d2h);
+  delete net;
+}
+
+bnn_status check_pad_bits(const uint32_t* dev, int64_t rows, int64_t words_per_row, int valid_bits_last,
+                          const char* what, int layer) {
+  if (valid_bits_last == 32) return BNN_OK;
+  std::vector<uint32_t> h((size_t)(rows * words_per_row));
+  cudaError_t e = cudaMemcpy(h.data(), dev, h.size() * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_net_create: reading %s of layer %d: %s", what, layer, cudaGetErrorString(e));
+  const uint32_t mask = (valid_bits_last == 0) ? 0u : (0xffffffffu >> valid_bits_last);
+  for (int64_t r = 0; r < rows; ++r)
+    if (h[(size_t)(r * words_per_row + words_per_row - 1)] & mask)
+      return fail(BNN_E_PADBITS, "bnn_net_create: layer %d %s row %lld has nonzero pad bits", layer, what, (long long)r);
+  return BNN_OK;
+}
+
+// Returns the start event of a new (start, end) pair for `stage`, recorded on s; or null.
+struct ProfScope {
+  bnn_net* net;
+  cudaStream_t s;
+  cudaEvent_t end = nullptr;
+  ProfScope(bnn_net* n, int stage, cudaStream_t st) : net(n), s(st) {
+    if (!net->prof) return;
+    if (net->ev_used + 2 > net->ev_pool.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) { net->prof = false; return; }
+        net->ev_pool.push_back(e);
+      }
+    }
+    cudaEvent_t b = net->ev_pool[net->ev_used];
+    end = net->ev_pool[net->ev_used + 1];
+    net->ev_used += 2;
+    net->pending_stage.push_back(stage);
+    cudaEventRecord(b, s);
+  }
+  ~ProfScope() {
+    if (end) cudaEventRecord(end, s);
+  }
+};
+
+bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
+  const void* cur = images;
+  bnn_dtype cur_dt = net->in_dt;
+  if (net->mode != BNN_MODE_NONE) {
+    ProfScope ps(net, 0, s);
+    bnn_status st = launch_pack(images, net->in_dt, nb, net->h, net->w, net->c, net->mode, net->T, net->packed_in, s);
+    if (st != BNN_OK) return st;
+    cur = net->packed_in;
+    cur_dt = BNN_BITS;
+  }
+  const int nl = (int)net->L.size();
+  for (int i = 0; i < nl; ++i) {
+    const LayerPlan& P = net->L[i];
+    const bool last = (i == nl - 1);
+    bnn_status st;
+    ProfScope ps(net, i + 1, s);
+    if (P.kind == 1) {
+      uint32_t* out = net->buf[i & 1];
+      st = launch_conv(cur, cur_dt, nb, P.H, P.W, P.c_in, P.wt, P.c_out, P.k, P.thr, P.flip, P.pool, out, nullptr, s);
+      cur = out;
+      cur_dt = BNN_BITS;
+    } else if (!last) {
+      uint32_t* out = net->buf[i & 1];
+      st = launch_dense((const uint32_t*)cur, nb, P.d, P.wt, P.l, P.thr, P.flip, out, nullptr, nullptr, s);
+      cur = out;
+    } else {
+      int32_t* lg = logits ? logits : net->logits_tmp;
+      st = launch_dense((const uint32_t*)cur, nb, P.d, P.wt, P.l, nullptr, nullptr, nullptr, lg,
+                        P.l <= 32 ? cls : nullptr, s);
+      if (st == BNN_OK && cls != nullptr && P.l > 32) {
+        ProfScope pa(net, nl + 1, s);
+        argmax_kernel<<<grid_for((int64_t)nb * 32, 256), 256, 0, s>>>(lg, nb, P.l, cls);
+        st = check_launch("argmax_kernel");
+      }
+    }
+    if (st != BNN_OK) return st;
+  }
+  return BNN_OK;
+}
+
+int launches_per_chunk(const bnn_net* net, bool want_cls) {
+  int n = (net->mode != BNN_MODE_NONE ? 1 : 0) + (int)net->L.size();
+  if (want_cls && net->L.back().l > 32) n += 1;
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const float* T, const bnn_layer* layers,
+                          int n_layers, int max_batch, bnn_net** out) {
+  if (out == nullptr) return fail(BNN_E_ARG, "bnn_net_create: out is null");
+  *out = nullptr;
+  if (h < 1 || w < 1 || c < 1 || n_layers < 1 || layers == nullptr) return fail(BNN_E_ARG, "bnn_net_create: bad sizes");
+  if (max_batch < 1 || max_batch > 65536) return fail(BNN_E_ARG, "bnn_net_create: max_batch must be in [1, 65536]");
+  if (in_dt != BNN_U8 && in_dt != BNN_F32) return fail(BNN_E_CONFIG, "bnn_net_create: input dtype must be U8 or F32");
+  if (mode < BNN_MODE_NONE || mode > BNN_LBP) return fail(BNN_E_ARG, "bnn_net_create: bad mode %d", mode);
+  if ((mode == BNN_THRESH_RGB || mode == BNN_THRESH_GRAY) && T == nullptr) return fail(BNN_E_ARG, "bnn_net_create: mode needs T");
+  if ((mode == BNN_THRESH_GRAY || mode == BNN_LBP) && (c != 3 || in_dt != BNN_U8))
+    return fail(BNN_E_CONFIG, "bnn_net_create: GRAY/LBP need u8 input with 3 channels");
+  if (layers[n_layers - 1].kind != 2) return fail(BNN_E_CONFIG, "bnn_net_create: the last layer must be dense");
+
+  bnn_net* net = new (std::nothrow) bnn_net();
+  if (!net) return fail(BNN_E_NOMEM, "bnn_net_create: out of host memory");
+  net->h = h; net->w = w; net->c = c; net->in_dt = in_dt; net->mode = mode; net->T = T;
+  net->img_bytes = (int64_t)h * w * c * (in_dt == BNN_U8 ? 1 : 4);
+  net->c0 = (mode == BNN_THRESH_GRAY) ? 1 : (mode == BNN_LBP ? 3 : c);
+  net->packed_in_words = (mode == BNN_MODE_NONE) ? 0 : (int64_t)h * w * ((net->c0 + 31) / 32);
+  int H = h, W = w, C = net->c0;
+  int64_t D = -1;  // >= 0 once in the dense part
+  net->buf_words = 1;
+  for (int i = 0; i < n_layers; ++i) {
+    const bnn_layer& Ls = layers[i];
+    LayerPlan P{};
+    P.kind = Ls.kind; P.k = Ls.k; P.c_out = Ls.c_out; P.pool = Ls.pool; P.l = Ls.l;
+    P.wt = Ls.wt; P.thr = Ls.thr; P.flip = Ls.flip;
+    if (Ls.wt == nullptr) { net_free(net); return fail(BNN_E_ARG, "bnn_net_create: layer %d has no weights", i); }
+    if (!aligned16(Ls.wt)) { net_free(net); return fail(BNN_E_ALIGN, "bnn_net_create: layer %d weights not 16-byte aligned", i); }
+    if (Ls.kind == 1) {
+      if (D >= 0) { net_free(net); return fail(BNN_E_SHAPE, "bnn_net_create: conv layer %d after a dense layer", i); }
+      if (Ls.k != 1 && Ls.k != 3 && Ls.k != 5 && Ls.k != 7) { net_free(net); return fail(BNN_E_UNSUPPORTED, "bnn_net_create: layer %d k=%d", i, Ls.k); }
+      if (Ls.c_out < 1 || (Ls.pool != 1 && Ls.pool != 2)) { net_free(net); return fail(BNN_E_ARG, "bnn_net_create: layer %d bad c_out/pool", i); }
+      if (Ls.pool == 2 && ((H & 1) || (W & 1))) { net_free(net); return fail(BNN_E_SHAPE, "bnn_net_create: layer %d pools an odd map %dx%d", i, H, W); }
+      P.c_in = C; P.H = H; P.W = W;
+      P.x_dt = (i == 0 && mode == BNN_MODE_NONE) ? in_dt : BNN_BITS;
+      if (P.x_dt != BNN_BITS && C > 32) { net_free(net); return fail(BNN_E_CONFIG, "bnn_net_create: real first layer needs c <= 32"); }
+      const int cw = (C + 31) / 32;
+      bnn_status st = check_pad_bits(Ls.wt, (int64_t)Ls.c_out * Ls.k * Ls.k, cw, C % 32 == 0 ? 32 : C % 32, "weights", i);
+      if (st != BNN_OK) { net_free(net); return st; }
+      H /= Ls.pool; W /= Ls.pool; C = Ls.c_out;
+      P.out_words_per_img = (int64_t)H * W * ((C + 31) / 32);
+      net->buf_words = std::max(net->buf_words, P.out_words_per_img);
+    } else if (Ls.kind == 2) {
+      if (i == 0 && mode == BNN_MODE_NONE) { net_free(net); return fail(BNN_E_CONFIG, "bnn_net_create: mode NONE needs a conv first layer"); }
+      if (Ls.l < 1) { net_free(net); return fail(BNN_E_ARG, "bnn_net_create: layer %d l < 1", i); }
+      if (D < 0) {
+        if (C % 32 != 0 && (int64_t)H * W != 1) {
+          net_free(net);
+          return fail(BNN_E_UNSUPPORTED, "bnn_net_create: conv->dense at layer %d needs channels %% 32 == 0 (got %d)", i, C);
+        }
+        D = (int64_t)H * W * C;
+      }
+      P.d = D;
+      const int64_t dw = (D + 31) / 32;
+      bnn_status st = check_pad_bits(Ls.wt, Ls.l, dw, D % 32 == 0 ? 32 : (int)(D % 32), "weights", i);
+      if (st != BNN_OK) { net_free(net); return st; }
+      D = Ls.l;
+      P.out_words_per_img = (Ls.l + 31) / 32;
+      if (i != n_layers - 1) net->buf_words = std::max(net->buf_words, P.out_words_per_img);
+    } else {
+      net_free(net);
+      return fail(BNN_E_ARG, "bnn_net_create: layer %d has unknown kind %d", i, Ls.kind);
+    }
+    net->L.push_back(P);
+  }
+  net->chunk = max_batch;
+  cudaError_t e = cudaSuccess;
+  if (net->packed_in_words) e = cudaMalloc(&net->packed_in, (size_t)(net->packed_in_words * max_batch * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->buf[0], (size_t)(net->buf_words * max_batch * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->buf[1], (size_t)(net->buf_words * max_batch * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->logits_tmp, (size_t)net->L.back().l * max_batch * 4);
+  if (e != cudaSuccess) {
+    net_free(net);
+    return fail(BNN_E_CUDA, "bnn_net_create: workspace allocation: %s", cudaGetErrorString(e));
+  }
+  *out = net;
+  return BNN_OK;
+}
+
+bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits, int32_t* cls, bnn_stream_t stream) {
+  if (net == nullptr) return fail(BNN_E_ARG, "bnn_forward: null net");
+  if (n < 0) return fail(BNN_E_ARG, "bnn_forward: n < 0");
+  if (n > 0 && images == nullptr) return fail(BNN_E_ARG, "bnn_forward: null images");
+  BNN_REQUIRE_ALIGNED(images, "bnn_forward images");
+  BNN_REQUIRE_ALIGNED(logits, "bnn_forward logits");
+  BNN_REQUIRE_ALIGNED(cls, "bnn_forward cls");
+  const int L = net->L.back().l;
+  for (int s0 = 0; s0 < n; s0 += net->chunk) {
+    const int nb = std::min(net->chunk, n - s0);
+    const void* x = (const uint8_t*)images + (int64_t)s0 * net->img_bytes;
+    bnn_status st = forward_chunk(net, x, nb, logits ? logits + (int64_t)s0 * L : nullptr, cls ? cls + s0 : nullptr,
+                                  (cudaStream_t)stream);
+    if (st != BNN_OK) return st;
+  }
+  return BNN_OK;
+}
+
+int bnn_forward_launches(const bnn_net* net, int n) {
+  if (!net || n <= 0) return 0;
+  const int chunks = (n + net->chunk - 1) / net->chunk;
+  return chunks * launches_per_chunk(net, true);
+}
+
+bnn_status bnn_forward_host(bnn_net* net, const void* h_images, int n, int32_t* h_logits, int32_t* h_cls,
+                            bnn_stream_t stream) {
+  if (net == nullptr) return fail(BNN_E_ARG, "bnn_forward_host: null net");
+  if (n < 0) return fail(BNN_E_ARG, "bnn_forward_host: n < 0");
+  if (n > 0 && h_images == nullptr) return fail(BNN_E_ARG, "bnn_forward_host: null images");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int L = net->L.back().l;
+  cudaError_t e = cudaSuccess;
+  if (net->hchunk == 0) {
+    const int hc = std::min(net->chunk, 4096);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaMalloc(&net->d_in[i], (size_t)(net->img_bytes * hc));
+      if (e == cudaSuccess) e = cudaMalloc(&net->d_logits[i], (size_t)L * hc * 4);
+      if (e == cudaSuccess) e = cudaMalloc(&net->d_cls[i], (size_t)hc * 4);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->ev_h2d[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->ev_comp[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->ev_d2h[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&net->h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&net->d2h, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_host: staging allocation: %s", cudaGetErrorString(e));
+    net->hchunk = hc;
+  }
+  const int hc = net->hchunk;
+  // order the copy streams after everything already queued on the compute stream
+  cudaEventRecord(net->ev_comp[0], s);
+  cudaEventRecord(net->ev_comp[1], s);
+  cudaEventRecord(net->ev_d2h[0], s);
+  cudaEventRecord(net->ev_d2h[1], s);
+  int chunk_idx = 0;
+  for (int s0 = 0; s0 < n; s0 += hc, ++chunk_idx) {
+    const int b = chunk_idx & 1;
+    const int nb = std::min(hc, n - s0);
+    cudaStreamWaitEvent(net->h2d, net->ev_comp[b], 0);
+    e = cudaMemcpyAsync(net->d_in[b], (const uint8_t*)h_images + (int64_t)s0 * net->img_bytes,
+                        (size_t)(nb * net->img_bytes), cudaMemcpyHostToDevice, net->h2d);
+    if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_host: H2D: %s", cudaGetErrorString(e));
+    cudaEventRecord(net->ev_h2d[b], net->h2d);
+    cudaStreamWaitEvent(s, net->ev_h2d[b], 0);
+    cudaStreamWaitEvent(s, net->ev_d2h[b], 0);
+    bnn_status st = forward_chunk(net, net->d_in[b], nb, net->d_logits[b], net->d_cls[b], s);
+    if (st != BNN_OK) return st;
+    cudaEventRecord(net->ev_comp[b], s);
+    cudaStreamWaitEvent(net->d2h, net->ev_comp[b], 0);
+    if (h_logits) {
+      e = cudaMemcpyAsync(h_logits + (int64_t)s0 * L, net->d_logits[b], (size_t)nb * L * 4, cudaMemcpyDeviceToHost, net->d2h);
+      if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_host: D2H: %s", cudaGetErrorString(e));
+    }
+    if (h_cls) {
+      e = cudaMemcpyAsync(h_cls + s0, net->d_cls[b], (size_t)nb * 4, cudaMemcpyDeviceToHost, net->d2h);
+      if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_host: D2H: %s", cudaGetErrorString(e));
+    }
+    cudaEventRecord(net->ev_d2h[b], net->d2h);
+  }
+  e = cudaStreamSynchronize(net->d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_host: %s", cudaGetErrorString(e));
+  return BNN_OK;
+}
+
+int bnn_net_profile(bnn_net* net, int enable) {
+  if (net == nullptr) return -(int)fail(BNN_E_ARG, "bnn_net_profile: null net");
+  const int ns = (int)net->L.size() + 2;
+  if (enable) {
+    cudaDeviceSynchronize();
+    net->ev_used = 0;
+    net->pending_stage.clear();
+    net->stage_ms.assign(ns, 0.0);
+    net->stage_launches.assign(ns, 0);
+  }
+  net->prof = enable != 0;
+  return ns;
+}
+
+int bnn_net_profile_read(bnn_net* net, double* ms, int64_t* launches, int cap) {
+  if (net == nullptr) return -(int)fail(BNN_E_ARG, "bnn_net_profile_read: null net");
+  const int ns = (int)net->L.size() + 2;
+  if ((int)net->stage_ms.size() != ns) { net->stage_ms.assign(ns, 0.0); net->stage_launches.assign(ns, 0); }
+  for (size_t i = 0; i < net->pending_stage.size(); ++i) {
+    cudaEvent_t b = net->ev_pool[2 * i], e = net->ev_pool[2 * i + 1];
+    cudaError_t err = cudaEventSynchronize(e);
+    float t = 0.f;
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&t, b, e);
+    if (err != cudaSuccess) return -(int)fail(BNN_E_CUDA, "bnn_net_profile_read: %s", cudaGetErrorString(err));
+    net->stage_ms[net->pending_stage[i]] += t;
+    net->stage_launches[net->pending_stage[i]] += 1;
+  }
+  net->pending_stage.clear();
+  net->ev_used = 0;
+  for (int i = 0; i < ns && i < cap; ++i) {
+    if (ms) ms[i] = net->stage_ms[i];
+    if (launches) launches[i] = net->stage_launches[i];
+  }
+  return ns;
+}
+
+void bnn_net_destroy(bnn_net* net) { net_free(net); }
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+"""Parity of the CUDA path (libbnn.so through the C ABI) with the CPU oracle, element by element.
+
+Binary layers must match bit-exactly: packed words, int32 accumulators and logits (north_star).
+The f32 real first layer must match within 1e-5 relative error (reading R18).
+Inputs come from paper_1808_00209_b200.synth (seeded, CPU generator), are copied to the GPU for the
+CUDA path and handed unchanged to the oracle.  Sizes span several tiles and ragged tails.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_1808_00209_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def u32(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def dev(t):
+    return t.contiguous().cuda()
+
+
+# ------------------------------------------------------------------------------------ pack
+@pytest.mark.parametrize("dtype", [torch.uint8, torch.int8, torch.float32, torch.int32])
+@pytest.mark.parametrize("c", [1, 3, 32, 33, 70])
+def test_pack_sign(cuda, orc, dtype, c):
+    g = torch.Generator().manual_seed(c)
+    if dtype == torch.float32:
+        x = torch.randn((2, 5, 7, c), generator=g)
+        x[0, 0, 0, 0] = 0.0
+        x[0, 0, 1, 0] = -0.0
+    elif dtype == torch.uint8:
+        x = torch.randint(0, 3, (2, 5, 7, c), generator=g, dtype=torch.uint8)
+    else:
+        x = torch.randint(-3, 4, (2, 5, 7, c), generator=g).to(dtype)
+    y = u32(cuda.pack(dev(x), cuda.SIGN))
+    ref = np.stack([orc.pack_channels(orc.binarize_input(x[i].numpy().astype(np.float64), orc.SIGN))
+                    for i in range(2)])
+    assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("n,h,w", [(3, 96, 96), (1, 5, 7), (2, 3, 3), (1, 1, 1)])
+@pytest.mark.parametrize("mode", ["rgb", "rgb_int", "gray", "lbp"])
+def test_pack_input_modes(cuda, orc, n, h, w, mode):
+    x = synth.images(n, h, w, 3, 1000 + h + n)
+    if mode == "rgb":
+        T = synth.thresholds(3, 5)
+        m = cuda.THRESH_RGB
+    elif mode == "rgb_int":
+        T = torch.tensor([-128.0, -100.0, -1.0])  # X + T = 0 ties occur
+        m = cuda.THRESH_RGB
+    elif mode == "gray":
+        T = torch.tensor([-120.0])
+        m = cuda.THRESH_GRAY
+    else:
+        T = None
+        m = cuda.LBP
+    y = u32(cuda.pack(dev(x), m, None if T is None else dev(T)))
+    om = {cuda.THRESH_RGB: orc.THRESH_RGB, cuda.THRESH_GRAY: orc.THRESH_GRAY, cuda.LBP: orc.LBP}[m]
+    ref = np.stack([orc.pack_channels(orc.binarize_input(x[i].numpy(), om, None if T is None else T.numpy()))
+                    for i in range(n)])
+    assert np.array_equal(y, ref)
+
+
+def test_pack_rgb_f32(cuda, orc):
+    x = torch.rand((2, 9, 11, 3)) * 300 - 20
+    T = torch.tensor([-128.5, 3.25, -0.0])
+    y = u32(cuda.pack(dev(x), cuda.THRESH_RGB, dev(T)))
+    ref = np.stack([orc.pack_channels(orc.binarize_input(x[i].numpy(), orc.THRESH_RGB, T.numpy())) for i in range(2)])
+    assert np.array_equal(y, ref)
+
+
+# ------------------------------------------------------------------------------------ conv
+def conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=False, flip=False, seed=0):
+    xs = synth.pm1((n, h, w, cin), 10 + seed)
+    ws = synth.pm1((cout, k, k, cin), 20 + seed)
+    t = synth.int_thresholds(cout, 30 + seed, -2 * k, 2 * k + 1) if thr else None
+    f = synth.flips(cout, 40 + seed) if flip else None
+    xp = cuda.pack(dev(xs))
+    wp = cuda.pack_weights(dev(ws))
+    y, acc = cuda.conv2d(xp, cuda.BITS, cin, wp, cout, k, None if t is None else dev(t), None if f is None else dev(f),
+                         pool=pool, want_y=True, want_acc=True)
+    torch.cuda.synchronize()
+    acc = acc.cpu().numpy()
+    y = u32(y)
+    for i in range(n):
+        ra = orc.conv_binary(xs[i].numpy(), ws.numpy())
+        assert np.array_equal(acc[i], ra), "acc mismatch image %d" % i
+        b = orc.binarize(ra, None if t is None else t.numpy(), None if f is None else f.numpy())
+        if pool == 2:
+            b = orc.maxpool2(b)
+        assert np.array_equal(y[i], orc.pack_channels(b)), "packed mismatch image %d" % i
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,pool", [
+    (2, 48, 48, 32, 32, 5, 2),    # vehicle conv2
+    (2, 96, 96, 3, 32, 5, 2),     # vehicle conv1 (dense-patch kernel)
+    (1, 96, 96, 1, 32, 5, 2),     # gray conv1
+    (3, 10, 14, 32, 32, 3, 1),    # ragged tiles
+    (2, 12, 20, 40, 40, 3, 2),    # ragged channels (pad bits in and out, 2 groups)
+    (1, 9, 7, 64, 33, 1, 1),      # k = 1, odd map
+    (1, 16, 16, 300, 70, 3, 1),   # multi-chunk (cw = 10 > 8)
+    (1, 13, 11, 16, 8, 7, 1),     # k = 7 patch path (7*7*16 > 256 -> generic)
+    (1, 14, 18, 5, 20, 7, 2),     # k = 7 dense patch (245 bits = 8 words)
+    (2, 8, 8, 128, 64, 3, 2),     # small map tile
+    (1, 4, 6, 32, 32, 5, 1),      # map smaller than the kernel reach
+    (1, 32, 32, 3, 128, 3, 1),    # CIFAR conv1 (27-bit patch)
+])
+def test_conv_binary(cuda, orc, n, h, w, cin, cout, k, pool):
+    conv_case(cuda, orc, n, h, w, cin, cout, k, pool, seed=h + cin + k)
+
+
+@pytest.mark.parametrize("cin,k", [(3, 5), (32, 3)])
+def test_conv_threshold_flip(cuda, orc, cin, k):
+    conv_case(cuda, orc, 2, 16, 16, cin, 40, k, 2, thr=True, flip=True, seed=7)
+
+
+@pytest.mark.parametrize("algo,tpc", [(1, 0), (0, 1), (0, 3), (1, 7)])
+def test_conv_tiling_invariance(cuda, orc, algo, tpc):
+    """Launch configuration does not change a single bit (and the generic kernel agrees with
+    the dense-patch kernel on the first layer)."""
+    try:
+        cuda.set_option("conv_algo", algo)
+        cuda.set_option("tiles_per_cta", tpc)
+        conv_case(cuda, orc, 2, 24, 40, 3, 32, 5, 2, seed=3)
+        conv_case(cuda, orc, 3, 16, 32, 32, 32, 3, 1, seed=4)
+    finally:
+        cuda.set_option("conv_algo", 0)
+        cuda.set_option("tiles_per_cta", 0)
+
+
+def test_conv_empty_batch(cuda):
+    xp = torch.zeros((0, 8, 8, 1), dtype=torch.int32, device="cuda")
+    wp = cuda.pack_weights(dev(synth.pm1((32, 3, 3, 32), 1)))
+    y, _ = cuda.conv2d(xp, cuda.BITS, 32, wp, 32, 3)
+    assert y.shape == (0, 8, 8, 1)
+
+
+@pytest.mark.parametrize("k,pool", [(5, 2), (3, 1), (1, 1), (7, 2)])
+@pytest.mark.parametrize("cin", [3, 1])
+def test_conv_real_u8(cuda, orc, k, pool, cin):
+    n, h, w, cout = 2, 20, 24, 40
+    x = synth.images(n, h, w, cin, 50 + k)
+    ws = synth.pm1((cout, k, k, cin), 60 + k)
+    t = synth.int_thresholds(cout, 61, -300, 300)
+    y, acc = cuda.conv2d(dev(x), cuda.U8, cin, cuda.pack_weights(dev(ws)), cout, k, dev(t), None, pool=pool,
+                         want_acc=True)
+    torch.cuda.synchronize()
+    acc = acc.cpu().numpy()
+    y = u32(y)
+    for i in range(n):
+        ra = orc.conv_real(x[i].numpy().astype(np.float64), ws.numpy())
+        assert np.array_equal(acc[i], ra.astype(np.int64))
+        b = orc.binarize(ra, t.numpy())
+        if pool == 2:
+            b = orc.maxpool2(b)
+        assert np.array_equal(y[i], orc.pack_channels(b))
+
+
+def test_conv_real_f32(cuda, orc):
+    n, h, w, cin, cout, k = 2, 12, 10, 3, 36, 5
+    x = torch.randn((n, h, w, cin), generator=torch.Generator().manual_seed(3)) * 50
+    ws = synth.pm1((cout, k, k, cin), 70)
+    y, acc = cuda.conv2d(dev(x), cuda.F32, cin, cuda.pack_weights(dev(ws)), cout, k, None, None, pool=2, want_acc=True)
+    torch.cuda.synchronize()
+    acc = acc.cpu().numpy().astype(np.float64)
+    y = u32(y)
+    exempt = 0
+    for i in range(n):
+        ra = orc.conv_real(x[i].numpy().astype(np.float64), ws.numpy())
+        scale = orc.conv_real(np.abs(x[i].numpy().astype(np.float64)), np.ones_like(ws.numpy()))[..., :1]
+        assert np.all(np.abs(acc[i] - ra) <= 1e-5 * np.maximum(np.abs(ra), scale))
+        ref_bits = orc.maxpool2(orc.binarize(ra))
+        tiny = np.abs(ra) <= 1e-5 * scale  # sign decided by rounding: exempt (reading R18)
+        tiny_any = tiny.reshape(h // 2, 2, w // 2, 2, cout).any(axis=(1, 3))
+        mismatch = orc.unpack_channels(y[i], cout) != ref_bits
+        assert not np.any(mismatch & ~tiny_any)
+        exempt += int(mismatch.sum())
+    assert exempt <= 4
+
+
+# ------------------------------------------------------------------------------------ pool, dense
+@pytest.mark.parametrize("n,h,w,c", [(2, 96, 96, 32), (3, 6, 10, 70), (1, 2, 2, 1)])
+def test_maxpool(cuda, orc, n, h, w, c):
+    xs = synth.pm1((n, h, w, c), 80 + c)
+    y = u32(cuda.maxpool(cuda.pack(dev(xs)), c))
+    for i in range(n):
+        assert np.array_equal(y[i], orc.pack_channels(orc.maxpool2(xs[i].numpy())))
+
+
+@pytest.mark.parametrize("n,d,l", [(5, 18432, 100), (130, 100, 100), (70, 100, 4), (33, 4096, 10), (1, 37, 1),
+                                   (64, 2048, 1024)])
+def test_dense(cuda, orc, n, d, l):
+    xs = synth.pm1((n, d), 90 + d)
+    ws = synth.pm1((l, d), 91 + l)
+    t = synth.int_thresholds(l, 92, -4, 5)
+    xp = cuda.pack(dev(xs).view(n, 1, 1, d)).view(n, -1)
+    y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None, want_acc=True, want_cls=True)
+    torch.cuda.synchronize()
+    acc, y, cls = acc.cpu().numpy(), u32(y), cls.cpu().numpy()
+    for i in range(n):
+        ra = orc.dense(xs[i].numpy(), ws.numpy())
+        assert np.array_equal(acc[i], ra)
+        assert np.array_equal(y[i], orc.pack(orc.binarize(ra[None], t.numpy())[0], 32))
+        assert cls[i] == orc.argmax(ra)
+
+
+# ------------------------------------------------------------------------------------ forward
+def build_net(cuda, spec, mode, seed, max_batch=4096, thr=False):
+    layers = synth.make_weights(spec, mode, seed)
+    dev_layers = []
+    for i, L in enumerate(layers):
+        D = dict(L)
+        D["wt"] = cuda.pack_weights(dev(L["wt"]))
+        if thr and i < len(layers) - 1:
+            nout = L["c_out"] if L["kind"] == "conv" else L["l"]
+            L["thr"] = synth.int_thresholds(nout, seed + i, -3, 4)
+            L["flip"] = synth.flips(nout, seed + 50 + i)
+            D["thr"], D["flip"] = dev(L["thr"]), dev(L["flip"])
+        dev_layers.append(D)
+    T = {1: synth.thresholds(3, seed), 2: torch.tensor([-127.0])}.get(mode)
+    net = cuda.Net(spec["h"], spec["w"], spec["c"], cuda.U8, mode, None if T is None else dev(T), dev_layers,
+                   max_batch=max_batch)
+    return net, layers, T
+
+
+def oracle_net(orc, spec, mode, layers, T):
+    ol = []
+    for L in layers:
+        D = dict(L)
+        D["wt"] = L["wt"].numpy()
+        if L.get("thr") is not None:
+            D["thr"] = L["thr"].numpy()
+            D["flip"] = L["flip"].numpy()
+        ol.append(D)
+    om = {0: orc.SIGN, 1: orc.THRESH_RGB, 2: orc.THRESH_GRAY, 3: orc.LBP, -1: orc.NONE}[mode]
+    return orc.Net(spec["h"], spec["w"], spec["c"], om, None if T is None else T.numpy(), ol)
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3, -1, 0])
+def test_forward_vehicle(cuda, orc, mode):
+    net, layers, T = build_net(cuda, synth.VEHICLE, mode, 500 + mode)
+    imgs = synth.images(6, 96, 96, 3, 600 + mode)
+    logits, cls = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=6)
+    assert np.array_equal(logits.cpu().numpy(), ref_logits)
+    assert np.array_equal(cls.cpu().numpy(), ref_cls)
+
+
+def test_forward_thresholds_and_chunking(cuda, orc):
+    """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
+    imgs = synth.images(5, 96, 96, 3, 778)
+    logits, cls = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=5)
+    assert np.array_equal(logits.cpu().numpy(), ref_logits)
+    assert np.array_equal(cls.cpu().numpy(), ref_cls)
+
+
+def test_forward_host_equals_forward(cuda):
+    net, _, _ = build_net(cuda, synth.VEHICLE, 1, 900, max_batch=4096)
+    imgs = synth.images(9000, 96, 96, 3, 901)  # 3 host chunks of <= 4096, ragged
+    lg_d, cls_d = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    lg_h, cls_h = net.forward_host(imgs.pin_memory())
+    assert torch.equal(lg_h, lg_d.cpu()) and torch.equal(cls_h, cls_d.cpu())
+    assert cuda.forward_launches(net, 9000) == 3 * 6
+
+
+def test_forward_cifar(cuda, orc):
+    net, layers, T = build_net(cuda, synth.CIFAR, 1, 1200)
+    imgs = synth.images(3, 32, 32, 3, 1201)
+    logits, cls = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref_logits, ref_cls = oracle_net(orc, synth.CIFAR, 1, layers, T).forward(imgs.numpy(), threads=3)
+    assert np.array_equal(logits.cpu().numpy(), ref_logits)
+    assert np.array_equal(cls.cpu().numpy(), ref_cls)
+
+
+def test_forward_fault_injection(cuda, orc):
+    """Flipping one conv2 weight bit must change the GPU result exactly as it changes the
+    oracle's (the parity check is sensitive)."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 1300)
+    layers[1]["wt"][5, 2, 2, 7] *= -1
+    dl = []
+    for L in layers:
+        D = dict(L)
+        D["wt"] = cuda.pack_weights(dev(L["wt"]))
+        dl.append(D)
+    net2 = cuda.Net(96, 96, 3, cuda.U8, 1, dev(T), dl, max_batch=64)
+    imgs = synth.images(4, 96, 96, 3, 1301)
+    lg, _ = net2.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref, _ = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=4)
+    assert np.array_equal(lg.cpu().numpy(), ref)
