@@ -193,6 +193,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_1808_00209_b200 as bnn
+    from paper_1808_00209_b200 import dist as bdist
     from paper_1808_00209_b200 import synth
 
     assert torch.cuda.is_available(), "bench.py needs a GPU (the CUDA path has no CPU fallback)"
@@ -225,8 +226,7 @@ def main():
     def step():
         net.forward(images, logits, cls)
         if world > 1:
-            dist.all_gather_into_tensor(logits_all, logits)
-            dist.all_gather_into_tensor(cls_all, cls)
+            bdist.gather_predictions(logits, cls, logits_all, cls_all)
 
     for _ in range(a.warmup):
         step()

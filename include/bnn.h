@@ -86,8 +86,9 @@ BNN_API const char* bnn_last_error(void);
 BNN_API int bnn_version(void);
 
 /* Process-wide tuning / test knobs (not thread-safe against concurrent launches):
- *   "conv_algo"     0 = automatic (default); 1 = force the generic one-word-per-tap
- *                   binary conv even where the dense-patch first-layer kernel applies.
+ *   "conv_algo"     first-layer kernel choice for c_in < 32: 0 = automatic (default);
+ *                   1 = generic one-word-per-tap conv; 2 = dense-patch kernel; 3 = strip
+ *                   kernel (lane = channel); 4 = strip kernel (lane = pixel).
  *   "tiles_per_cta" 0 = automatic (default); k > 0 = every conv CTA walks k output tiles.
  * Results are bit-identical for every setting (tiling invariance is a parity test).
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */

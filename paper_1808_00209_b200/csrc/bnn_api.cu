@@ -129,6 +129,55 @@ bnn_status launch_conv_patch_t(ConvArgs A, cudaStream_t s) {
   return check_launch("conv_patch_kernel");
 }
 
+template <int K, int WY, int WX, bool SRC_U8>
+bnn_status launch_conv_strip_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  constexpr int PR = 2, PC = 8;
+  constexpr int TH = WY * PR, TW = WX * PC;
+  A.tiles_y = (A.H + TH - 1) / TH;
+  A.tiles_x = (A.W + TW - 1) / TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = choose_tpc(A.total_tiles, false);
+  const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
+  dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
+  conv_strip_kernel<K, PR, PC, WY, WX, SRC_U8><<<grid, WY * WX * 32, 0, s>>>(A, xu8, T);
+  return check_launch("conv_strip_kernel");
+}
+
+template <int WY, int WX, bool SRC_U8>
+bnn_status dispatch_conv_strip(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  switch (k) {
+    case 3: return launch_conv_strip_t<3, WY, WX, SRC_U8>(A, xu8, T, s);
+    case 5: return launch_conv_strip_t<5, WY, WX, SRC_U8>(A, xu8, T, s);
+    case 7: return launch_conv_strip_t<7, WY, WX, SRC_U8>(A, xu8, T, s);
+  }
+  return fail(BNN_E_UNSUPPORTED, "conv_strip: k=%d", k);
+}
+
+template <int K, int NW, bool SRC_U8>
+bnn_status launch_conv_first_lp_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  constexpr int TH = 16, TW = 32;
+  A.tiles_y = (A.H + TH - 1) / TH;
+  A.tiles_x = (A.W + TW - 1) / TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = choose_tpc(A.total_tiles, false);
+  const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
+  dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
+  conv_first_lp_kernel<K, NW, SRC_U8><<<grid, 256, 0, s>>>(A, xu8, T);
+  return check_launch("conv_first_lp_kernel");
+}
+
+// (k, words-per-patch) combinations of the strip layout that the lane = pixel kernel covers
+template <bool SRC_U8>
+bnn_status dispatch_conv_first_lp(int k, int nw, const ConvArgs& A, const uint8_t* xu8, const float* T,
+                                  cudaStream_t s) {
+#define BNN_LP(KK, NN) if (k == KK && nw == NN) return launch_conv_first_lp_t<KK, NN, SRC_U8>(A, xu8, T, s)
+  BNN_LP(3, 1); BNN_LP(3, 2); BNN_LP(3, 3);
+  BNN_LP(5, 1); BNN_LP(5, 2); BNN_LP(5, 3); BNN_LP(5, 5);
+  BNN_LP(7, 2); BNN_LP(7, 4); BNN_LP(7, 7);
+#undef BNN_LP
+  return fail(BNN_E_UNSUPPORTED, "conv_first_lp: k=%d nw=%d", k, nw);
+}
+
 template <int K, int WY, int WX>
 bnn_status launch_conv_real_u8_t(RealConvArgs A, cudaStream_t s) {
   constexpr int PR = 2, PC = 8;
@@ -181,9 +230,36 @@ bnn_status dispatch_conv_real_u8(int k, const RealConvArgs& A, cudaStream_t s) {
   return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: k=%d not supported (1, 3, 5, 7)", k);
 }
 
-// Is the dense-patch first-layer kernel applicable?  (few input channels, one word/pixel)
+// First-layer kernels for few input channels (one word per pixel):
+//   strip  : K-tap row strips stacked rpw = 32/(K c_in) rows per word (conv_strip_kernel)
+//   patch  : the K*K*c_in bits packed densely (conv_patch_kernel)
+// conv_algo: 0 auto, 1 generic one-word-per-tap, 2 dense patch, 3 strip.
+int strip_words(int c_in, int k) {
+  const int S = k * c_in;
+  if (k < 3 || S > 32) return 1 << 30;
+  const int rpw = 32 / S;
+  return (k + rpw - 1) / rpw;
+}
+int dense_words(int c_in, int k) { return (k * k * c_in + 31) / 32; }
+
+bool use_strip(int c_in, int k) {
+  if (c_in >= 32 || strip_words(c_in, k) > 7) return false;
+  if (g_opt_conv_algo == 3) return true;
+  return g_opt_conv_algo == 0 && strip_words(c_in, k) <= dense_words(c_in, k);
+}
+
+// lane = pixel first-layer kernel (conv_algo 0 = auto or 4 = forced)
+bool use_first_lp(int c_in, int k) {
+  if (g_opt_conv_algo != 0 && g_opt_conv_algo != 4) return false;
+  const int nw = strip_words(c_in, k);
+  if (c_in >= 32 || nw > 7) return false;
+  const bool have = (k == 3 && nw <= 3) || (k == 5 && (nw <= 3 || nw == 5)) || (k == 7 && (nw == 2 || nw == 4 || nw == 7));
+  if (!have) return false;
+  return g_opt_conv_algo == 4 || nw <= dense_words(c_in, k);
+}
+
 bool use_patch(int c_in, int k) {
-  return g_opt_conv_algo == 0 && c_in < 32 && k > 1 && k * k * c_in <= 256;
+  return (g_opt_conv_algo == 0 || g_opt_conv_algo == 2) && c_in < 32 && k > 1 && k * k * c_in <= 256;
 }
 
 bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c_in, const uint32_t* wt, int c_out,
@@ -196,6 +272,10 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
     A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
     A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
     A.cwo = (c_out + 31) / 32; A.pool = pool;
+    if (use_first_lp(c_in, k)) return dispatch_conv_first_lp<false>(k, strip_words(c_in, k), A, nullptr, nullptr, s);
+    if (use_strip(c_in, k))
+      return small ? dispatch_conv_strip<4, 1, false>(k, A, nullptr, nullptr, s)
+                   : dispatch_conv_strip<4, 2, false>(k, A, nullptr, nullptr, s);
     const bool patch = use_patch(c_in, k);
     return small ? dispatch_conv_bin<4, 1>(k, A, patch, s) : dispatch_conv_bin<4, 2>(k, A, patch, s);
   }
@@ -410,18 +490,46 @@ struct ProfScope {
   }
 };
 
+// Layer 0 fuses the input threshold (SIGN / THRESH_RGB on u8 pixels) into the strip conv kernel.
+bool fused_input(const bnn_net* net) {
+  if (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) return false;
+  if (net->in_dt != BNN_U8 || net->c > 4 || net->L[0].kind != 1) return false;
+  return use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
+}
+
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
   const void* cur = images;
   bnn_dtype cur_dt = net->in_dt;
-  if (net->mode != BNN_MODE_NONE) {
+  const int nl = (int)net->L.size();
+  int first = 0;
+  if (fused_input(net)) {
+    // layer 0 reads the u8 image and thresholds it itself (no packed round trip through HBM)
+    const LayerPlan& P = net->L[0];
+    ProfScope ps(net, 1, s);
+    ConvArgs A{};
+    A.x = nullptr; A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.y = net->buf[0]; A.acc = nullptr;
+    A.n = nb; A.H = P.H; A.W = P.W; A.cw = 1; A.c_in = P.c_in; A.c_out = P.c_out;
+    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool;
+    const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
+    const bool small = (P.W <= 8 || P.H <= 8);
+    bnn_status st;
+    if (use_first_lp(P.c_in, P.k))
+      st = dispatch_conv_first_lp<true>(P.k, strip_words(P.c_in, P.k), A, (const uint8_t*)images, T, s);
+    else
+      st = small ? dispatch_conv_strip<4, 1, true>(P.k, A, (const uint8_t*)images, T, s)
+                 : dispatch_conv_strip<4, 2, true>(P.k, A, (const uint8_t*)images, T, s);
+    if (st != BNN_OK) return st;
+    cur = net->buf[0];
+    cur_dt = BNN_BITS;
+    first = 1;
+  } else if (net->mode != BNN_MODE_NONE) {
     ProfScope ps(net, 0, s);
     bnn_status st = launch_pack(images, net->in_dt, nb, net->h, net->w, net->c, net->mode, net->T, net->packed_in, s);
     if (st != BNN_OK) return st;
     cur = net->packed_in;
     cur_dt = BNN_BITS;
   }
-  const int nl = (int)net->L.size();
-  for (int i = 0; i < nl; ++i) {
+  for (int i = first; i < nl; ++i) {
     const LayerPlan& P = net->L[i];
     const bool last = (i == nl - 1);
     bnn_status st;
@@ -451,7 +559,7 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
 }
 
 int launches_per_chunk(const bnn_net* net, bool want_cls) {
-  int n = (net->mode != BNN_MODE_NONE ? 1 : 0) + (int)net->L.size();
+  int n = (net->mode != BNN_MODE_NONE && !fused_input(net) ? 1 : 0) + (int)net->L.size();
   if (want_cls && net->L.back().l > 32) n += 1;
   return n;
 }

@@ -307,6 +307,313 @@ conv_patch_kernel(const ConvArgs A) {
   }
 }
 
+// First binary layer with few input channels, "strip" layout.  For every input row r of the
+// halo tile and output column x, the K horizontal taps x-R..x+R of c_in bits each form one
+// S = K*c_in bit strip (built with K warp shuffles per row, one lane per column).  A patch word
+// then stacks rpw = 32/S strips of consecutive rows (top-aligned), so the K x K x c_in patch of
+// an output pixel is ceil(K/rpw) words (vehicle conv1: 15-bit strips, 2 rows/word, 3 words) and
+// costs a few shifts per pixel instead of a per-bit loop.  The weights are repacked the same way
+// in registers.  With SRC_U8 the kernel reads the u8 image and applies the Section 2.3 threshold
+// (bit_c = x_c > -T_c, or x_c > 0 for SIGN) itself, so the input never makes a packed round trip
+// through HBM.
+template <int K, int PR, int PC, int WY, int WX, bool SRC_U8>
+__global__ void __launch_bounds__(WY * WX * 32)
+conv_strip_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float* __restrict__ Tt) {
+  constexpr int R = (K - 1) / 2;
+  constexpr int TH = WY * PR, TW = WX * PC;
+  constexpr int IR = TH + K - 1;
+  constexpr int IC = TW + K - 1;
+  constexpr int NT = WY * WX * 32;
+  constexpr int NWARP = WY * WX;
+  static_assert(IC <= 32, "one lane per halo column");
+
+  __shared__ uint32_t strips[IR * TW];
+  __shared__ __align__(16) uint32_t patch[K * TH * TW];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / WX, wx = warp % WX;
+  const int g = blockIdx.y;
+  const int o = g * 32 + lane;
+  const bool ovalid = o < A.c_out;
+  const int thr_o = (A.thr != nullptr && ovalid) ? A.thr[o] : 0;
+  const bool flip_o = (A.flip != nullptr && ovalid) ? (A.flip[o] != 0) : false;
+  const int cin = A.c_in;
+  const int S = K * cin;
+  const int rpw = 32 / S;
+  const int nw = (K + rpw - 1) / rpw;
+  const int nbits = K * K * cin;
+
+  // thresholds for the fused u8 path: bit_c = x_c > t_c
+  float tc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (SRC_U8 && Tt != nullptr) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < cin) tc[c] = -Tt[c];
+  }
+
+  // this lane's weights in the strip layout
+  uint32_t wreg[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    wreg[j] = 0u;
+    if (j < nw && ovalid) {
+      for (int t = 0; t < rpw; ++t) {
+        const int ky = j * rpw + t;
+        if (ky >= K) break;
+        uint32_t ws = 0;
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx)
+          ws |= (__ldg(A.wt + (int64_t)o * K * K + ky * K + kx) >> (32 - cin)) << (cin * (K - 1 - kx));
+        wreg[j] |= ws << (32 - (t + 1) * S);
+      }
+    }
+  }
+
+  const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
+  const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
+  const int tiles_img = A.tiles_x * A.tiles_y;
+
+  for (int64_t tile = t_begin; tile < t_end; ++tile) {
+    const int img = (int)(tile / tiles_img);
+    const int trem = (int)(tile - (int64_t)img * tiles_img);
+    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    const int oy0 = ty * TH, ox0 = tx * TW;
+
+    // phase A: one warp per halo row: lane = halo column -> c_in-bit code -> K-tap strips
+    for (int r = warp; r < IR; r += NWARP) {
+      const int gy = oy0 - R + r, gx = ox0 - R + lane;
+      uint32_t code = 0u;  // outside the map: all bits 0 = -1 (R4)
+      if (lane < IC && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) {
+        const int64_t pix = ((int64_t)img * A.H + gy) * A.W + gx;
+        if (SRC_U8) {
+          const uint8_t* px = xu8 + pix * cin;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < cin) code |= (uint32_t)((float)px[c] > tc[c]) << (cin - 1 - c);
+        } else {
+          code = __ldg(A.x + pix) >> (32 - cin);
+        }
+      }
+      uint32_t strip = 0u;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) strip |= __shfl_sync(BNN_FULL_MASK, code, (lane + kx) & 31) << (cin * (K - 1 - kx));
+      if (lane < TW) strips[r * TW + lane] = strip;
+    }
+    __syncthreads();
+    // phase B: patch words = rpw strips of consecutive rows, top-aligned
+    for (int it = tid; it < nw * TH * TW; it += NT) {
+      const int j = it / (TH * TW);
+      const int pix = it - j * (TH * TW);
+      const int py = pix / TW, px = pix - py * TW;
+      uint32_t word = 0u;
+      for (int t = 0; t < rpw; ++t) {
+        const int row = j * rpw + t;
+        if (row < K) word |= strips[(py + row) * TW + px] << (32 - (t + 1) * S);
+      }
+      patch[it] = word;
+    }
+    __syncthreads();
+
+    int acc[PR][PC];
+#pragma unroll
+    for (int r = 0; r < PR; ++r)
+#pragma unroll
+      for (int p = 0; p < PC; ++p) acc[r][p] = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < nw) {
+#pragma unroll
+        for (int r = 0; r < PR; ++r) {
+          const uint4* src = reinterpret_cast<const uint4*>(patch + (j * TH + wy * PR + r) * TW + wx * PC);
+#pragma unroll
+          for (int v = 0; v < PC / 4; ++v) {
+            const uint4 q = src[v];
+            acc[r][4 * v] += popc(q.x ^ wreg[j]);
+            acc[r][4 * v + 1] += popc(q.y ^ wreg[j]);
+            acc[r][4 * v + 2] += popc(q.z ^ wreg[j]);
+            acc[r][4 * v + 3] += popc(q.w ^ wreg[j]);
+          }
+        }
+      }
+    }
+    int a[PR][PC];
+#pragma unroll
+    for (int r = 0; r < PR; ++r)
+#pragma unroll
+      for (int p = 0; p < PC; ++p) a[r][p] = nbits - 2 * acc[r][p];
+    conv_epilogue<PR, PC>(A, img, oy0 + wy * PR, ox0 + wx * PC, g, lane, a, thr_o, flip_o);
+  }
+}
+
+// First binary layer, "lane = pixel" mapping (the fast path for c_in <= 10).
+// With only NW (1..7) patch words per output, the lane = channel kernels above spend most of
+// their issue slots on the per-pixel epilogue (ballot, brev, addressing).  Here each thread owns
+// two vertically adjacent output pixels and walks the 32 output channels of its group: the
+// channel's NW weight words and its integer limit arrive with one broadcast LDS.128, and
+//   bit = (K*K*c_in - 2 acc > thr)  <=>  acc <= lim,  lim = floor((K*K*c_in - thr - 1) / 2)
+// sets bit 31 - c of the output word with one predicated OR -- the packed word is built in a
+// register, the flip mask is one XOR, the 2x2 OR-pool is one OR plus one shuffle.
+// Patch layout: strips of K taps (S = K*c_in bits) stacked RPW = ceil(K/NW) rows per word.
+template <int K, int NW, bool SRC_U8>
+__global__ void __launch_bounds__(256)
+conv_first_lp_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float* __restrict__ Tt) {
+  constexpr int NWARP = 8, PRW = 2;
+  constexpr int TH = NWARP * PRW, TW = 32;
+  constexpr int R = (K - 1) / 2;
+  constexpr int IR = TH + K - 1, IC = TW + K - 1;
+  constexpr int RPW = (K + NW - 1) / NW;
+  constexpr int WS = (NW + 1 + 3) & ~3;  // words per channel slot: NW weight words + limit
+  constexpr int NT = NWARP * 32;
+
+  __shared__ uint32_t codes[IR * IC];
+  __shared__ uint32_t strips[IR * TW];
+  __shared__ __align__(16) int32_t wsm[32 * WS];
+  __shared__ uint32_t flipmask_s;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.y;
+  const int cin = A.c_in;
+  const int S = K * cin;
+  const int nbits = K * K * cin;
+
+  if (warp == 0) {
+    const int o = g * 32 + lane;
+    const bool ovalid = o < A.c_out;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      uint32_t word = 0u;
+#pragma unroll
+      for (int t = 0; t < RPW; ++t) {
+        const int ky = j * RPW + t;
+        if (ky < K && ovalid) {
+          uint32_t ws = 0u;
+#pragma unroll
+          for (int kx = 0; kx < K; ++kx)
+            ws |= (__ldg(A.wt + (int64_t)o * K * K + ky * K + kx) >> (32 - cin)) << (cin * (K - 1 - kx));
+          word |= ws << (32 - (t + 1) * S);
+        }
+      }
+      wsm[lane * WS + j] = (int32_t)word;
+    }
+    int lim = -1;  // invalid channel: acc >= 0 > lim, bit stays 0
+    if (ovalid) {
+      const int64_t thr = (A.thr != nullptr) ? (int64_t)A.thr[o] : 0;
+      int64_t v = ((int64_t)nbits - thr - 1) >> 1;  // floor division
+      v = v < -1 ? -1 : (v > nbits ? nbits : v);
+      lim = (int)v;
+    }
+    wsm[lane * WS + NW] = lim;
+    const uint32_t fm = ballot_pack(ovalid && A.flip != nullptr && A.flip[o] != 0);
+    if (lane == 0) flipmask_s = fm;
+  }
+
+  float tc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (SRC_U8 && Tt != nullptr) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < cin) tc[c] = -Tt[c];
+  }
+  __syncthreads();
+  const uint32_t flipmask = flipmask_s;
+
+  const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
+  const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
+  const int tiles_img = A.tiles_x * A.tiles_y;
+
+  for (int64_t tile = t_begin; tile < t_end; ++tile) {
+    const int img = (int)(tile / tiles_img);
+    const int trem = (int)(tile - (int64_t)img * tiles_img);
+    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    const int oy0 = ty * TH, ox0 = tx * TW;
+
+    __syncthreads();  // previous tile's readers of codes / strips are done
+    for (int i = tid; i < IR * IC; i += NT) {
+      const int r = i / IC, cc = i - r * IC;
+      const int gy = oy0 - R + r, gx = ox0 - R + cc;
+      uint32_t code = 0u;  // outside the map: -1 (R4)
+      if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) {
+        const int64_t pix = ((int64_t)img * A.H + gy) * A.W + gx;
+        if (SRC_U8) {
+          const uint8_t* px = xu8 + pix * cin;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < cin) code |= (uint32_t)((float)px[c] > tc[c]) << (cin - 1 - c);
+        } else {
+          code = __ldg(A.x + pix) >> (32 - cin);
+        }
+      }
+      codes[i] = code;
+    }
+    __syncthreads();
+    for (int i = tid; i < IR * TW; i += NT) {
+      const int r = i / TW, x = i - r * TW;
+      uint32_t strip = 0u;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) strip |= codes[r * IC + x + kx] << (cin * (K - 1 - kx));
+      strips[i] = strip;
+    }
+    __syncthreads();
+
+    // this thread's two pixels: tile rows 2*warp and 2*warp + 1, column lane
+    uint32_t s[K + 1];
+#pragma unroll
+    for (int i = 0; i <= K; ++i) s[i] = strips[(PRW * warp + i) * TW + lane];
+    uint32_t p0[NW], p1[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      p0[j] = 0u;
+      p1[j] = 0u;
+#pragma unroll
+      for (int t = 0; t < RPW; ++t) {
+        const int ky = j * RPW + t;
+        if (ky < K) {
+          p0[j] |= s[ky] << (32 - (t + 1) * S);
+          p1[j] |= s[ky + 1] << (32 - (t + 1) * S);
+        }
+      }
+    }
+    const int oy = oy0 + PRW * warp, ox = ox0 + lane;
+    const bool in0 = oy < A.H && ox < A.W, in1 = (oy + 1) < A.H && ox < A.W;
+    uint32_t w0 = 0u, w1 = 0u;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      int wv[WS];
+#pragma unroll
+      for (int q = 0; q < WS / 4; ++q) {
+        const int4 v = reinterpret_cast<const int4*>(wsm + c * WS)[q];
+        wv[4 * q] = v.x; wv[4 * q + 1] = v.y; wv[4 * q + 2] = v.z; wv[4 * q + 3] = v.w;
+      }
+      int a0 = 0, a1 = 0;
+#pragma unroll
+      for (int j = 0; j < NW; ++j) {
+        a0 += popc(p0[j] ^ (uint32_t)wv[j]);
+        a1 += popc(p1[j] ^ (uint32_t)wv[j]);
+      }
+      const int lim = wv[NW];
+      if (a0 <= lim) w0 |= 1u << (31 - c);
+      if (a1 <= lim) w1 |= 1u << (31 - c);
+      if (A.acc != nullptr && g * 32 + c < A.c_out) {
+        if (in0) A.acc[(((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * 32 + c] = nbits - 2 * a0;
+        if (in1) A.acc[(((int64_t)img * A.H + oy + 1) * A.W + ox) * A.c_out + g * 32 + c] = nbits - 2 * a1;
+      }
+    }
+    w0 ^= flipmask;
+    w1 ^= flipmask;
+    if (A.y != nullptr) {
+      if (A.pool == 2) {
+        uint32_t v = w0 | w1;
+        v |= __shfl_xor_sync(BNN_FULL_MASK, v, 1);
+        const int Ho = A.H >> 1, Wo = A.W >> 1;
+        const int py = oy >> 1, px = ox >> 1;
+        if ((lane & 1) == 0 && py < Ho && px < Wo) A.y[(((int64_t)img * Ho + py) * Wo + px) * A.cwo + g] = v;
+      } else {
+        if (in0) A.y[(((int64_t)img * A.H + oy) * A.W + ox) * A.cwo + g] = w0;
+        if (in1) A.y[(((int64_t)img * A.H + oy + 1) * A.W + ox) * A.cwo + g] = w1;
+      }
+    }
+  }
+}
+
 // Real-valued first layer ("no input binarization"): acc = sum w * x with
 // w in {+1,-1} and ZERO padding (R5).  u8 input: exact int32 via IDP4A.U8.S8 on a per-pixel
 // byte patch staged in shared memory.  f32 input: fp32 FFMA in (ky, kx, c) order (R18).

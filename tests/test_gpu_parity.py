@@ -117,7 +117,7 @@ def test_conv_threshold_flip(cuda, orc, cin, k):
     conv_case(cuda, orc, 2, 16, 16, cin, 40, k, 2, thr=True, flip=True, seed=7)
 
 
-@pytest.mark.parametrize("algo,tpc", [(1, 0), (0, 1), (0, 3), (1, 7)])
+@pytest.mark.parametrize("algo,tpc", [(1, 0), (2, 0), (3, 0), (4, 0), (0, 1), (0, 3), (1, 7), (3, 5), (4, 2)])
 def test_conv_tiling_invariance(cuda, orc, algo, tpc):
     """Launch configuration does not change a single bit (and the generic kernel agrees with
     the dense-patch kernel on the first layer)."""
@@ -250,6 +250,30 @@ def test_forward_vehicle(cuda, orc, mode):
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
 
 
+@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 0])
+def test_forward_vehicle_unfused_first_layer(cuda, orc, mode, algo):
+    """The same net through the separate pack kernel + generic (1) / dense-patch (2) first layer."""
+    try:
+        cuda.set_option("conv_algo", algo)
+        test_forward_vehicle(cuda, orc, mode)
+    finally:
+        cuda.set_option("conv_algo", 0)
+
+
+@pytest.mark.parametrize("algo", [3, 4])
+@pytest.mark.parametrize("k", [3, 5, 7])
+@pytest.mark.parametrize("cin", [1, 2, 3, 4, 6])
+def test_conv_strip_shapes(cuda, orc, k, cin, algo):
+    if k * cin > 32:
+        pytest.skip("strip wider than a word")
+    try:
+        cuda.set_option("conv_algo", algo)
+        conv_case(cuda, orc, 2, 18, 20, cin, 36, k, 2, thr=True, seed=k * 10 + cin)
+    finally:
+        cuda.set_option("conv_algo", 0)
+
+
 def test_forward_thresholds_and_chunking(cuda, orc):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
@@ -268,7 +292,7 @@ def test_forward_host_equals_forward(cuda):
     torch.cuda.synchronize()
     lg_h, cls_h = net.forward_host(imgs.pin_memory())
     assert torch.equal(lg_h, lg_d.cpu()) and torch.equal(cls_h, cls_d.cpu())
-    assert cuda.forward_launches(net, 9000) == 3 * 6
+    assert cuda.forward_launches(net, 9000) == 3 * 5
 
 
 def test_forward_cifar(cuda, orc):
