@@ -201,6 +201,17 @@ BNN_API bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t*
 BNN_API bnn_status bnn_forward_host(bnn_net* net, const void* h_images, int n, int32_t* h_logits, int32_t* h_cls,
                             bnn_stream_t stream);
 
+/* Latency path for small batches (BASELINE config 1; the paper's protocol PAPER.md:135-137 times
+ * the kernels of one image after its copy to the device).  bnn_net_staging allocates (once) device
+ * staging buffers owned by the net for up to max_staged (<= 256) images and returns them: the
+ * caller writes images to *in ([max_staged, h, w, c] of the net's dtype) and reads *logits
+ * ([max_staged, l_last] int32) / *cls ([max_staged] int32).  bnn_forward_staged(net, n, stream)
+ * runs the forward pass of the first n staged images; the first call for a given n captures the
+ * whole pass into a CUDA graph, later calls replay it as ONE graph launch.  Asynchronous.
+ * Errors: BNN_E_ARG (n > max_staged or no staging), BNN_E_CUDA. */
+BNN_API bnn_status bnn_net_staging(bnn_net* net, int max_staged, void** in, int32_t** logits, int32_t** cls);
+BNN_API bnn_status bnn_forward_staged(bnn_net* net, int n, bnn_stream_t stream);
+
 /* Number of kernel launches one bnn_forward of n images enqueues (for launch accounting). */
 BNN_API int bnn_forward_launches(const bnn_net* net, int n);
 

@@ -69,6 +69,10 @@ def lib():
         L.bnn_forward_host.restype = i
         L.bnn_forward_launches.argtypes = [vp, i]
         L.bnn_forward_launches.restype = i
+        L.bnn_net_staging.argtypes = [vp, i, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)]
+        L.bnn_net_staging.restype = i
+        L.bnn_forward_staged.argtypes = [vp, i, vp]
+        L.bnn_forward_staged.restype = i
         L.bnn_net_profile.argtypes = [vp, i]
         L.bnn_net_profile.restype = i
         L.bnn_net_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), i]
@@ -171,6 +175,18 @@ def dense(x: torch.Tensor, d: int, wt: torch.Tensor, l: int, thr=None, flip=None
     return y, acc, cls
 
 
+class _DeviceBuffer:
+    """A library-owned device buffer exposed through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _alias(ptr: int, shape, typestr: str, device) -> torch.Tensor:
+    return torch.as_tensor(_DeviceBuffer(ptr, shape, typestr), device=device)
+
+
 def forward_launches(net: "Net", n: int) -> int:
     return lib().bnn_forward_launches(net.handle, n)
 
@@ -226,6 +242,22 @@ class Net:
         _check(lib().bnn_forward_host(self.handle, _ptr(images), n, _ptr(logits), _ptr(cls), _stream(stream)),
                "bnn_forward_host")
         return logits, cls
+
+    def staging(self, max_staged: int):
+        """bnn_net_staging: the net's device staging buffers as torch tensors (aliases, no copy):
+        (images [m, h, w, c], logits int32 [m, L], cls int32 [m])."""
+        pin, plog, pcls = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().bnn_net_staging(self.handle, max_staged, ctypes.byref(pin), ctypes.byref(plog),
+                                     ctypes.byref(pcls)), "bnn_net_staging")
+        itype = "|u1" if self.in_dtype == U8 else "<f4"
+        dev = self.device
+        return (_alias(pin.value, (max_staged, self.h, self.w, self.c), itype, dev),
+                _alias(plog.value, (max_staged, self.n_classes), "<i4", dev),
+                _alias(pcls.value, (max_staged,), "<i4", dev))
+
+    def forward_staged(self, n: int, stream=None):
+        """bnn_forward_staged: graph-replayed forward of the first n staged images."""
+        _check(lib().bnn_forward_staged(self.handle, n, _stream(stream)), "bnn_forward_staged")
 
     def profile(self, enable: bool = True) -> int:
         """bnn_net_profile: reset and start (or stop) per-stage event timing."""

@@ -428,6 +428,13 @@ struct bnn_net {
   std::vector<int> pending_stage;  // stage of event pair i (events 2i, 2i+1 of the pool)
   std::vector<double> stage_ms;
   std::vector<int64_t> stage_launches;
+  // graph-replayed staging path (bnn_forward_staged)
+  int max_staged = 0;
+  void* st_in = nullptr;
+  int32_t* st_logits = nullptr;
+  int32_t* st_cls = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  std::vector<cudaGraphExec_t> graphs;  // index n
 };
 
 namespace {
@@ -447,6 +454,12 @@ void net_free(bnn_net* net) {
     if (net->ev_d2h[i]) cudaEventDestroy(net->ev_d2h[i]);
   }
   for (cudaEvent_t e : net->ev_pool) cudaEventDestroy(e);
+  for (cudaGraphExec_t g : net->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  cudaFree(net->st_in);
+  cudaFree(net->st_logits);
+  cudaFree(net->st_cls);
+  if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
   if (net->h2d) cudaStreamDestroy(net->h2d);
   if (net->d2h) cudaStreamDestroy(net->d2h);
   delete net;
@@ -663,6 +676,59 @@ bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits,
                                   (cudaStream_t)stream);
     if (st != BNN_OK) return st;
   }
+  return BNN_OK;
+}
+
+bnn_status bnn_net_staging(bnn_net* net, int max_staged, void** in, int32_t** logits, int32_t** cls) {
+  if (net == nullptr) return fail(BNN_E_ARG, "bnn_net_staging: null net");
+  if (max_staged < 1 || max_staged > 256 || max_staged > net->chunk)
+    return fail(BNN_E_ARG, "bnn_net_staging: max_staged must be in [1, min(256, max_batch)]");
+  if (net->max_staged < max_staged) {
+    for (cudaGraphExec_t g : net->graphs)
+      if (g) cudaGraphExecDestroy(g);
+    net->graphs.clear();
+    cudaFree(net->st_in);
+    cudaFree(net->st_logits);
+    cudaFree(net->st_cls);
+    net->st_in = nullptr; net->st_logits = nullptr; net->st_cls = nullptr; net->max_staged = 0;
+    cudaError_t e = cudaMalloc(&net->st_in, (size_t)(net->img_bytes * max_staged));
+    if (e == cudaSuccess) e = cudaMalloc(&net->st_logits, (size_t)net->L.back().l * max_staged * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&net->st_cls, (size_t)max_staged * 4);
+    if (e == cudaSuccess && net->cap_stream == nullptr) e = cudaStreamCreateWithFlags(&net->cap_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_net_staging: %s", cudaGetErrorString(e));
+    net->max_staged = max_staged;
+    net->graphs.assign(max_staged + 1, nullptr);
+  }
+  if (in) *in = net->st_in;
+  if (logits) *logits = net->st_logits;
+  if (cls) *cls = net->st_cls;
+  return BNN_OK;
+}
+
+bnn_status bnn_forward_staged(bnn_net* net, int n, bnn_stream_t stream) {
+  if (net == nullptr) return fail(BNN_E_ARG, "bnn_forward_staged: null net");
+  if (net->max_staged == 0) return fail(BNN_E_ARG, "bnn_forward_staged: call bnn_net_staging first");
+  if (n < 1 || n > net->max_staged) return fail(BNN_E_ARG, "bnn_forward_staged: n=%d not in [1, %d]", n, net->max_staged);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (net->graphs[n] == nullptr) {
+    const bool prof = net->prof;
+    net->prof = false;
+    cudaError_t e = cudaStreamBeginCapture(net->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { net->prof = prof; return fail(BNN_E_CUDA, "bnn_forward_staged: begin capture: %s", cudaGetErrorString(e)); }
+    bnn_status st = forward_chunk(net, net->st_in, n, net->st_logits, net->st_cls, net->cap_stream);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(net->cap_stream, &graph);
+    net->prof = prof;
+    if (st != BNN_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+    if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_staged: end capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_staged: instantiate: %s", cudaGetErrorString(e));
+    net->graphs[n] = exec;
+  }
+  cudaError_t e = cudaGraphLaunch(net->graphs[n], s);
+  if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_staged: launch: %s", cudaGetErrorString(e));
   return BNN_OK;
 }
 

@@ -295,6 +295,22 @@ def test_forward_host_equals_forward(cuda):
     assert cuda.forward_launches(net, 9000) == 3 * 5
 
 
+def test_forward_staged_graph(cuda, orc):
+    """The graph-replayed latency path (config 1) equals the oracle, for n = 1 and n = 3, and a
+    replay after new images were staged uses the new images."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 1400, max_batch=64)
+    onet = oracle_net(orc, synth.VEHICLE, 1, layers, T)
+    st_in, st_lg, st_cls = net.staging(4)
+    for n, seed in [(1, 1401), (3, 1402), (1, 1403), (3, 1404)]:
+        imgs = synth.images(n, 96, 96, 3, seed)
+        st_in[:n].copy_(imgs.cuda())
+        net.forward_staged(n)
+        torch.cuda.synchronize()
+        ref_l, ref_c = onet.forward(imgs.numpy(), threads=n)
+        assert np.array_equal(st_lg[:n].cpu().numpy(), ref_l)
+        assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
+
+
 def test_forward_cifar(cuda, orc):
     net, layers, T = build_net(cuda, synth.CIFAR, 1, 1200)
     imgs = synth.images(3, 32, 32, 3, 1201)
