@@ -90,6 +90,7 @@ BNN_API int bnn_version(void);
  *                   1 = generic one-word-per-tap conv; 2 = dense-patch kernel; 3 = strip
  *                   kernel (lane = channel); 4 = strip kernel (lane = pixel).
  *   "tiles_per_cta" 0 = automatic (default); k > 0 = every conv CTA walks k output tiles.
+ *   "gemv_max_n"    dense layers over n <= value images use the GEMV kernel (default 16).
  * Results are bit-identical for every setting (tiling invariance is a parity test).
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */
 BNN_API int bnn_set_option(const char* key, int value);

@@ -58,6 +58,7 @@ int num_sms() {
 // tuning / test knobs (bnn_set_option)
 int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap conv
 int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
+int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -298,9 +299,16 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
   A.cls = (l <= 32) ? cls : nullptr;
   A.n = n; A.l = l; A.lw = (l + 31) / 32; A.d = d; A.dw = (d + 31) / 32;
   constexpr int PI = 8, NWARP = 8, DC = 64;
-  dim3 grid((unsigned)((n + PI * NWARP - 1) / (PI * NWARP)), (unsigned)A.lw);
-  dense_kernel<PI, NWARP, DC><<<grid, NWARP * 32, 0, s>>>(A);
-  bnn_status st = check_launch("dense_kernel");
+  bnn_status st;
+  if (n <= g_opt_gemv_max_n) {
+    const int warps = std::min(32, l);
+    dense_gemv_kernel<<<dim3((unsigned)n, (unsigned)A.lw), warps * 32, 0, s>>>(A);
+    st = check_launch("dense_gemv_kernel");
+  } else {
+    dim3 grid((unsigned)((n + PI * NWARP - 1) / (PI * NWARP)), (unsigned)A.lw);
+    dense_kernel<PI, NWARP, DC><<<grid, NWARP * 32, 0, s>>>(A);
+    st = check_launch("dense_kernel");
+  }
   if (st != BNN_OK) return st;
   if (cls != nullptr && l > 32) {
     argmax_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, s>>>(acc, n, l, cls);
@@ -322,6 +330,7 @@ int bnn_set_option(const char* key, int value) {
   if (key == nullptr) return (int)fail(BNN_E_ARG, "bnn_set_option: null key");
   if (strcmp(key, "conv_algo") == 0) { g_opt_conv_algo = value; return BNN_OK; }
   if (strcmp(key, "tiles_per_cta") == 0) { g_opt_tiles_per_cta = value; return BNN_OK; }
+  if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 

@@ -94,6 +94,55 @@ dense_kernel(const DenseArgs A) {
   }
 }
 
+// Small-batch dense (GEMV, the paper's batch-1 case, Section 3.2): one CTA per (image, group of
+// 32 outputs), warp w computes output g*32 + w with its lanes striding over the dw words (16-byte
+// loads when dw % 4 == 0) and one __reduce_add_sync; warp 0 then thresholds, packs (brev(ballot))
+// and takes the argmax.  No image slots are wasted at n = 1 (the GEMM kernel computes 64 per CTA).
+__global__ void __launch_bounds__(1024)
+dense_gemv_kernel(const DenseArgs A) {
+  __shared__ int part[32];
+  const int img = blockIdx.x, g = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int o = g * 32 + warp;
+  int acc = 0;
+  if (o < A.l) {
+    const uint32_t* xr = A.x + (int64_t)img * A.dw;
+    const uint32_t* wr = A.wt + (int64_t)o * A.dw;
+    if ((A.dw & 3) == 0) {
+      const uint4* x4 = reinterpret_cast<const uint4*>(xr);
+      const uint4* w4 = reinterpret_cast<const uint4*>(wr);
+      for (int64_t j = lane; j < (A.dw >> 2); j += 32) {
+        const uint4 a = __ldg(x4 + j), b = __ldg(w4 + j);
+        acc += popc(a.x ^ b.x) + popc(a.y ^ b.y) + popc(a.z ^ b.z) + popc(a.w ^ b.w);
+      }
+    } else {
+      for (int64_t j = lane; j < A.dw; j += 32) acc += popc(__ldg(xr + j) ^ __ldg(wr + j));
+    }
+  }
+  acc = __reduce_add_sync(BNN_FULL_MASK, acc);
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (warp != 0) return;
+  const int oo = g * 32 + lane;
+  const bool ovalid = oo < A.l && lane < (int)(blockDim.x >> 5);
+  const int a = ovalid ? (int)A.d - 2 * part[lane] : 0;
+  if (A.acc != nullptr && ovalid) A.acc[(int64_t)img * A.l + oo] = a;
+  const int t = (A.thr != nullptr && ovalid) ? A.thr[oo] : 0;
+  const bool f = (A.flip != nullptr && ovalid) ? (A.flip[oo] != 0) : false;
+  const uint32_t word = ballot_pack(ovalid && ((a > t) != f));
+  if (A.y != nullptr && lane == 0) A.y[(int64_t)img * A.lw + g] = word;
+  if (A.cls != nullptr) {
+    int bv = ovalid ? a : INT_MIN, bi = ovalid ? oo : INT_MAX;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const int ov = __shfl_xor_sync(BNN_FULL_MASK, bv, s);
+      const int oi = __shfl_xor_sync(BNN_FULL_MASK, bi, s);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) A.cls[img] = bi;
+  }
+}
+
 // argmax over int32 logits [n, l], first maximum wins (R19).  One warp per image.
 __global__ void argmax_kernel(const int32_t* __restrict__ logits, int n, int l, int32_t* __restrict__ cls) {
   const int lane = threadIdx.x & 31;

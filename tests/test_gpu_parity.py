@@ -207,6 +207,16 @@ def test_dense(cuda, orc, n, d, l):
         assert cls[i] == orc.argmax(ra)
 
 
+@pytest.mark.parametrize("gemv_max", [0, 1000])
+@pytest.mark.parametrize("n,d,l", [(3, 18432, 100), (20, 100, 4), (7, 37, 40), (2, 4096, 10)])
+def test_dense_gemv_and_gemm_paths(cuda, orc, gemv_max, n, d, l):
+    try:
+        cuda.set_option("gemv_max_n", gemv_max)
+        test_dense(cuda, orc, n, d, l)
+    finally:
+        cuda.set_option("gemv_max_n", 16)
+
+
 # ------------------------------------------------------------------------------------ forward
 def build_net(cuda, spec, mode, seed, max_batch=4096, thr=False):
     layers = synth.make_weights(spec, mode, seed)
