@@ -14,6 +14,7 @@
 
 #include "bnn.h"
 #include "k_conv.cuh"
+#include "k_conv_tc.cuh"
 #include "k_dense.cuh"
 #include "k_pack.cuh"
 
@@ -59,6 +60,7 @@ int num_sms() {
 int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap conv
 int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
 int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
+int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -179,6 +181,86 @@ bnn_status dispatch_conv_first_lp(int k, int nw, const ConvArgs& A, const uint8_
   return fail(BNN_E_UNSUPPORTED, "conv_first_lp: k=%d nw=%d", k, nw);
 }
 
+// ---- tensor-core (tcgen05 kind::i8) binary conv
+// Resident CTAs per SM of a 256-thread tcgen05 kernel: registers, shared memory (227 KB usable,
+// ~1 KB reserved per CTA) and TMEM columns (512 per SM).
+template <typename F>
+int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols) {
+  if (dyn_smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+  cudaFuncAttributes fa;
+  int regs = 128, static_smem = 2048;
+  if (cudaFuncGetAttributes(&fa, kfn) == cudaSuccess) { regs = fa.numRegs; static_smem = (int)fa.sharedSizeBytes; }
+  (void)cudaGetLastError();
+  const int by_regs = 65536 / (((regs + 7) & ~7) * 256);
+  const int by_smem = (227 * 1024) / ((int)dyn_smem + static_smem + 1024);
+  const int by_tmem = 512 / (int)tmem_cols;
+  return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_tmem, 8)));
+}
+
+template <int K, int NT, bool SRC_U8>
+bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  auto kfn = conv_first_tc_kernel<K, NT, SRC_U8>;
+  static int occ = -1;
+  if (occ < 0) occ = tc_occupancy(kfn, 0, (2 * NT <= 64) ? 64 : (2 * NT <= 128 ? 128 : 256));
+  A.tiles_y = (A.H + 15) / 16;
+  A.tiles_x = (A.W + 7) / 8;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = 0;
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
+  kfn<<<grid, 256, 0, s>>>(A, xu8, T);
+  return check_launch("conv_first_tc_kernel");
+}
+
+// first layer on the tensor cores: strips of K * c_in <= 16 bytes; conv_algo 0 (auto) or 5 (forced)
+bool use_first_tc(int c_in, int k) {
+  if (g_opt_conv_tc == 0 || (g_opt_conv_algo != 0 && g_opt_conv_algo != 5)) return false;
+  return (k == 3 || k == 5 || k == 7) && c_in < 32 && k * c_in <= 16;
+}
+
+template <bool SRC_U8>
+bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  const bool wide = A.c_out > 32;
+  switch (k) {
+    case 3: return wide ? launch_conv_first_tc_t<3, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<3, 32, SRC_U8>(A, xu8, T, s);
+    case 5: return wide ? launch_conv_first_tc_t<5, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<5, 32, SRC_U8>(A, xu8, T, s);
+    case 7: return wide ? launch_conv_first_tc_t<7, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<7, 32, SRC_U8>(A, xu8, T, s);
+  }
+  return fail(BNN_E_UNSUPPORTED, "conv_first_tc: k=%d", k);
+}
+
+template <int K, int CW, int NT>
+bnn_status launch_conv_tc_t(ConvArgs A, cudaStream_t s) {
+  using C = ConvTcCfg<K, CW, NT>;
+  auto kfn = conv_tc_kernel<K, CW, NT>;
+  static int occ = -1;  // CTAs per SM for this instantiation (smem / TMEM bound)
+  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.tiles_per_cta = 0;
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
+  kfn<<<grid, 256, C::SMEM, s>>>(A);
+  return check_launch("conv_tc_kernel");
+}
+
+// (k, words per pixel) -> tensor-core instantiation; returns false if none applies
+bool tc_supported(int k, int cw) {
+  if (g_opt_conv_tc == 0) return false;
+  return (k == 5 && (cw == 1 || cw == 2)) || (k == 3 && (cw == 1 || cw == 2 || cw == 4)) || (k == 7 && cw == 1);
+}
+
+bnn_status dispatch_conv_tc(int k, int cw, const ConvArgs& A, cudaStream_t s) {
+  if (k == 5 && cw == 1) return launch_conv_tc_t<5, 1, 32>(A, s);
+  if (k == 5 && cw == 2) return launch_conv_tc_t<5, 2, 64>(A, s);
+  if (k == 3 && cw == 1) return launch_conv_tc_t<3, 1, 32>(A, s);
+  if (k == 3 && cw == 2) return launch_conv_tc_t<3, 2, 64>(A, s);
+  if (k == 3 && cw == 4) return launch_conv_tc_t<3, 4, 128>(A, s);
+  if (k == 7 && cw == 1) return launch_conv_tc_t<7, 1, 32>(A, s);
+  return fail(BNN_E_UNSUPPORTED, "conv_tc: k=%d cw=%d", k, cw);
+}
+
 template <int K, int WY, int WX>
 bnn_status launch_conv_real_u8_t(RealConvArgs A, cudaStream_t s) {
   constexpr int PR = 2, PC = 8;
@@ -273,7 +355,9 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
     A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
     A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
     A.cwo = (c_out + 31) / 32; A.pool = pool;
+    if (use_first_tc(c_in, k)) return dispatch_conv_first_tc<false>(k, A, nullptr, nullptr, s);
     if (use_first_lp(c_in, k)) return dispatch_conv_first_lp<false>(k, strip_words(c_in, k), A, nullptr, nullptr, s);
+    if (c_in >= 32 && tc_supported(k, A.cw)) return dispatch_conv_tc(k, A.cw, A, s);
     if (use_strip(c_in, k))
       return small ? dispatch_conv_strip<4, 1, false>(k, A, nullptr, nullptr, s)
                    : dispatch_conv_strip<4, 2, false>(k, A, nullptr, nullptr, s);
@@ -331,6 +415,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_algo") == 0) { g_opt_conv_algo = value; return BNN_OK; }
   if (strcmp(key, "tiles_per_cta") == 0) { g_opt_tiles_per_cta = value; return BNN_OK; }
   if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
+  if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 
@@ -516,7 +601,7 @@ struct ProfScope {
 bool fused_input(const bnn_net* net) {
   if (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) return false;
   if (net->in_dt != BNN_U8 || net->c > 4 || net->L[0].kind != 1) return false;
-  return use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
+  return use_first_tc(net->c, net->L[0].k) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
 }
 
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
@@ -535,7 +620,9 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
     const bool small = (P.W <= 8 || P.H <= 8);
     bnn_status st;
-    if (use_first_lp(P.c_in, P.k))
+    if (use_first_tc(P.c_in, P.k))
+      st = dispatch_conv_first_tc<true>(P.k, A, (const uint8_t*)images, T, s);
+    else if (use_first_lp(P.c_in, P.k))
       st = dispatch_conv_first_lp<true>(P.k, strip_words(P.c_in, P.k), A, (const uint8_t*)images, T, s);
     else
       st = small ? dispatch_conv_strip<4, 1, true>(P.k, A, (const uint8_t*)images, T, s)

@@ -108,8 +108,27 @@ def conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=False, flip=False, see
     (1, 4, 6, 32, 32, 5, 1),      # map smaller than the kernel reach
     (1, 32, 32, 3, 128, 3, 1),    # CIFAR conv1 (27-bit patch)
 ])
-def test_conv_binary(cuda, orc, n, h, w, cin, cout, k, pool):
-    conv_case(cuda, orc, n, h, w, cin, cout, k, pool, seed=h + cin + k)
+@pytest.mark.parametrize("tc", [1, 0])
+def test_conv_binary(cuda, orc, n, h, w, cin, cout, k, pool, tc):
+    """tc = 1: layers with c_in >= 32 run on the tensor cores (tcgen05 kind::i8) where an
+    instantiation exists; tc = 0: everything on the XOR-popcount integer path."""
+    try:
+        cuda.set_option("conv_tc", tc)
+        conv_case(cuda, orc, n, h, w, cin, cout, k, pool, seed=h + cin + k)
+    finally:
+        cuda.set_option("conv_tc", 1)
+
+
+@pytest.mark.parametrize("n,h,w,cin,cout,k,pool", [
+    (3, 48, 48, 32, 32, 5, 2),    # vehicle conv2 on tcgen05
+    (1, 16, 16, 64, 70, 5, 2),    # c_out > NT: two channel tiles, ragged
+    (1, 13, 11, 40, 36, 3, 1),    # cw = 2 with pad channels, ragged map
+    (1, 16, 24, 128, 128, 3, 2),  # cw = 4, NT = 128
+    (1, 14, 10, 32, 33, 7, 1),    # k = 7
+    (5, 24, 16, 64, 64, 5, 1),    # many tiles per CTA (double-buffered TMEM accumulators)
+])
+def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool):
+    conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=True, flip=True, seed=900 + h + k)
 
 
 @pytest.mark.parametrize("cin,k", [(3, 5), (32, 3)])
@@ -117,7 +136,7 @@ def test_conv_threshold_flip(cuda, orc, cin, k):
     conv_case(cuda, orc, 2, 16, 16, cin, 40, k, 2, thr=True, flip=True, seed=7)
 
 
-@pytest.mark.parametrize("algo,tpc", [(1, 0), (2, 0), (3, 0), (4, 0), (0, 1), (0, 3), (1, 7), (3, 5), (4, 2)])
+@pytest.mark.parametrize("algo,tpc", [(1, 0), (2, 0), (3, 0), (4, 0), (5, 0), (0, 1), (0, 3), (1, 7), (3, 5), (4, 2)])
 def test_conv_tiling_invariance(cuda, orc, algo, tpc):
     """Launch configuration does not change a single bit (and the generic kernel agrees with
     the dense-patch kernel on the first layer)."""
@@ -260,7 +279,7 @@ def test_forward_vehicle(cuda, orc, mode):
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
 
 
-@pytest.mark.parametrize("algo", [1, 2, 3])
+@pytest.mark.parametrize("algo", [1, 2, 3, 4])
 @pytest.mark.parametrize("mode", [1, 0])
 def test_forward_vehicle_unfused_first_layer(cuda, orc, mode, algo):
     """The same net through the separate pack kernel + generic (1) / dense-patch (2) first layer."""
@@ -271,7 +290,7 @@ def test_forward_vehicle_unfused_first_layer(cuda, orc, mode, algo):
         cuda.set_option("conv_algo", 0)
 
 
-@pytest.mark.parametrize("algo", [3, 4])
+@pytest.mark.parametrize("algo", [3, 4, 5])
 @pytest.mark.parametrize("k", [3, 5, 7])
 @pytest.mark.parametrize("cin", [1, 2, 3, 4, 6])
 def test_conv_strip_shapes(cuda, orc, k, cin, algo):
