@@ -155,6 +155,64 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+
+def read_peaks():
+    """MEASURED_PEAKS.json (driver-written) else the B200_PROFILING.md fallback."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return {"hbm_gbs": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained",
+                    d["bf16_tflops"]), "source": "measured (MEASURED_PEAKS.json)"}
+        except (ValueError, KeyError):
+            pass
+    return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def dominant_roofline(net, spec, mode, stage_ms, stage_launch, images_total, clocks, dev):
+    """Roofline object for the conv layer with the largest live CUDA-event time.
+    POPC-path kernels: algorithmic popcounts / time vs the POPC pipe (16/clk/SM measured, x SMs x max clock).
+    tcgen05 kernels: algorithmic int8 ops (2 x binary MACs) / time vs the int8 dense tensor peak =
+    measured bf16 (sustained: the kernel runs inside a long step) x 2 (nominal i8 : bf16 ratio)."""
+    import torch
+    popc_img, mac_img = conv_popc_per_image(spec, mode)
+    conv_stages = [i for i, Ly in enumerate(spec["layers"]) if Ly["kind"] == "conv"]
+    dom = max(conv_stages, key=lambda i: stage_ms[i + 1])
+    launches = max(1, stage_launch[dom + 1])
+    ms_per_launch = stage_ms[dom + 1] / launches
+    imgs_per_launch = images_total / launches
+    kernel = net.layer_kernel(dom, int(imgs_per_launch))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    peaks = read_peaks()
+    if "_tc_" in kernel:
+        achieved = 2.0 * mac_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3)
+        peak = 2.0 * peaks["bf16_sustained"] * 1e12
+        r = {"bound": "tensor", "pipe": "tcgen05 kind::i8", "unit": "TOPS (int8, 2 x binary MAC)",
+             "peak_basis": "int8 dense = 2 x bf16 sustained %.1f TFLOP/s, %s" % (peaks["bf16_sustained"], peaks["source"]),
+             "popc_equivalent_frac": popc_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3) /
+                                     (POPC_PER_CLK_SM * sms * sm_max * 1e6)}
+    else:
+        achieved = popc_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3)
+        peak = POPC_PER_CLK_SM * sms * sm_max * 1e6
+        r = {"bound": "alu", "pipe": "POPC (16/clk/SM, measured: profiles/pipe_probe_r01.txt)", "unit": "Tpopc/s",
+             "peak_basis": "16 POPC/clk/SM x %d SMs x %.0f MHz (sm max clock)" % (sms, sm_max)}
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile)).get("layer%d" % dom)
+            if tj and kernel in tj["kernel"]:
+                traffic = tj["dram_bytes_per_launch"] * imgs_per_launch / tj["images_per_launch"]
+        except (ValueError, KeyError):
+            traffic = None
+    step_ms = sum(stage_ms)
+    r.update({"kernel": "layer%d %s" % (dom, kernel), "achieved": achieved / 1e12, "peak": peak / 1e12,
+              "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
+              "images_per_launch": imgs_per_launch,
+              "kernel_share_of_step": stage_ms[dom + 1] / step_ms if step_ms else None})
+    return r
+
 # ----------------------------------------------------------------------------------- reference arm
 def run_reference(a, rank, world):
     """The reference arm: the CPU oracle on the host cores, same metric/config, each step a bounded
@@ -264,32 +322,7 @@ def main():
     value = world * B / (ms * 1e-3)
 
     # ---- roofline of the dominant conv kernel (live CUDA-event times of its launches)
-    popc_img, mac_img = conv_popc_per_image(spec, mode)
-    conv_stages = [i for i, Ly in enumerate(spec["layers"]) if Ly["kind"] == "conv"]
-    dom = max(conv_stages, key=lambda i: stage_ms[i + 1])
-    dom_ms_per_launch = stage_ms[dom + 1] / max(1, stage_launch[dom + 1])
-    imgs_per_launch = B * a.steps / max(1, stage_launch[dom + 1])
-    achieved = popc_img[dom] * imgs_per_launch / (dom_ms_per_launch * 1e-3)
-    sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak = POPC_PER_CLK_SM * torch.cuda.get_device_properties(dev).multi_processor_count * sm_max * 1e6
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            tj = json.load(open(tfile))
-            k = "layer%d" % dom
-            if k in tj:
-                traffic = tj[k]["dram_bytes_per_launch"] * (imgs_per_launch / tj[k]["images_per_launch"])
-        except (ValueError, KeyError):
-            traffic = None
-    step_ms_total = sum(stage_ms) / a.steps
-    roofline = {"bound": "alu", "pipe": "POPC (16/clk/SM, measured)", "kernel": "layer%d conv (%s)" % (
-        dom, "dense-patch" if dom == 0 else "conv_bin_kernel"), "achieved": achieved / 1e12, "peak": peak / 1e12,
-        "unit": "Tpopc/s", "frac": achieved / peak, "traffic": traffic,
-        "peak_basis": "16 POPC/clk/SM x %d SMs x %.0f MHz (sm max clock)" % (
-            torch.cuda.get_device_properties(dev).multi_processor_count, sm_max),
-        "kernel_share_of_step": stage_ms[dom + 1] / a.steps / step_ms_total if step_ms_total else None,
-        "ms_per_launch": dom_ms_per_launch, "images_per_launch": imgs_per_launch}
+    roofline = dominant_roofline(net, spec, mode, stage_ms, stage_launch, B * a.steps, clocks, dev)
     stages = {("pack" if i == 0 else ("layer%d" % (i - 1) if i <= len(spec["layers"]) else "argmax")):
               round(stage_ms[i] / a.steps, 4) for i in range(len(stage_ms)) if stage_launch[i]}
 
@@ -339,6 +372,7 @@ def main():
                "sample": "%d vehicle images (%s), %.1f s on %d threads, one image per thread" % (done, a.mode, el, cores)}
 
     launches = bnn.forward_launches(net, B) * a.steps
+    _, mac_img = conv_popc_per_image(spec, mode)
     tot_mac = sum(mac_img) * B * world
     line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

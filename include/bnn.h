@@ -213,6 +213,11 @@ BNN_API bnn_status bnn_forward_host(bnn_net* net, const void* h_images, int n, i
 BNN_API bnn_status bnn_net_staging(bnn_net* net, int max_staged, void** in, int32_t** logits, int32_t** cls);
 BNN_API bnn_status bnn_forward_staged(bnn_net* net, int n, bnn_stream_t stream);
 
+/* Name of the CUDA kernel family bnn_forward uses for `layer` when running n images (e.g.
+ * "conv_tc_kernel", "conv_first_tc_kernel", "conv_bin_kernel", "dense_kernel"); "" if out of range.
+ * For measurement labelling (bench.py roofline) and tests. */
+BNN_API const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n);
+
 /* Number of kernel launches one bnn_forward of n images enqueues (for launch accounting). */
 BNN_API int bnn_forward_launches(const bnn_net* net, int n);
 

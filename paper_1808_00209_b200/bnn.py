@@ -73,6 +73,8 @@ def lib():
         L.bnn_net_staging.restype = i
         L.bnn_forward_staged.argtypes = [vp, i, vp]
         L.bnn_forward_staged.restype = i
+        L.bnn_net_layer_kernel.argtypes = [vp, i, i]
+        L.bnn_net_layer_kernel.restype = ctypes.c_char_p
         L.bnn_net_profile.argtypes = [vp, i]
         L.bnn_net_profile.restype = i
         L.bnn_net_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), i]
@@ -258,6 +260,10 @@ class Net:
     def forward_staged(self, n: int, stream=None):
         """bnn_forward_staged: graph-replayed forward of the first n staged images."""
         _check(lib().bnn_forward_staged(self.handle, n, _stream(stream)), "bnn_forward_staged")
+
+    def layer_kernel(self, layer: int, n: int) -> str:
+        """bnn_net_layer_kernel: the kernel family layer `layer` runs on for a batch of n."""
+        return lib().bnn_net_layer_kernel(self.handle, layer, n).decode()
 
     def profile(self, enable: bool = True) -> int:
         """bnn_net_profile: reset and start (or stop) per-stage event timing."""

@@ -15,6 +15,7 @@
 #include "bnn.h"
 #include "k_conv.cuh"
 #include "k_conv_tc.cuh"
+#include "k_conv_first_tc.cuh"
 #include "k_dense.cuh"
 #include "k_pack.cuh"
 
@@ -110,6 +111,9 @@ bnn_status launch_conv_bin_t(ConvArgs A, cudaStream_t s) {
   A.tiles_y = (A.H + TH - 1) / TH;
   A.tiles_x = (A.W + TW - 1) / TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = choose_tpc(A.total_tiles, A.cw > CWC);
   const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
   if (gx > 0x7fffffff) return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: too many tiles");
@@ -125,6 +129,9 @@ bnn_status launch_conv_patch_t(ConvArgs A, cudaStream_t s) {
   A.tiles_y = (A.H + TH - 1) / TH;
   A.tiles_x = (A.W + TW - 1) / TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = choose_tpc(A.total_tiles, false);
   const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
   dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
@@ -139,6 +146,9 @@ bnn_status launch_conv_strip_t(ConvArgs A, const uint8_t* xu8, const float* T, c
   A.tiles_y = (A.H + TH - 1) / TH;
   A.tiles_x = (A.W + TW - 1) / TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = choose_tpc(A.total_tiles, false);
   const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
   dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
@@ -162,6 +172,9 @@ bnn_status launch_conv_first_lp_t(ConvArgs A, const uint8_t* xu8, const float* T
   A.tiles_y = (A.H + TH - 1) / TH;
   A.tiles_x = (A.W + TW - 1) / TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = choose_tpc(A.total_tiles, false);
   const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
   dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
@@ -197,14 +210,18 @@ int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols) {
   return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_tmem, 8)));
 }
 
-template <int K, int NT, bool SRC_U8>
+template <int K, int NT, int CIN, bool SRC_U8>
 bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  auto kfn = conv_first_tc_kernel<K, NT, SRC_U8>;
+  auto kfn = conv_first_tc_kernel<K, NT, CIN, SRC_U8>;
   static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, 0, (2 * NT <= 64) ? 64 : (2 * NT <= 128 ? 128 : 256));
-  A.tiles_y = (A.H + 15) / 16;
-  A.tiles_x = (A.W + 7) / 8;
+  using C = FirstTcCfg<K, NT, CIN, SRC_U8>;
+  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = 0;
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
@@ -212,21 +229,32 @@ bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T
   return check_launch("conv_first_tc_kernel");
 }
 
-// first layer on the tensor cores: strips of K * c_in <= 16 bytes; conv_algo 0 (auto) or 5 (forced)
-bool use_first_tc(int c_in, int k) {
+// First layer on the tensor cores: strips of K * c_in <= 16 int8.  Instantiated (k, c_in) pairs:
+// packed input k=3: c_in 1..5, k=5: 1..3, k=7: 1..2; fused u8 input: c_in = 3, k = 3 or 5.
+// conv_algo 0 (auto) or 5 (forced).
+bool use_first_tc(int c_in, int k, bool u8) {
   if (g_opt_conv_tc == 0 || (g_opt_conv_algo != 0 && g_opt_conv_algo != 5)) return false;
-  return (k == 3 || k == 5 || k == 7) && c_in < 32 && k * c_in <= 16;
+  if (u8) return c_in == 3 && (k == 3 || k == 5);
+  return (k == 3 && c_in >= 1 && c_in <= 5) || (k == 5 && c_in >= 1 && c_in <= 3) || (k == 7 && c_in >= 1 && c_in <= 2);
 }
 
 template <bool SRC_U8>
 bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   const bool wide = A.c_out > 32;
-  switch (k) {
-    case 3: return wide ? launch_conv_first_tc_t<3, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<3, 32, SRC_U8>(A, xu8, T, s);
-    case 5: return wide ? launch_conv_first_tc_t<5, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<5, 32, SRC_U8>(A, xu8, T, s);
-    case 7: return wide ? launch_conv_first_tc_t<7, 128, SRC_U8>(A, xu8, T, s) : launch_conv_first_tc_t<7, 32, SRC_U8>(A, xu8, T, s);
+  const int c = A.c_in;
+#define BNN_FTC(KK, CC)                                                                           \
+  if (k == KK && c == CC)                                                                          \
+    return wide ? launch_conv_first_tc_t<KK, 128, CC, SRC_U8>(A, xu8, T, s)                       \
+                : launch_conv_first_tc_t<KK, 32, CC, SRC_U8>(A, xu8, T, s)
+  if constexpr (SRC_U8) {
+    BNN_FTC(3, 3); BNN_FTC(5, 3);
+  } else {
+    BNN_FTC(3, 1); BNN_FTC(3, 2); BNN_FTC(3, 3); BNN_FTC(3, 4); BNN_FTC(3, 5);
+    BNN_FTC(5, 1); BNN_FTC(5, 2); BNN_FTC(5, 3);
+    BNN_FTC(7, 1); BNN_FTC(7, 2);
   }
-  return fail(BNN_E_UNSUPPORTED, "conv_first_tc: k=%d", k);
+#undef BNN_FTC
+  return fail(BNN_E_UNSUPPORTED, "conv_first_tc: k=%d c_in=%d", k, c);
 }
 
 template <int K, int CW, int NT>
@@ -238,6 +266,9 @@ bnn_status launch_conv_tc_t(ConvArgs A, cudaStream_t s) {
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = 0;
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
@@ -269,6 +300,9 @@ bnn_status launch_conv_real_u8_t(RealConvArgs A, cudaStream_t s) {
   A.tiles_y = (A.H + TH - 1) / TH;
   A.tiles_x = (A.W + TW - 1) / TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = choose_tpc(A.total_tiles, false);
   const int nb = K * K * A.c_in, nw = (nb + 3) / 4;
   const size_t in_bytes = (size_t)((IR * IC * A.c_in + 15) & ~15);
@@ -355,7 +389,7 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
     A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
     A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
     A.cwo = (c_out + 31) / 32; A.pool = pool;
-    if (use_first_tc(c_in, k)) return dispatch_conv_first_tc<false>(k, A, nullptr, nullptr, s);
+    if (use_first_tc(c_in, k, false)) return dispatch_conv_first_tc<false>(k, A, nullptr, nullptr, s);
     if (use_first_lp(c_in, k)) return dispatch_conv_first_lp<false>(k, strip_words(c_in, k), A, nullptr, nullptr, s);
     if (c_in >= 32 && tc_supported(k, A.cw)) return dispatch_conv_tc(k, A.cw, A, s);
     if (use_strip(c_in, k))
@@ -372,6 +406,18 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
   const int64_t work = (int64_t)n * (h / pool) * (w / pool) * A.cwo * 32;
   conv_real_f32_kernel<<<grid_for(work, 256), 256, 0, s>>>(A, k);
   return check_launch("conv_real_f32_kernel");
+}
+
+// The kernel family launch_conv / the fused first layer pick (kept in step with the dispatch above).
+const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
+  if (x_dt == BNN_U8) return "conv_real_u8_kernel";
+  if (x_dt == BNN_F32) return "conv_real_f32_kernel";
+  if (use_first_tc(c_in, k, false)) return "conv_first_tc_kernel";
+  if (use_first_lp(c_in, k)) return "conv_first_lp_kernel";
+  if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) return "conv_tc_kernel";
+  if (use_strip(c_in, k)) return "conv_strip_kernel";
+  if (use_patch(c_in, k)) return "conv_patch_kernel";
+  return "conv_bin_kernel";
 }
 
 // ---------------------------------------------------------------------------- dense
@@ -601,7 +647,7 @@ struct ProfScope {
 bool fused_input(const bnn_net* net) {
   if (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) return false;
   if (net->in_dt != BNN_U8 || net->c > 4 || net->L[0].kind != 1) return false;
-  return use_first_tc(net->c, net->L[0].k) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
+  return use_first_tc(net->c, net->L[0].k, true) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
 }
 
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
@@ -620,7 +666,7 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
     const bool small = (P.W <= 8 || P.H <= 8);
     bnn_status st;
-    if (use_first_tc(P.c_in, P.k))
+    if (use_first_tc(P.c_in, P.k, true))
       st = dispatch_conv_first_tc<true>(P.k, A, (const uint8_t*)images, T, s);
     else if (use_first_lp(P.c_in, P.k))
       st = dispatch_conv_first_lp<true>(P.k, strip_words(P.c_in, P.k), A, (const uint8_t*)images, T, s);
@@ -826,6 +872,13 @@ bnn_status bnn_forward_staged(bnn_net* net, int n, bnn_stream_t stream) {
   cudaError_t e = cudaGraphLaunch(net->graphs[n], s);
   if (e != cudaSuccess) return fail(BNN_E_CUDA, "bnn_forward_staged: launch: %s", cudaGetErrorString(e));
   return BNN_OK;
+}
+
+const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
+  if (net == nullptr || layer < 0 || layer >= (int)net->L.size()) return "";
+  const LayerPlan& P = net->L[layer];
+  if (P.kind == 2) return std::min(n, net->chunk) <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
+  return conv_kernel_name(P.x_dt, P.c_in, P.k);
 }
 
 int bnn_forward_launches(const bnn_net* net, int n) {

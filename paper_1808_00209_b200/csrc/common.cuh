@@ -23,6 +23,29 @@ BNN_DEV int dp4a_us(uint32_t a, uint32_t b, int c) {
   return d;
 }
 
+// Division by a runtime-invariant divisor d (1 <= d < 2^31) for numerators n < 2^31, as a
+// multiply-high + add + shift (Granlund-Montgomery): l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1, q = (umulhi(m, n) + n) >> l.  Built on the host.
+struct FastDiv {
+  uint32_t d, m, l;
+  __host__ __device__ FastDiv() : d(1), m(1), l(0) {}
+  __host__ explicit FastDiv(uint32_t div) : d(div) {
+    l = 0;
+    while ((1ull << l) < div) ++l;
+    m = (uint32_t)((((1ull << l) - div) << 32) / div + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(m, n) + n) >> l; }
+};
+
+// For u8 x: (x > t) <=> (x > u8_threshold(t)) exactly (R14): x integer, so x > t <=> x > floor(t);
+// clamped to [-1, 255]; NaN t (never true) -> 255.
+BNN_DEV int u8_threshold(float t) {
+  if (!(t == t)) return 255;
+  if (t < -1.0f) return -1;
+  if (t >= 255.0f) return 255;
+  return (int)floorf(t);
+}
+
 BNN_DEV int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 BNN_DEV int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 

@@ -31,9 +31,22 @@ struct ConvArgs {
   int32_t* acc;        // [n, H, W, c_out] or null
   int n, H, W, cw, c_in, c_out, cwo, pool;
   int tiles_x, tiles_y;
-  int64_t total_tiles;
+  int64_t total_tiles;  // < 2^31 (checked by the host)
   int tiles_per_cta;
+  FastDiv fd_img, fd_tx;  // division by tiles_x * tiles_y and by tiles_x
 };
+
+// tile index -> (image, tile row, tile column), two multiply-high divisions
+template <typename Args>
+BNN_DEV void tile_coords(const Args& A, int64_t tile, int& img, int& ty, int& tx) {
+  const uint32_t t = (uint32_t)tile;
+  const uint32_t im = A.fd_img.div(t);
+  const uint32_t rem = t - im * (uint32_t)(A.tiles_x * A.tiles_y);
+  const uint32_t y = A.fd_tx.div(rem);
+  img = (int)im;
+  ty = (int)y;
+  tx = (int)(rem - y * (uint32_t)A.tiles_x);
+}
 
 // Epilogue shared by the binary conv kernels: threshold + pack (+ OR-pool) + stores.
 // a[r][p] holds the exact integer accumulator of output pixel (oy0+r, ox0+p), channel o.
@@ -121,12 +134,10 @@ conv_bin_kernel(const ConvArgs A) {
 
   const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
   const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
-  const int tiles_img = A.tiles_x * A.tiles_y;
 
   for (int64_t tile = t_begin; tile < t_end; ++tile) {
-    const int img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int img, ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     const int oy0 = ty * TH, ox0 = tx * TW;
 
     int acc[PR][PC];
@@ -240,12 +251,10 @@ conv_patch_kernel(const ConvArgs A) {
 
   const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
   const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
-  const int tiles_img = A.tiles_x * A.tiles_y;
 
   for (int64_t tile = t_begin; tile < t_end; ++tile) {
-    const int img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int img, ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     const int oy0 = ty * TH, ox0 = tx * TW;
 
     __syncthreads();  // previous tile's readers are done
@@ -344,11 +353,11 @@ conv_strip_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float
   const int nbits = K * K * cin;
 
   // thresholds for the fused u8 path: bit_c = x_c > t_c
-  float tc[4] = {0.f, 0.f, 0.f, 0.f};
+  int ti[4] = {0, 0, 0, 0};  // u8 bit_c = x_c > ti_c  (SIGN: x > 0)
   if (SRC_U8 && Tt != nullptr) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (c < cin) tc[c] = -Tt[c];
+      if (c < cin) ti[c] = u8_threshold(-Tt[c]);
   }
 
   // this lane's weights in the strip layout
@@ -371,12 +380,10 @@ conv_strip_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float
 
   const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
   const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
-  const int tiles_img = A.tiles_x * A.tiles_y;
 
   for (int64_t tile = t_begin; tile < t_end; ++tile) {
-    const int img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int img, ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     const int oy0 = ty * TH, ox0 = tx * TW;
 
     // phase A: one warp per halo row: lane = halo column -> c_in-bit code -> K-tap strips
@@ -389,7 +396,7 @@ conv_strip_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float
           const uint8_t* px = xu8 + pix * cin;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (c < cin) code |= (uint32_t)((float)px[c] > tc[c]) << (cin - 1 - c);
+            if (c < cin) code |= (uint32_t)((int)px[c] > ti[c]) << (cin - 1 - c);
         } else {
           code = __ldg(A.x + pix) >> (32 - cin);
         }
@@ -507,23 +514,21 @@ conv_first_lp_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
     if (lane == 0) flipmask_s = fm;
   }
 
-  float tc[4] = {0.f, 0.f, 0.f, 0.f};
+  int ti[4] = {0, 0, 0, 0};  // u8 bit_c = x_c > ti_c  (SIGN: x > 0)
   if (SRC_U8 && Tt != nullptr) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (c < cin) tc[c] = -Tt[c];
+      if (c < cin) ti[c] = u8_threshold(-Tt[c]);
   }
   __syncthreads();
   const uint32_t flipmask = flipmask_s;
 
   const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
   const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
-  const int tiles_img = A.tiles_x * A.tiles_y;
 
   for (int64_t tile = t_begin; tile < t_end; ++tile) {
-    const int img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int img, ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     const int oy0 = ty * TH, ox0 = tx * TW;
 
     __syncthreads();  // previous tile's readers of codes / strips are done
@@ -537,7 +542,7 @@ conv_first_lp_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
           const uint8_t* px = xu8 + pix * cin;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (c < cin) code |= (uint32_t)((float)px[c] > tc[c]) << (cin - 1 - c);
+            if (c < cin) code |= (uint32_t)((int)px[c] > ti[c]) << (cin - 1 - c);
         } else {
           code = __ldg(A.x + pix) >> (32 - cin);
         }
@@ -628,6 +633,7 @@ struct RealConvArgs {
   int tiles_x, tiles_y;
   int64_t total_tiles;
   int tiles_per_cta;
+  FastDiv fd_img, fd_tx;
 };
 
 template <int K, int PR, int PC, int WY, int WX>
@@ -680,13 +686,11 @@ conv_real_u8_kernel(const RealConvArgs A) {
 
   const int64_t t_begin = (int64_t)blockIdx.x * A.tiles_per_cta;
   const int64_t t_end = min(t_begin + A.tiles_per_cta, A.total_tiles);
-  const int tiles_img = A.tiles_x * A.tiles_y;
   const uint8_t* xall = reinterpret_cast<const uint8_t*>(A.x);
 
   for (int64_t tile = t_begin; tile < t_end; ++tile) {
-    const int img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int img, ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     const int oy0 = ty * TH, ox0 = tx * TW;
     __syncthreads();
     const uint8_t* xin = xall + (int64_t)img * A.H * A.W * cin;

@@ -42,9 +42,11 @@ BNN_DEV void expand_word(uint32_t w, const uint32_t* lut, uint32_t (&o)[8]) {
 // 32w..32w+31 = output pixels m of the tile.  Waits for the tile's MMAs, reads 32 channel sums at a
 // time (tcgen05.ld 32x32b.x32), thresholds them into one packed word per pixel (Eq. 1 + Eq. 2),
 // ORs 2x2 pixels for the fused pool (lanes m^1 and m^8 are the neighbours), stores.
+// col_base: first TMEM column of the tile's accumulator; warp = TMEM lane quarter (0..3);
+// (oy0, ox0): output origin of this 16 x 8 block.
 template <int NT>
-BNN_DEV void tc_epilogue(const ConvArgs& A, uint32_t tmem, int buf, uint32_t phase, uint64_t* bar, int g, int img,
-                         int oy0, int ox0, int warp, int lane, const int32_t* s_thr, const uint32_t* s_flip) {
+BNN_DEV void tc_epilogue(const ConvArgs& A, uint32_t tmem, uint32_t col_base, uint32_t phase, uint64_t* bar, int g,
+                         int img, int oy0, int ox0, int warp, int lane, const int32_t* s_thr, const uint32_t* s_flip) {
   constexpr int TW = 8;
   tc::mbar_wait(bar, phase);
   tc::fence_after();
@@ -54,12 +56,18 @@ BNN_DEV void tc_epilogue(const ConvArgs& A, uint32_t tmem, int buf, uint32_t pha
 #pragma unroll 1
   for (int c0 = 0; c0 < NT && g * NT + c0 < A.c_out; c0 += 32) {
     int v[32];
-    tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * NT + c0), v);
+    tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + col_base + (uint32_t)c0, v);
+    int th[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int4 t4 = reinterpret_cast<const int4*>(s_thr + c0)[q];
+      th[4 * q] = t4.x; th[4 * q + 1] = t4.y; th[4 * q + 2] = t4.z; th[4 * q + 3] = t4.w;
+    }
     tc::tmem_ld_wait();
+    // bit_c = v_c > thr_c  <=>  thr_c - v_c < 0: shift the sign bits in, channel 0 ends at bit 31
     uint32_t word = 0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (v[c] > s_thr[c0 + c]) word |= 1u << (31 - c);
+    for (int c = 0; c < 32; ++c) word = __funnelshift_l((uint32_t)(th[c] - v[c]), word, 1);
     const int nvalid = A.c_out - (g * NT + c0);
     const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
     word = (word ^ s_flip[c0 / 32]) & vmask;
@@ -109,7 +117,8 @@ conv_tc_kernel(const ConvArgs A) {
   }
   if (tid < NT) {
     const int o = g * NT + tid;
-    s_thr[tid] = (o < A.c_out && A.thr != nullptr) ? A.thr[o] : 0;
+    // clamped to +-2^30: |acc| <= 2^20 here, so thr - acc never overflows and the compare is unchanged
+    s_thr[tid] = (o < A.c_out && A.thr != nullptr) ? max(-(1 << 30), min(1 << 30, A.thr[o])) : 0;
   }
   if (warp < NT / 32) {
     const int o = g * NT + warp * 32 + lane;
@@ -150,13 +159,11 @@ conv_tc_kernel(const ConvArgs A) {
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  const int tiles_img = A.tiles_x * A.tiles_y;
   constexpr uint32_t idesc = tc::idesc_i8(128, NT);
 
   auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
-    img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
+    int ty, tx;
+    tile_coords(A, tile, img, ty, tx);
     oy0 = ty * TH;
     ox0 = tx * TW;
   };
@@ -164,7 +171,7 @@ conv_tc_kernel(const ConvArgs A) {
   auto epilogue = [&](int64_t tile, int buf, uint32_t phase) {
     int img, oy0, ox0;
     tile_origin(tile, img, oy0, ox0);
-    tc_epilogue<NT>(A, tmem, buf, phase, &bar[buf], g, img, oy0, ox0, warp, lane, s_thr, s_flip);
+    tc_epilogue<NT>(A, tmem, (uint32_t)(buf * NT), phase, &bar[buf], g, img, oy0, ox0, warp, lane, s_thr, s_flip);
   };
 
   // The packed input words of the next tile are loaded into registers (pref) right after the
@@ -211,18 +218,18 @@ conv_tc_kernel(const ConvArgs A) {
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (tid == 0) {
-      const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
-      uint32_t accumulate = 0;
-#pragma unroll 1
+    if (tid == 128) {  // warp 4 issues; warps 0-3 go straight to the previous tile's epilogue
+      // descriptor start addresses advance in 16-byte units: compile-time offsets per (tap, word)
+      const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(a), NPIX * 16, IC * 16);
+      const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(sB), NT * 16, 128);
+      const uint32_t d_tmem = tmem + (uint32_t)(buf * NT);
+#pragma unroll
       for (int t = 0; t < KK; ++t) {
-        const int ky = t / K, kx = t - ky * K;
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(((j * 2) * NPIX + ky * IC + kx) * 16), NPIX * 16, IC * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(((t * CW + j) * 2) * NT * 16), NT * 16, 128);
-          tc::mma_i8(tmem + (uint32_t)(buf * NT), ad, bd, idesc, accumulate);
-          accumulate = 1;
+          const uint64_t a_off = (uint64_t)((j * 2) * NPIX + (t / K) * IC + (t % K));
+          const uint64_t b_off = (uint64_t)(((t * CW + j) * 2) * NT);
+          tc::mma_i8(d_tmem, ad0 + a_off, bd0 + b_off, idesc, (t | j) ? 1u : 0u);
         }
       }
       tc::commit(&bar[buf]);
@@ -235,182 +242,6 @@ conv_tc_kernel(const ConvArgs A) {
   // drain: the other buffer's last commit may be unobserved by warps >= 4; wait before dealloc
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
-}
-
-// First binary layer (c_in * K <= 16) on the tensor cores, "strip" layout.  S[r][x] is 16 bytes of
-// int8: byte kx*c_in + c = +/-1 of channel c of halo pixel (r, x + kx); bytes >= K*c_in are don't-care
-// (their weights are 0).  One MMA covers two kernel rows: A row m = output pixel (oy, ox) reads
-// S[oy + 2p][ox] as K-chunk 0 and S[oy + 2p + 1][ox] as K-chunk 1, i.e. core matrices of 8
-// consecutive ox, SBO = LBO = one strip row (8 x 16 B).  The vehicle conv1 (K = 5, c_in = 3) is
-// 3 MMAs (M128 N32 K32) per 128 output pixels.  With SRC_U8 the u8 image is thresholded in the
-// kernel (bit = x_c > -T_c, R14), so the input is read once, as bytes.
-template <int K, int NT, bool SRC_U8>
-__global__ void __launch_bounds__(256, 3)
-conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float* __restrict__ Tt) {
-  constexpr int R = (K - 1) / 2, TH = 16, TW = 8;
-  constexpr int IR = TH + K - 1, IC = TW + K - 1, NPIX = IR * IC;
-  constexpr int NMMA = (K + 1) / 2, SR = TH + 2 * NMMA - 1;  // strip rows incl. the spare of odd K
-  constexpr uint32_t A_BYTES = SR * TW * 16;
-  constexpr uint32_t B_BYTES = NMMA * 2 * NT * 16;
-  constexpr uint32_t TMEM_COLS = (2 * NT <= 32) ? 32 : (2 * NT <= 64 ? 64 : (2 * NT <= 128 ? 128 : (2 * NT <= 256 ? 256 : 512)));
-  constexpr int PF = (NPIX + 255) / 256;
-  __shared__ __align__(128) uint8_t sA[2][A_BYTES];
-  __shared__ __align__(128) uint8_t sB[B_BYTES];
-  __shared__ uint32_t codes[NPIX];
-  __shared__ int32_t s_thr[NT];
-  __shared__ uint32_t s_lut[16];
-  __shared__ uint32_t s_flip[NT / 32];
-  __shared__ uint64_t bar[2];
-  __shared__ uint32_t tmem_base_s;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = blockIdx.y;
-  const int cin = A.c_in;
-  const int nbytes = K * cin;  // valid bytes of a strip
-  if (tid < 16) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v |= (((tid >> (3 - k)) & 1) ? 0x01u : 0xFFu) << (8 * k);
-    s_lut[tid] = v;
-  }
-  if (tid < NT) {
-    const int o = g * NT + tid;
-    s_thr[tid] = (o < A.c_out && A.thr != nullptr) ? A.thr[o] : 0;
-  }
-  if (warp < NT / 32) {
-    const int o = g * NT + warp * 32 + lane;
-    const uint32_t fm = ballot_pack(o < A.c_out && A.flip != nullptr && A.flip[o] != 0);
-    if (lane == 0) s_flip[warp] = fm;
-  }
-  for (int i = tid; i < 2 * (int)A_BYTES / 16; i += 256) reinterpret_cast<uint4*>(&sA[0][0])[i] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) tc::tmem_alloc<TMEM_COLS>(&tmem_base_s);
-  if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
-    tc::fence_mbar_init();
-  }
-  float tc_thr[4] = {0.f, 0.f, 0.f, 0.f};
-  if (SRC_U8 && Tt != nullptr) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (c < cin) tc_thr[c] = -Tt[c];
-  }
-  __syncthreads();
-  // weights: B[p][chunk][n] = strip of kernel row 2p + chunk (0 beyond K), bytes >= K*c_in zeroed
-  for (int i = tid; i < NMMA * 2 * NT; i += 256) {
-    const int n = i % NT, pc = i / NT;
-    const int ky = pc;  // = 2p + chunk
-    const int o = g * NT + n;
-    uint32_t bits = 0;
-    if (o < A.c_out && ky < K) {
-#pragma unroll
-      for (int kx = 0; kx < K; ++kx)
-        bits |= (__ldg(A.wt + ((int64_t)o * K + ky) * K + kx) >> (32 - cin)) << (32 - (kx + 1) * cin);
-    }
-    uint32_t o8[8];
-    expand_word(bits, s_lut, o8);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) m |= ((4 * q + b < nbytes && o < A.c_out && ky < K) ? 0xFFu : 0u) << (8 * b);
-      o8[q] &= m;
-    }
-    *reinterpret_cast<uint4*>(sB + ((size_t)pc * NT + n) * 16) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-  }
-  tc::fence_async_smem();
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = tmem_base_s;
-  const int tiles_img = A.tiles_x * A.tiles_y;
-  constexpr uint32_t idesc = tc::idesc_i8(128, NT);
-
-  auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
-    img = (int)(tile / tiles_img);
-    const int trem = (int)(tile - (int64_t)img * tiles_img);
-    const int ty = trem / A.tiles_x, tx = trem - ty * A.tiles_x;
-    oy0 = ty * TH;
-    ox0 = tx * TW;
-  };
-  // prefetch: the raw input of this thread's halo pixels (u8 channels packed in a word, or the packed word)
-  uint32_t pref[PF];
-  auto load_tile = [&](int64_t tile) {
-    int img, oy0, ox0;
-    tile_origin(tile, img, oy0, ox0);
-#pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int p = tid + q * 256;
-      uint32_t code = 0u;  // outside the map: -1 (R4)
-      if (p < NPIX) {
-        const int r = p / IC, c = p - r * IC;
-        const int gy = oy0 - R + r, gx = ox0 - R + c;
-        if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) {
-          const int64_t pix = ((int64_t)img * A.H + gy) * A.W + gx;
-          if (SRC_U8) {
-            const uint8_t* px = xu8 + pix * cin;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-              if (ch < cin) code |= (uint32_t)((float)px[ch] > tc_thr[ch]) << (cin - 1 - ch);
-          } else {
-            code = __ldg(A.x + pix) >> (32 - cin);
-          }
-        }
-      }
-      pref[q] = code;
-    }
-  };
-  if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
-
-  int it = 0;
-  int64_t prev = -1;
-  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-#pragma unroll
-    for (int q = 0; q < PF; ++q)
-      if (tid + q * 256 < NPIX) codes[tid + q * 256] = pref[q];
-    if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));  // sA[buf] free again
-    __syncthreads();
-    for (int i = tid; i < IR * TW; i += 256) {
-      const int r = i / TW, x = i - r * TW;
-      uint32_t bits = 0;
-#pragma unroll
-      for (int kx = 0; kx < K; ++kx) bits |= codes[r * IC + x + kx] << (32 - (kx + 1) * cin);
-      uint32_t o8[8];
-      expand_word(bits, s_lut, o8);
-      *reinterpret_cast<uint4*>(&sA[buf][(size_t)i * 16]) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-    }
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (tid == 0) {
-      const uint32_t a0 = tc::smem_addr(&sA[buf][0]), b0 = tc::smem_addr(sB);
-#pragma unroll
-      for (int p = 0; p < NMMA; ++p) {
-        const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(2 * p * TW * 16), TW * 16, TW * 16);
-        const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * NT * 16), NT * 16, 128);
-        tc::mma_i8(tmem + (uint32_t)(buf * NT), ad, bd, idesc, p > 0 ? 1u : 0u);
-      }
-      tc::commit(&bar[buf]);
-    }
-    if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
-    if (prev >= 0 && warp < 4) {
-      int img, oy0, ox0;
-      tile_origin(prev, img, oy0, ox0);
-      tc_epilogue<NT>(A, tmem, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1), &bar[buf ^ 1], g, img, oy0, ox0, warp, lane,
-                      s_thr, s_flip);
-    }
-    prev = tile;
-  }
-  if (prev >= 0 && warp < 4) {
-    int img, oy0, ox0;
-    tile_origin(prev, img, oy0, ox0);
-    tc_epilogue<NT>(A, tmem, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1), &bar[(it - 1) & 1], g, img, oy0, ox0, warp,
-                    lane, s_thr, s_flip);
-  }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 }  // namespace bnn

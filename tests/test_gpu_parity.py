@@ -303,6 +303,29 @@ def test_conv_strip_shapes(cuda, orc, k, cin, algo):
         cuda.set_option("conv_algo", 0)
 
 
+@pytest.mark.parametrize("algo", [0, 4, 1])
+@pytest.mark.parametrize("T", [[-128.0, -0.5, -255.25], [float("nan"), float("inf"), -float("inf")], [0.0, -1e-7, 1e30]])
+def test_forward_input_threshold_edges(cuda, orc, algo, T):
+    """R14: the GPU's x > -T (integer compare on u8 in the fused first layer, fp32 in bnn_pack) equals
+    the oracle's (double)x + T > 0 for integer, fractional, huge, infinite and NaN thresholds."""
+    try:
+        cuda.set_option("conv_algo", algo)
+        layers = synth.make_weights(synth.VEHICLE, 1, 1500)
+        Tt = torch.tensor(T, dtype=torch.float32)
+        dl = [dict(L, wt=cuda.pack_weights(dev(L["wt"]))) for L in layers]
+        net = cuda.Net(96, 96, 3, cuda.U8, 1, dev(Tt), dl, max_batch=8)
+        imgs = synth.images(3, 96, 96, 3, 1501)
+        imgs[0, :4, :4] = 128  # x + T = 0 ties for T = -128
+        imgs[1, :4, :4] = 0
+        imgs[2, :4, :4] = 255
+        lg, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+        ref_l, ref_c = oracle_net(orc, synth.VEHICLE, 1, layers, Tt).forward(imgs.numpy(), threads=3)
+        assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+    finally:
+        cuda.set_option("conv_algo", 0)
+
+
 def test_forward_thresholds_and_chunking(cuda, orc):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
