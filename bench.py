@@ -13,8 +13,9 @@ the timed region; the 906 MB input per GPU is larger than the 126 MB L2, so no L
 Prints ONE JSON line (rank 0).  `value` = images/s of the whole job (all ranks), timed with CUDA
 events on the forward stream, max over ranks.  `e2e` = the same metric through bnn_forward_host
 (pinned host images -> host logits/classes, copies inside the timed region).  `roofline` = the
-dominant conv kernel's popcount rate (algorithmic popcounts / its CUDA-event time) against the
-POPC pipe peak (16 / clk / SM, measured by tools/probes/pipe_probe.cu) x 148 SMs x max SM clock.
+dominant conv kernel (largest live CUDA-event time): tcgen05 kernels as int8 TOPS (2 x algorithmic
+binary MACs / time) vs 2 x the measured bf16 sustained peak; POPC kernels as algorithmic popcounts /
+time vs the POPC pipe (16 / clk / SM, tools/probes/pipe_probe.cu) x SMs x max SM clock.
 `cpu_baseline` = the CPU oracle (oracle/) on a bounded sample on the host cores (rank 0, N = 1).
 --impl reference times that oracle alone as the reference arm.
 """
