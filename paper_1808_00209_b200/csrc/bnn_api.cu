@@ -210,11 +210,11 @@ int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols) {
   return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_tmem, 8)));
 }
 
-template <int K, int NT, int CIN, bool SRC_U8>
+template <int K, int NT, int CIN, int SRC>
 bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  auto kfn = conv_first_tc_kernel<K, NT, CIN, SRC_U8>;
+  auto kfn = conv_first_tc_kernel<K, NT, CIN, SRC>;
   static int occ = -1;
-  using C = FirstTcCfg<K, NT, CIN, SRC_U8>;
+  using C = FirstTcCfg<K, NT, CIN, SRC>;
   if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
@@ -230,24 +230,24 @@ bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T
 }
 
 // First layer on the tensor cores: strips of K * c_in <= 16 int8.  Instantiated (k, c_in) pairs:
-// packed input k=3: c_in 1..5, k=5: 1..3, k=7: 1..2; fused u8 input: c_in = 3, k = 3 or 5.
-// conv_algo 0 (auto) or 5 (forced).
-bool use_first_tc(int c_in, int k, bool u8) {
+// packed input (kSrcBits) k=3: c_in 1..5, k=5: 1..3, k=7: 1..2; u8 thresholded in the kernel
+// (kSrcThresh) and real u8 (kSrcReal): c_in in {1, 3}, k in {3, 5}.  conv_algo 0 (auto) or 5 (forced).
+bool use_first_tc(int c_in, int k, int src) {
   if (g_opt_conv_tc == 0 || (g_opt_conv_algo != 0 && g_opt_conv_algo != 5)) return false;
-  if (u8) return c_in == 3 && (k == 3 || k == 5);
+  if (src != kSrcBits) return (c_in == 3 || c_in == 1) && (k == 3 || k == 5);
   return (k == 3 && c_in >= 1 && c_in <= 5) || (k == 5 && c_in >= 1 && c_in <= 3) || (k == 7 && c_in >= 1 && c_in <= 2);
 }
 
-template <bool SRC_U8>
+template <int SRC>
 bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   const bool wide = A.c_out > 32;
   const int c = A.c_in;
 #define BNN_FTC(KK, CC)                                                                           \
   if (k == KK && c == CC)                                                                          \
-    return wide ? launch_conv_first_tc_t<KK, 128, CC, SRC_U8>(A, xu8, T, s)                       \
-                : launch_conv_first_tc_t<KK, 32, CC, SRC_U8>(A, xu8, T, s)
-  if constexpr (SRC_U8) {
-    BNN_FTC(3, 3); BNN_FTC(5, 3);
+    return wide ? launch_conv_first_tc_t<KK, 128, CC, SRC>(A, xu8, T, s)                          \
+                : launch_conv_first_tc_t<KK, 32, CC, SRC>(A, xu8, T, s)
+  if constexpr (SRC != kSrcBits) {
+    BNN_FTC(3, 1); BNN_FTC(3, 3); BNN_FTC(5, 1); BNN_FTC(5, 3);
   } else {
     BNN_FTC(3, 1); BNN_FTC(3, 2); BNN_FTC(3, 3); BNN_FTC(3, 4); BNN_FTC(3, 5);
     BNN_FTC(5, 1); BNN_FTC(5, 2); BNN_FTC(5, 3);
@@ -389,7 +389,7 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
     A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
     A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
     A.cwo = (c_out + 31) / 32; A.pool = pool;
-    if (use_first_tc(c_in, k, false)) return dispatch_conv_first_tc<false>(k, A, nullptr, nullptr, s);
+    if (use_first_tc(c_in, k, kSrcBits)) return dispatch_conv_first_tc<kSrcBits>(k, A, nullptr, nullptr, s);
     if (use_first_lp(c_in, k)) return dispatch_conv_first_lp<false>(k, strip_words(c_in, k), A, nullptr, nullptr, s);
     if (c_in >= 32 && tc_supported(k, A.cw)) return dispatch_conv_tc(k, A.cw, A, s);
     if (use_strip(c_in, k))
@@ -401,6 +401,12 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
   RealConvArgs A{};
   A.x = x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = acc;
   A.n = n; A.H = h; A.W = w; A.c_in = c_in; A.c_out = c_out; A.cwo = (c_out + 31) / 32; A.pool = pool;
+  if (x_dt == BNN_U8 && use_first_tc(c_in, k, kSrcReal)) {
+    ConvArgs B{};
+    B.x = nullptr; B.wt = wt; B.thr = thr; B.flip = flip; B.y = y; B.acc = (int32_t*)acc;
+    B.n = n; B.H = h; B.W = w; B.cw = 1; B.c_in = c_in; B.c_out = c_out; B.cwo = (c_out + 31) / 32; B.pool = pool;
+    return dispatch_conv_first_tc<kSrcReal>(k, B, (const uint8_t*)x, nullptr, s);
+  }
   if (x_dt == BNN_U8) return small ? dispatch_conv_real_u8<4, 1>(k, A, s) : dispatch_conv_real_u8<4, 2>(k, A, s);
   // f32
   const int64_t work = (int64_t)n * (h / pool) * (w / pool) * A.cwo * 32;
@@ -410,9 +416,9 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
 
 // The kernel family launch_conv / the fused first layer pick (kept in step with the dispatch above).
 const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
-  if (x_dt == BNN_U8) return "conv_real_u8_kernel";
+  if (x_dt == BNN_U8) return use_first_tc(c_in, k, kSrcReal) ? "conv_first_tc_kernel" : "conv_real_u8_kernel";
   if (x_dt == BNN_F32) return "conv_real_f32_kernel";
-  if (use_first_tc(c_in, k, false)) return "conv_first_tc_kernel";
+  if (use_first_tc(c_in, k, kSrcBits)) return "conv_first_tc_kernel";
   if (use_first_lp(c_in, k)) return "conv_first_lp_kernel";
   if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) return "conv_tc_kernel";
   if (use_strip(c_in, k)) return "conv_strip_kernel";
@@ -647,7 +653,7 @@ struct ProfScope {
 bool fused_input(const bnn_net* net) {
   if (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) return false;
   if (net->in_dt != BNN_U8 || net->c > 4 || net->L[0].kind != 1) return false;
-  return use_first_tc(net->c, net->L[0].k, true) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
+  return use_first_tc(net->c, net->L[0].k, kSrcThresh) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
 }
 
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
@@ -666,8 +672,8 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
     const bool small = (P.W <= 8 || P.H <= 8);
     bnn_status st;
-    if (use_first_tc(P.c_in, P.k, true))
-      st = dispatch_conv_first_tc<true>(P.k, A, (const uint8_t*)images, T, s);
+    if (use_first_tc(P.c_in, P.k, kSrcThresh))
+      st = dispatch_conv_first_tc<kSrcThresh>(P.k, A, (const uint8_t*)images, T, s);
     else if (use_first_lp(P.c_in, P.k))
       st = dispatch_conv_first_lp<true>(P.k, strip_words(P.c_in, P.k), A, (const uint8_t*)images, T, s);
     else

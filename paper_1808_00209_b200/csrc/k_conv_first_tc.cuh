@@ -1,24 +1,29 @@
-// k_conv_first_tc.cuh -- the first binary layer (few input channels, c_in * K <= 16) on the tensor
-// cores (tcgen05.mma kind::i8), Eq. (3) with the paper's input binarization fused (Section 2.3).
+// k_conv_first_tc.cuh -- the first conv layer (few input channels, c_in * K <= 16) on the tensor
+// cores (tcgen05.mma kind::i8), Eq. (3) with the paper's input handling fused (Section 2.3).
 //
 // Strip layout.  For every halo row r and halo column x, S[r][x] = the K taps x, .., x+K-1 of
-// c_in channels each (bit order [kx][c], MSB first) expanded to K*c_in int8 (+1 = 0x01,
-// -1 = 0xFF) in a 16-byte slot (bytes >= K*c_in are don't-care: their weights are 0).  One MMA
-// covers two kernel rows: A row m = output pixel (oy, ox) reads S[oy + 2p][ox] as K-chunk 0 and
-// S[oy + 2p + 1][ox] as K-chunk 1 -- core matrices of 8 consecutive ox, SBO = LBO = one strip row
-// (8 x 16 B) -- so the vehicle conv1 (K = 5, c_in = 3: 75 products per output channel) is
-// 3 MMAs (M128 N32 K32) per 128 output pixels.
+// c_in channels each (order [kx][c]) as K*c_in int8 in a 16-byte slot (bytes >= K*c_in are
+// don't-care: their weights are 0).  One MMA covers two kernel rows: A row m = output pixel (oy, ox)
+// reads S[oy + 2p][ox] as K-chunk 0 and S[oy + 2p + 1][ox] as K-chunk 1 -- core matrices of 8
+// consecutive ox, SBO = LBO = one strip row (8 x 16 B) -- so the vehicle conv1 (K = 5, c_in = 3:
+// 75 products per output channel) is 3 MMAs (M128 N32 K32) per 128 output pixels.
 //
 // A tile is 32 rows x 8 columns = two M = 128 MMA blocks that share the staged strips and the
 // weights; all 8 warps run the epilogue (warp w: block w / 4, TMEM lanes 32 (w % 4) ..).
-// Input: u8 pixels thresholded in the kernel (bit = x_c > -T_c as an exact integer compare, R14;
-// SIGN: x > 0), or packed words (c_in bits at the top).  Out-of-map pixels are -1 (R4).
+// Sources (SRC):
+//   kSrcBits   packed words (c_in bits at the top), binary layer, out-of-map = -1 (R4)
+//   kSrcThresh u8 pixels binarized in the kernel: bit = x_c > -T_c as an exact integer compare
+//              (R14; SIGN: x > 0), then as kSrcBits -- the packed input never exists in HBM
+//   kSrcReal   u8 pixels as UNSIGNED int8 A operands ("no input binarization"),
+//              zero padding (R5); exact int32 sums of +/-x.
 #pragma once
 #include "k_conv_tc.cuh"
 
 namespace bnn {
 
-template <int K, int NT, int CIN, bool SRC_U8>
+enum { kSrcBits = 0, kSrcThresh = 1, kSrcReal = 2 };
+
+template <int K, int NT, int CIN, int SRC>
 struct FirstTcCfg {
   static constexpr int R = (K - 1) / 2, TH = 32, TW = 8, MB = TH / 16;  // MMA blocks per tile
   static constexpr int IR = TH + K - 1, IC = TW + K - 1, NPIX = IR * IC;
@@ -29,17 +34,20 @@ struct FirstTcCfg {
   static constexpr uint32_t B_BYTES = NMMA * 2 * NT * 16;
   static constexpr uint32_t TMEM_COLS = (4 * NT <= 128) ? 128 : (4 * NT <= 256 ? 256 : 512);  // 2 buffers x MB
   static constexpr int PF = (NPIX + 255) / 256;
+  // staging: one c_in-bit code per halo pixel (bits), or the halo's bytes (+ 8 B of slack) (real)
+  static constexpr int STAGE_WORDS = (SRC == kSrcReal) ? (NPIX * CIN + 3) / 4 + 6 : NPIX;
   static_assert(S <= 16 && IC <= 32 && MB == 2, "strip must fit 16 int8");
 };
 
-template <int K, int NT, int CIN, bool SRC_U8>
+template <int K, int NT, int CIN, int SRC>
 __global__ void __launch_bounds__(256, 3)
 conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float* __restrict__ Tt) {
-  using C = FirstTcCfg<K, NT, CIN, SRC_U8>;
+  using C = FirstTcCfg<K, NT, CIN, SRC>;
   constexpr int R = C::R, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, NMMA = C::NMMA, PF = C::PF;
+  constexpr bool U8 = SRC != kSrcBits;
   __shared__ __align__(128) uint8_t sA[2][C::A_BYTES];
   __shared__ __align__(128) uint8_t sB[C::B_BYTES];
-  __shared__ uint32_t codes[NPIX];
+  __shared__ __align__(16) uint32_t stage[C::STAGE_WORDS];
   __shared__ __align__(16) int32_t s_thr[NT];
   __shared__ uint32_t s_lut[16];
   __shared__ uint32_t s_flip[NT / 32];
@@ -65,17 +73,19 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
     if (lane == 0) s_flip[warp] = fm;
   }
   for (int i = tid; i < 2 * (int)C::A_BYTES / 16; i += 256) reinterpret_cast<uint4*>(&sA[0][0])[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < C::STAGE_WORDS; i += 256) stage[i] = 0u;
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
     tc::fence_mbar_init();
   }
-  int ti[CIN];  // u8: bit_c = x_c > ti_c (SIGN: x > 0)
+  int ti[CIN];  // kSrcThresh: bit_c = x_c > ti_c (SIGN: x > 0)
 #pragma unroll
-  for (int c = 0; c < CIN; ++c) ti[c] = (SRC_U8 && Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
+  for (int c = 0; c < CIN; ++c) ti[c] = (SRC == kSrcThresh && Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
   __syncthreads();
-  // weights: B[p][chunk][n] = strip of kernel row ky = 2p + chunk (0 beyond K), bytes >= S zeroed
+  // weights: B[p][chunk][n] = strip of kernel row ky = 2p + chunk (0 beyond K), order [kx][c],
+  // +/-1 int8, bytes >= S zeroed
   for (int i = tid; i < NMMA * 2 * NT; i += 256) {
     const int n = i % NT, ky = i / NT;
     const int o = g * NT + n;
@@ -102,7 +112,7 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  constexpr uint32_t idesc = tc::idesc_i8(128, NT);
+  constexpr uint32_t idesc = tc::idesc_i8(128, NT, SRC != kSrcReal);  // real pixels: unsigned A
 
   auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
     int ty, tx;
@@ -110,15 +120,15 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
     oy0 = ty * TH;
     ox0 = tx * TW;
   };
-  // prefetch: the RAW bytes / word of this thread's halo pixels of the next tile; turned into
-  // c_in-bit codes only when the tile is staged (the loads fly during the epilogue).
+  // prefetch: the RAW bytes / word of this thread's halo pixels of the next tile; staged (and
+  // thresholded) only after the current epilogue, so the loads fly meanwhile.
   uint32_t praw[PF][CIN];
   bool pin[PF];
   auto load_tile = [&](int64_t tile) {
     int img, oy0, ox0;
     tile_origin(tile, img, oy0, ox0);
-    const uint8_t* xi = SRC_U8 ? xu8 + (int64_t)img * A.H * A.W * CIN : nullptr;
-    const uint32_t* wi = SRC_U8 ? nullptr : A.x + (int64_t)img * A.H * A.W;
+    const uint8_t* xi = U8 ? xu8 + (int64_t)img * A.H * A.W * CIN : nullptr;
+    const uint32_t* wi = U8 ? nullptr : A.x + (int64_t)img * A.H * A.W;
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
       const int p = tid + q * 256;
@@ -127,7 +137,7 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
       pin[q] = p < NPIX && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W;
       if (pin[q]) {
         const int off = gy * A.W + gx;  // < 2^31 per image
-        if (SRC_U8) {
+        if (U8) {
 #pragma unroll
           for (int ch = 0; ch < CIN; ++ch) praw[q][ch] = (uint32_t)__ldg(xi + off * CIN + ch);
         } else {
@@ -146,28 +156,47 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
     for (int q = 0; q < PF; ++q) {
       const int p = tid + q * 256;
       if (p < NPIX) {
-        uint32_t code = 0u;
-        if (pin[q]) {
-          if (SRC_U8) {
+        if (SRC == kSrcReal) {
+          uint8_t* hb = reinterpret_cast<uint8_t*>(stage);
 #pragma unroll
-            for (int ch = 0; ch < CIN; ++ch) code |= (uint32_t)((int)praw[q][ch] > ti[ch]) << (CIN - 1 - ch);
-          } else {
-            code = praw[q][0] >> (32 - CIN);
+          for (int ch = 0; ch < CIN; ++ch) hb[p * CIN + ch] = pin[q] ? (uint8_t)praw[q][ch] : (uint8_t)0;  // R5: 0
+        } else {
+          uint32_t code = 0u;  // R4: -1
+          if (pin[q]) {
+            if (SRC == kSrcThresh) {
+#pragma unroll
+              for (int ch = 0; ch < CIN; ++ch) code |= (uint32_t)((int)praw[q][ch] > ti[ch]) << (CIN - 1 - ch);
+            } else {
+              code = praw[q][0] >> (32 - CIN);
+            }
           }
+          stage[p] = code;
         }
-        codes[p] = code;
       }
     }
     if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));  // sA[buf] free again
     __syncthreads();
     for (int i = tid; i < C::IR * TW; i += 256) {
       const int r = i >> 3, x = i & 7;
-      uint32_t strip = 0;
+      uint32_t o4[4];
+      if (SRC == kSrcReal) {
+        // the strip is the 16 bytes of the halo row starting at pixel x (15 used): byte-aligned copy
+        const int o = (r * IC + x) * CIN;
+        const int w0 = o >> 2, sh = 8 * (o & 3);
+        uint32_t w[5];
 #pragma unroll
-      for (int kx = 0; kx < K; ++kx) strip |= codes[r * IC + x + kx] << (32 - (kx + 1) * CIN);
-      uint32_t o8[8];
-      expand_word(strip, s_lut, o8);
-      *reinterpret_cast<uint4*>(&sA[buf][(size_t)i * 16]) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+        for (int j = 0; j < 5; ++j) w[j] = stage[w0 + j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o4[j] = __funnelshift_r(w[j], w[j + 1], sh);
+      } else {
+        uint32_t strip = 0;
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) strip |= stage[r * IC + x + kx] << (32 - (kx + 1) * CIN);
+        uint32_t o8[8];
+        expand_word(strip, s_lut, o8);
+        o4[0] = o8[0]; o4[1] = o8[1]; o4[2] = o8[2]; o4[3] = o8[3];
+      }
+      *reinterpret_cast<uint4*>(&sA[buf][(size_t)i * 16]) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
     }
     tc::fence_async_smem();
     tc::fence_before();

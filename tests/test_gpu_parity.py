@@ -157,9 +157,19 @@ def test_conv_empty_batch(cuda):
     assert y.shape == (0, 8, 8, 1)
 
 
+@pytest.mark.parametrize("tc", [1, 0])
 @pytest.mark.parametrize("k,pool", [(5, 2), (3, 1), (1, 1), (7, 2)])
 @pytest.mark.parametrize("cin", [3, 1])
-def test_conv_real_u8(cuda, orc, k, pool, cin):
+def test_conv_real_u8(cuda, orc, k, pool, cin, tc):
+    """Real u8 first layer: tc = 1 runs k in {3, 5} on tcgen05 with unsigned int8 A operands."""
+    try:
+        cuda.set_option("conv_tc", tc)
+        _conv_real_u8_case(cuda, orc, k, pool, cin)
+    finally:
+        cuda.set_option("conv_tc", 1)
+
+
+def _conv_real_u8_case(cuda, orc, k, pool, cin):
     n, h, w, cout = 2, 20, 24, 40
     x = synth.images(n, h, w, cin, 50 + k)
     ws = synth.pm1((cout, k, k, cin), 60 + k)
