@@ -62,6 +62,7 @@ int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap co
 int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
 int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
+int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -238,10 +239,43 @@ bool use_first_tc(int c_in, int k, int src) {
   return (k == 3 && c_in >= 1 && c_in <= 5) || (k == 5 && c_in >= 1 && c_in <= 3) || (k == 7 && c_in >= 1 && c_in <= 2);
 }
 
+template <int K, int NT, int CIN, int SRC>
+bnn_status launch_conv_first_tc_pool_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  auto kfn = conv_first_tc_pool_kernel<K, NT, CIN, SRC>;
+  static int occ = -1;
+  using C = FirstTcPoolCfg<K, NT, CIN, SRC>;
+  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
+  kfn<<<grid, 256, 0, s>>>(A, xu8, T);
+  return check_launch("conv_first_tc_pool_kernel");
+}
+
 template <int SRC>
 bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   const bool wide = A.c_out > 32;
   const int c = A.c_in;
+  if (A.pool == 2 && g_opt_first_pool_tc) {
+#define BNN_FTCP(KK, CC)                                                                          \
+  if (k == KK && c == CC)                                                                          \
+    return wide ? launch_conv_first_tc_pool_t<KK, 64, CC, SRC>(A, xu8, T, s)                      \
+                : launch_conv_first_tc_pool_t<KK, 32, CC, SRC>(A, xu8, T, s)
+    if constexpr (SRC != kSrcBits) {
+      BNN_FTCP(3, 1); BNN_FTCP(3, 3); BNN_FTCP(5, 1); BNN_FTCP(5, 3);
+    } else {
+      BNN_FTCP(3, 1); BNN_FTCP(3, 2); BNN_FTCP(3, 3); BNN_FTCP(3, 4); BNN_FTCP(3, 5);
+      BNN_FTCP(5, 1); BNN_FTCP(5, 2); BNN_FTCP(5, 3);
+      BNN_FTCP(7, 1); BNN_FTCP(7, 2);
+    }
+#undef BNN_FTCP
+  }
 #define BNN_FTC(KK, CC)                                                                           \
   if (k == KK && c == CC)                                                                          \
     return wide ? launch_conv_first_tc_t<KK, 128, CC, SRC>(A, xu8, T, s)                          \
@@ -468,6 +502,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "tiles_per_cta") == 0) { g_opt_tiles_per_cta = value; return BNN_OK; }
   if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
+  if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 

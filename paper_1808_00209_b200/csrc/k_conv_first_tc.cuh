@@ -235,4 +235,272 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
+// Pooled variant (pool = 2): the MMA rows are ordered by pool window.  A tile is 16 x 8 POOLED
+// pixels (a 32 x 16 conv region); strips are stored in two planes by conv-column parity, so for
+// pool offset (dy, dx) the 8 consecutive pooled columns px..px+7 of one pooled row are 8
+// consecutive 16-byte strips (one core matrix): A start = plane dx, strip row dy + 2p (+ chunk),
+// SBO = 2 strip rows (next pooled row), LBO = 1 strip row.  The four offsets accumulate into four
+// TMEM blocks, and the epilogue thread of pooled pixel m reads its 4 window pixels' sums:
+//   OR of the 4 thresholded bits == (max of the 4 sums) > thr          (R9, sign is monotone)
+// -- 3 integer max + 1 compare-shift per channel instead of 4 thresholds and 2 shuffles.  With a
+// flip (bit = (acc > thr) XOR 1 = acc <= thr) the OR is (min <= thr): the sums are negated
+// (-acc > -thr - 1) and the same max is used.
+template <int K, int NT, int CIN, int SRC>
+struct FirstTcPoolCfg {
+  static constexpr int R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW;
+  static constexpr int IR = TH + K - 1, IC = TW + K - 1, NPIX = IR * IC;
+  static constexpr int S = K * CIN;
+  static constexpr int NMMA = (K + 1) / 2;
+  static constexpr int SRR = TH + 2 * NMMA - 1;            // strip rows per parity plane
+  static constexpr uint32_t A_BYTES = 2 * SRR * PW * 16;   // 2 parity planes
+  static constexpr uint32_t B_BYTES = NMMA * 2 * NT * 16;
+  static constexpr uint32_t TMEM_COLS = (4 * NT <= 128) ? 128 : 256;  // 4 pool offsets (single set)
+  static constexpr int PF = (NPIX + 255) / 256;
+  static constexpr int STAGE_WORDS = (SRC == kSrcReal) ? (NPIX * CIN + 3) / 4 + 6 : NPIX;
+  static_assert(S <= 16 && IC <= 32 && NT <= 64, "strip must fit 16 int8; TMEM holds 8 x NT columns");
+};
+
+template <int K, int NT, int CIN, int SRC>
+__global__ void __launch_bounds__(256, 3)
+conv_first_tc_pool_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const float* __restrict__ Tt) {
+  using C = FirstTcPoolCfg<K, NT, CIN, SRC>;
+  constexpr int R = C::R, PH = C::PH, PW = C::PW, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX;
+  constexpr int NMMA = C::NMMA, PF = C::PF, SRR = C::SRR;
+  constexpr bool U8 = SRC != kSrcBits;
+  __shared__ __align__(128) uint8_t sA[2][C::A_BYTES];
+  __shared__ __align__(128) uint8_t sB[C::B_BYTES];
+  __shared__ __align__(16) uint32_t stage[C::STAGE_WORDS];
+  __shared__ __align__(16) int32_t s_thr[NT];
+  __shared__ __align__(16) int32_t s_sgn[NT];  // 0 or -1 (flip: negate the sums)
+  __shared__ uint32_t s_lut[16];
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ int s_any_flip;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.y;
+  if (tid < 16) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v |= (((tid >> (3 - k)) & 1) ? 0x01u : 0xFFu) << (8 * k);
+    s_lut[tid] = v;
+  }
+  if (tid == 0) s_any_flip = 0;
+  __syncthreads();
+  if (tid < NT) {
+    const int o = g * NT + tid;
+    const bool ok = o < A.c_out;
+    const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
+    const int t = (ok && A.thr != nullptr) ? max(-(1 << 29), min(1 << 29, A.thr[o])) : 0;
+    // flip: bit = acc <= t  <=>  -acc > -t - 1
+    s_thr[tid] = ok ? (f ? -t - 1 : t) : (1 << 30);  // invalid channels: never set
+    s_sgn[tid] = f ? -1 : 0;
+    if (f) s_any_flip = 1;
+  }
+  for (int i = tid; i < 2 * (int)C::A_BYTES / 16; i += 256) reinterpret_cast<uint4*>(&sA[0][0])[i] = make_uint4(0, 0, 0, 0);
+  for (int i = tid; i < C::STAGE_WORDS; i += 256) stage[i] = 0u;
+  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  int ti[CIN];
+#pragma unroll
+  for (int c = 0; c < CIN; ++c) ti[c] = (SRC == kSrcThresh && Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
+  __syncthreads();
+  for (int i = tid; i < NMMA * 2 * NT; i += 256) {
+    const int n = i % NT, ky = i / NT;
+    const int o = g * NT + n;
+    const bool ok = o < A.c_out && ky < K;
+    uint32_t bits = 0;
+    if (ok) {
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx)
+        bits |= (__ldg(A.wt + ((int64_t)o * K + ky) * K + kx) >> (32 - CIN)) << (32 - (kx + 1) * CIN);
+    }
+    uint32_t o8[8];
+    expand_word(bits, s_lut, o8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) m |= ((4 * q + b < C::S && ok) ? 0xFFu : 0u) << (8 * b);
+      o8[q] &= m;
+    }
+    *reinterpret_cast<uint4*>(sB + ((size_t)ky * NT + n) * 16) = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+  }
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const bool any_flip = s_any_flip != 0;
+  constexpr uint32_t idesc = tc::idesc_i8(128, NT, SRC != kSrcReal);
+
+  auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {  // conv-resolution origin
+    int ty, tx;
+    tile_coords(A, tile, img, ty, tx);
+    oy0 = ty * TH;
+    ox0 = tx * TW;
+  };
+  uint32_t praw[PF][CIN];
+  bool pin[PF];
+  auto load_tile = [&](int64_t tile) {
+    int img, oy0, ox0;
+    tile_origin(tile, img, oy0, ox0);
+    const uint8_t* xi = U8 ? xu8 + (int64_t)img * A.H * A.W * CIN : nullptr;
+    const uint32_t* wi = U8 ? nullptr : A.x + (int64_t)img * A.H * A.W;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int p = tid + q * 256;
+      const int r = p / IC, c = p - r * IC;
+      const int gy = oy0 - R + r, gx = ox0 - R + c;
+      pin[q] = p < NPIX && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W;
+      if (pin[q]) {
+        const int off = gy * A.W + gx;
+        if (U8) {
+#pragma unroll
+          for (int ch = 0; ch < CIN; ++ch) praw[q][ch] = (uint32_t)__ldg(xi + off * CIN + ch);
+        } else {
+          praw[q][0] = __ldg(wi + off);
+        }
+      }
+    }
+  };
+  auto epilogue = [&](int64_t tile, int buf, uint32_t phase) {
+    int img, oy0, ox0;
+    tile_origin(tile, img, oy0, ox0);
+    tc::mbar_wait(&bar[buf], phase);
+    tc::fence_after();
+    const int m = warp * 32 + lane;  // pooled pixel of the tile
+    const int py = (oy0 >> 1) + m / PW, px = (ox0 >> 1) + m % PW;
+    const int Ho = A.H >> 1, Wo = A.W >> 1;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < NT && g * NT + c0 < A.c_out; c0 += 32) {
+      if (A.acc != nullptr) {  // debug output: the 4 window pixels' sums, before any flip
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          int vv[32];
+          tc::tmem_ld32(lane_base + (uint32_t)(q * NT + c0), vv);
+          tc::tmem_ld_wait();
+          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+          if (oy < A.H && ox < A.W) {
+            int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + c0;
+            for (int c = 0; c < 32 && g * NT + c0 + c < A.c_out; ++c) dst[c] = vv[c];
+          }
+        }
+      }
+      uint32_t word = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // two halves of 16 channels (register pressure)
+        const int cb = c0 + 16 * h;
+        int mx[16], v[16];
+        tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), mx);
+        tc::tmem_ld_wait();
+        if (any_flip) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) mx[c] = (mx[c] ^ s_sgn[cb + c]) - s_sgn[cb + c];
+        }
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          tc::tmem_ld16(lane_base + (uint32_t)(q * NT + cb), v);
+          tc::tmem_ld_wait();
+          if (any_flip) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = (v[c] ^ s_sgn[cb + c]) - s_sgn[cb + c];
+          }
+#pragma unroll
+          for (int c = 0; c < 16; ++c) mx[c] = max(mx[c], v[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) word = __funnelshift_l((uint32_t)(s_thr[cb + c] - mx[c]), word, 1);
+      }
+      if (A.y != nullptr && py < Ho && px < Wo) A.y[(((int64_t)img * Ho + py) * Wo + px) * A.cwo + ((g * NT + c0) >> 5)] = word;
+    }
+    tc::fence_before();
+  };
+  if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
+
+  int it = 0;
+  int64_t prev = -1;
+  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int p = tid + q * 256;
+      if (p < NPIX) {
+        if (SRC == kSrcReal) {
+          uint8_t* hb = reinterpret_cast<uint8_t*>(stage);
+#pragma unroll
+          for (int ch = 0; ch < CIN; ++ch) hb[p * CIN + ch] = pin[q] ? (uint8_t)praw[q][ch] : (uint8_t)0;
+        } else {
+          uint32_t code = 0u;
+          if (pin[q]) {
+            if (SRC == kSrcThresh) {
+#pragma unroll
+              for (int ch = 0; ch < CIN; ++ch) code |= (uint32_t)((int)praw[q][ch] > ti[ch]) << (CIN - 1 - ch);
+            } else {
+              code = praw[q][0] >> (32 - CIN);
+            }
+          }
+          stage[p] = code;
+        }
+      }
+    }
+    if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));
+    __syncthreads();
+    for (int i = tid; i < C::IR * TW; i += 256) {
+      const int r = i / TW, x = i - r * TW;
+      uint32_t o4[4];
+      if (SRC == kSrcReal) {
+        const int o = (r * IC + x) * CIN;
+        const int w0 = o >> 2, sh = 8 * (o & 3);
+        uint32_t w[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) w[j] = stage[w0 + j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o4[j] = __funnelshift_r(w[j], w[j + 1], sh);
+      } else {
+        uint32_t strip = 0;
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) strip |= stage[r * IC + x + kx] << (32 - (kx + 1) * CIN);
+        uint32_t o8[8];
+        expand_word(strip, s_lut, o8);
+        o4[0] = o8[0]; o4[1] = o8[1]; o4[2] = o8[2]; o4[3] = o8[3];
+      }
+      // parity plane (x & 1), strip row r, pooled column x >> 1
+      *reinterpret_cast<uint4*>(&sA[buf][(size_t)(((x & 1) * SRR + r) * PW + (x >> 1)) * 16]) =
+          make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+    tc::fence_async_smem();
+    // single TMEM accumulator set (so 3 CTAs fit per SM): drain tile it-1 before tile it's MMAs
+    if (prev >= 0 && warp < 4) epilogue(prev, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 128) {
+      const uint32_t a0 = tc::smem_addr(&sA[buf][0]), b0 = tc::smem_addr(sB);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int dy = q >> 1, dx = q & 1;
+#pragma unroll
+        for (int p = 0; p < NMMA; ++p) {
+          const uint64_t ad =
+              tc::desc_kmajor(a0 + (uint32_t)(((dx * SRR + dy + 2 * p) * PW) * 16), PW * 16, 2 * PW * 16);
+          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * NT * 16), NT * 16, 128);
+          tc::mma_i8(tmem + (uint32_t)(q * NT), ad, bd, idesc, p > 0 ? 1u : 0u);
+        }
+      }
+      tc::commit(&bar[buf]);
+    }
+    if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
+    prev = tile;
+  }
+  if (prev >= 0 && warp < 4) epilogue(prev, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
 }  // namespace bnn

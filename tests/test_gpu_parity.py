@@ -119,6 +119,24 @@ def test_conv_binary(cuda, orc, n, h, w, cin, cout, k, pool, tc):
         cuda.set_option("conv_tc", 1)
 
 
+@pytest.mark.parametrize("pool_tc", [1, 0])
+@pytest.mark.parametrize("n,h,w,cin,cout,k,thr", [
+    (2, 96, 96, 3, 32, 5, True),   # vehicle conv1 (with thresholds + flips)
+    (2, 96, 96, 3, 32, 5, False),
+    (1, 36, 20, 1, 40, 5, True),   # gray, c_out > 32 (NT = 64), ragged tiles
+    (1, 34, 18, 2, 64, 7, False),  # k = 7
+    (2, 32, 32, 5, 33, 3, True),   # c_in = 5, k = 3
+])
+def test_conv_first_layer_pooled_tc(cuda, orc, pool_tc, n, h, w, cin, cout, k, thr):
+    """pool = 2 first layers: the pool-window-ordered tensor-core kernel (max of the 4 window sums,
+    flips by negation) vs the unordered one, both against the oracle."""
+    try:
+        cuda.set_option("first_pool_tc", pool_tc)
+        conv_case(cuda, orc, n, h, w, cin, cout, k, 2, thr=thr, flip=thr, seed=1700 + h + k + cin)
+    finally:
+        cuda.set_option("first_pool_tc", 1)
+
+
 @pytest.mark.parametrize("n,h,w,cin,cout,k,pool", [
     (3, 48, 48, 32, 32, 5, 2),    # vehicle conv2 on tcgen05
     (1, 16, 16, 64, 70, 5, 2),    # c_out > NT: two channel tiles, ragged
