@@ -16,6 +16,7 @@
 #include "k_conv.cuh"
 #include "k_conv_tc.cuh"
 #include "k_conv_first_tc.cuh"
+#include "k_conv_tc4.cuh"
 #include "k_dense.cuh"
 #include "k_pack.cuh"
 
@@ -63,6 +64,7 @@ int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
 int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
+int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -316,7 +318,34 @@ bool tc_supported(int k, int cw) {
   return (k == 5 && (cw == 1 || cw == 2)) || (k == 3 && (cw == 1 || cw == 2 || cw == 4)) || (k == 7 && cw == 1);
 }
 
+template <int K, int CW, int NT>
+bnn_status launch_conv_tc4_t(ConvArgs A, cudaStream_t s) {
+  using C = ConvTc4Cfg<K, CW, NT>;
+  auto kfn = conv_tc4_kernel<K, CW, NT>;
+  static int occ = -1;
+  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
+  kfn<<<grid, 256, C::SMEM, s>>>(A);
+  return check_launch("conv_tc4_kernel");
+}
+
 bnn_status dispatch_conv_tc(int k, int cw, const ConvArgs& A, cudaStream_t s) {
+  if (g_opt_conv_tc_fp4) {
+    if (k == 5 && cw == 1) return launch_conv_tc4_t<5, 1, 32>(A, s);
+    if (k == 5 && cw == 2) return launch_conv_tc4_t<5, 2, 64>(A, s);
+    if (k == 3 && cw == 1) return launch_conv_tc4_t<3, 1, 32>(A, s);
+    if (k == 3 && cw == 2) return launch_conv_tc4_t<3, 2, 64>(A, s);
+    if (k == 3 && cw == 4) return launch_conv_tc4_t<3, 4, 128>(A, s);
+    if (k == 7 && cw == 1) return launch_conv_tc4_t<7, 1, 32>(A, s);
+  }
   if (k == 5 && cw == 1) return launch_conv_tc_t<5, 1, 32>(A, s);
   if (k == 5 && cw == 2) return launch_conv_tc_t<5, 2, 64>(A, s);
   if (k == 3 && cw == 1) return launch_conv_tc_t<3, 1, 32>(A, s);
@@ -454,7 +483,7 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
   if (x_dt == BNN_F32) return "conv_real_f32_kernel";
   if (use_first_tc(c_in, k, kSrcBits)) return "conv_first_tc_kernel";
   if (use_first_lp(c_in, k)) return "conv_first_lp_kernel";
-  if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) return "conv_tc_kernel";
+  if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) return g_opt_conv_tc_fp4 ? "conv_tc4_kernel" : "conv_tc_kernel";
   if (use_strip(c_in, k)) return "conv_strip_kernel";
   if (use_patch(c_in, k)) return "conv_patch_kernel";
   return "conv_bin_kernel";
@@ -503,6 +532,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
+  if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 

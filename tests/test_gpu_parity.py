@@ -145,8 +145,14 @@ def test_conv_first_layer_pooled_tc(cuda, orc, pool_tc, n, h, w, cin, cout, k, t
     (1, 14, 10, 32, 33, 7, 1),    # k = 7
     (5, 24, 16, 64, 64, 5, 1),    # many tiles per CTA (double-buffered TMEM accumulators)
 ])
-def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool):
-    conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=True, flip=True, seed=900 + h + k)
+@pytest.mark.parametrize("fp4", [1, 0])
+def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool, fp4):
+    """fp4 = 1: kind::mxf4 (packed e2m1, two taps per MMA); fp4 = 0: kind::i8."""
+    try:
+        cuda.set_option("conv_tc_fp4", fp4)
+        conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=True, flip=True, seed=900 + h + k)
+    finally:
+        cuda.set_option("conv_tc_fp4", 1)
 
 
 @pytest.mark.parametrize("cin,k", [(3, 5), (32, 3)])
