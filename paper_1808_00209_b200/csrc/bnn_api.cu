@@ -17,6 +17,8 @@
 #include "k_conv_tc.cuh"
 #include "k_conv_first_tc.cuh"
 #include "k_conv_tc4.cuh"
+#include "k_dense_tc4.cuh"
+#include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
 #include "k_pack.cuh"
 
@@ -65,6 +67,7 @@ int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
+int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -315,7 +318,30 @@ bnn_status launch_conv_tc_t(ConvArgs A, cudaStream_t s) {
 // (k, words per pixel) -> tensor-core instantiation; returns false if none applies
 bool tc_supported(int k, int cw) {
   if (g_opt_conv_tc == 0) return false;
+  if (g_opt_conv_tc_fp4 && (k == 3 || k == 5 || k == 7)) return true;  // small + streamed (big) kernels
   return (k == 5 && (cw == 1 || cw == 2)) || (k == 3 && (cw == 1 || cw == 2 || cw == 4)) || (k == 7 && cw == 1);
+}
+
+template <int K, int CG, int NT>
+bnn_status launch_conv_tc4_big_t(ConvArgs A, cudaStream_t s) {
+  using C = ConvTc4BigCfg<K, CG, NT>;
+  auto kfn = conv_tc4_big_kernel<K, CG, NT>;
+  static int set = 0;
+  if (!set) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM); set = 1; }
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  const int groups = (A.c_out + NT - 1) / NT;
+  // one CTA per SM in total (TMEM 512 columns, ~200 KB smem): split the SMs over the channel groups
+  const int64_t per_group = std::max<int64_t>(1, num_sms() / groups);
+  const int64_t gx = std::min<int64_t>(A.total_tiles, per_group);
+  dim3 grid((unsigned)gx, (unsigned)groups);
+  kfn<<<grid, 256, C::SMEM, s>>>(A);
+  return check_launch("conv_tc4_big_kernel");
 }
 
 template <int K, int CW, int NT>
@@ -345,6 +371,9 @@ bnn_status dispatch_conv_tc(int k, int cw, const ConvArgs& A, cudaStream_t s) {
     if (k == 3 && cw == 2) return launch_conv_tc4_t<3, 2, 64>(A, s);
     if (k == 3 && cw == 4) return launch_conv_tc4_t<3, 4, 128>(A, s);
     if (k == 7 && cw == 1) return launch_conv_tc4_t<7, 1, 32>(A, s);
+    if (k == 3) return launch_conv_tc4_big_t<3, 4, 128>(A, s);
+    if (k == 5) return launch_conv_tc4_big_t<5, 2, 128>(A, s);
+    if (k == 7) return launch_conv_tc4_big_t<7, 1, 128>(A, s);
   }
   if (k == 5 && cw == 1) return launch_conv_tc_t<5, 1, 32>(A, s);
   if (k == 5 && cw == 2) return launch_conv_tc_t<5, 2, 64>(A, s);
@@ -483,13 +512,21 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
   if (x_dt == BNN_F32) return "conv_real_f32_kernel";
   if (use_first_tc(c_in, k, kSrcBits)) return "conv_first_tc_kernel";
   if (use_first_lp(c_in, k)) return "conv_first_lp_kernel";
-  if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) return g_opt_conv_tc_fp4 ? "conv_tc4_kernel" : "conv_tc_kernel";
+  if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) {
+    const int cw = (c_in + 31) / 32;
+    if (!g_opt_conv_tc_fp4) return "conv_tc_kernel";
+    const bool small = (k == 5 && cw <= 2) || (k == 3 && (cw <= 2 || cw == 4)) || (k == 7 && cw == 1);
+    return small ? "conv_tc4_kernel" : "conv_tc4_big_kernel";
+  }
   if (use_strip(c_in, k)) return "conv_strip_kernel";
   if (use_patch(c_in, k)) return "conv_patch_kernel";
   return "conv_bin_kernel";
 }
 
 // ---------------------------------------------------------------------------- dense
+// Dense layers with a real batch and a long reduction run on the tensor cores (kind::mxf4).
+bool use_dense_tc(int n, int64_t dw) { return g_opt_dense_tc && n >= 256 && dw >= 32 && (dw % 4) == 0; }
+
 bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,
                         const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, cudaStream_t s) {
   if (n == 0) return BNN_OK;
@@ -499,6 +536,28 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
   A.n = n; A.l = l; A.lw = (l + 31) / 32; A.d = d; A.dw = (d + 31) / 32;
   constexpr int PI = 8, NWARP = 8, DC = 64;
   bnn_status st;
+  if (use_dense_tc(n, A.dw)) {
+    // tensor cores: NT = 128 (l <= 128) or 256 output columns per CTA group
+    const bool wide = l > 128;
+    A.cls = (l <= (wide ? 256 : 128)) ? cls : nullptr;
+    const int ntiles = (n + 127) / 128;
+    auto launch = [&](auto kfn, uint32_t smem, int nt) {
+      static int set_nt128 = 0, set_nt256 = 0;
+      int& flag = (nt == 128) ? set_nt128 : set_nt256;
+      if (!flag) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); flag = 1; }
+      dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)((l + nt - 1) / nt));
+      kfn<<<grid, 256, smem, s>>>(A);
+    };
+    if (wide) launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM, 256);
+    else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM, 128);
+    st = check_launch("dense_tc4_kernel");
+    if (st != BNN_OK) return st;
+    if (cls != nullptr && A.cls == nullptr) {
+      argmax_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, s>>>(acc, n, l, cls);
+      return check_launch("argmax_kernel");
+    }
+    return BNN_OK;
+  }
   if (n <= g_opt_gemv_max_n) {
     const int warps = std::min(32, l);
     dense_gemv_kernel<<<dim3((unsigned)n, (unsigned)A.lw), warps * 32, 0, s>>>(A);
@@ -533,6 +592,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
+  if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 
@@ -948,7 +1008,11 @@ bnn_status bnn_forward_staged(bnn_net* net, int n, bnn_stream_t stream) {
 const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
   if (net == nullptr || layer < 0 || layer >= (int)net->L.size()) return "";
   const LayerPlan& P = net->L[layer];
-  if (P.kind == 2) return std::min(n, net->chunk) <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
+  if (P.kind == 2) {
+    const int nn = std::min(n, net->chunk);
+    if (use_dense_tc(nn, (P.d + 31) / 32)) return "dense_tc4_kernel";
+    return nn <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
+  }
   return conv_kernel_name(P.x_dt, P.c_in, P.k);
 }
 

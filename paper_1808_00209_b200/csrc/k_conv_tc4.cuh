@@ -35,7 +35,7 @@ BNN_DEV void expand_word_fp4(uint32_t w, const uint32_t* lut256, uint32_t (&o)[4
 }
 
 template <int K, int CW, int NT>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 conv_tc4_kernel(const ConvArgs A) {
   using C = ConvTc4Cfg<K, CW, NT>;
   constexpr int R = C::R, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KK = C::KK, U = C::U;

@@ -1,0 +1,210 @@
+// k_dense_tc4.cuh -- binary fully connected layer over the batch on the tensor cores
+// (Section 3.2), tcgen05.mma kind::mxf4 with +/-1 as e2m1 and unit block scales.
+//
+// GEMM: M = 128 images per tile, N = NT >= l outputs (multiple of 16), K = d.  The packed words of
+// KC words per stage are expanded to e2m1 (16 bytes per 32-bit word = one K-chunk) in shared memory:
+// plane kw holds the 128 images' (or NT outputs') chunk of word kw, so a core matrix is 8
+// consecutive images x 16 B, SBO = 128 B, and the second K-chunk of an MMA (K = 64 = two words) is
+// the next plane (LBO = one plane).  Two stages ping-pong: the MMAs of stage s run while stage s+1 is
+// expanded.  Pad bits / rows are e2m1 zero and contribute 0.  The epilogue is lane = image: all l
+// sums of an image are in one thread, so threshold-pack and the argmax need no cross-lane work.
+#pragma once
+#include "k_conv_tc4.cuh"
+#include "k_dense.cuh"
+
+namespace bnn {
+
+template <int NT>
+struct DenseTc4Cfg {
+  static constexpr int KC = 16;                         // words per stage (8 MMAs)
+  static constexpr uint32_t A_BYTES = KC * 128 * 16;    // 32 KB
+  static constexpr uint32_t B_BYTES = KC * NT * 16;
+  static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
+  static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 + 16;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(256, 1)
+dense_tc4_kernel(const DenseArgs A) {
+  using C = DenseTc4Cfg<NT>;
+  constexpr int KC = C::KC;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* sA = dsm;                                  // 2 x [kw][128][16]
+  uint8_t* sB = dsm + 2 * C::A_BYTES;                 // 2 x [kw][NT][16]
+  float* s_thr = reinterpret_cast<float*>(sB + 2 * C::B_BYTES);
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);
+  __shared__ uint64_t bar_stage[2], bar_acc;
+  __shared__ uint32_t tmem_base_s;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.y;
+  {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= (((tid >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+    s_lut[tid] = v;
+  }
+  if (tid < NT) {
+    const int o = g * NT + tid;
+    const int t = (o < A.l && A.thr != nullptr) ? max(-(1 << 24), min(1 << 24, A.thr[o])) : 0;
+    s_thr[tid] = (float)t;
+  }
+  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  if (tid == 0) {
+    tc::mbar_init(&bar_stage[0], 1);
+    tc::mbar_init(&bar_stage[1], 1);
+    tc::mbar_init(&bar_acc, 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t sfa = tmem + NT, sfb = tmem + NT + 8;
+  if (warp < 4) {
+    tc::tmem_st8_same(sfa + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
+    tc::tmem_st8_same(sfb + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
+    tc::tmem_st_wait();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  constexpr uint32_t idesc = tc::idesc_mxf4(128, NT);
+  const int dw = (int)A.dw;
+  const int nstage = (dw + KC - 1) / KC;
+  const int ntiles = (A.n + 127) / 128;
+  const int dvalid_last = (int)(A.d - (int64_t)(dw - 1) * 32);  // valid bits of the last word
+
+  // Stage loads are 16-byte vectors (4 words of one image / one output row; requires dw % 4 == 0)
+  // prefetched into registers right after the previous stage's MMAs are issued.
+  constexpr int PA = KC * 128 / 4 / 256, PB = KC * NT / 4 / 256;
+  uint4 ra[PA], rb[PB];
+  auto load_stage = [&](int img0, int st) {
+    const int w0 = st * KC;
+#pragma unroll
+    for (int q = 0; q < PA; ++q) {
+      const int i = tid + q * 256;
+      const int r = i & 127, k4 = i >> 7, w = w0 + 4 * k4, img = img0 + r;
+      ra[q] = (w < dw && img < A.n) ? __ldg(reinterpret_cast<const uint4*>(A.x + (int64_t)img * A.dw + w))
+                                    : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      const int i = tid + q * 256;
+      const int n = i % NT, k4 = i / NT, w = w0 + 4 * k4, o = g * NT + n;
+      rb[q] = (w < dw && o < A.l) ? __ldg(reinterpret_cast<const uint4*>(A.wt + (int64_t)o * A.dw + w))
+                                  : make_uint4(0, 0, 0, 0);
+    }
+  };
+  // 4 words -> 4 planes; pad bits of the last word -> e2m1 zero; words >= dw (zero vectors) -> zero
+  auto put4 = [&](uint8_t* base, int rows, int row, int w0k, uint4 v, bool valid_row) {
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int w = w0k + e;
+      uint32_t o4[4] = {0u, 0u, 0u, 0u};
+      if (valid_row && w < dw) {
+        expand_word_fp4(wv[e], s_lut, o4);
+        if (w == dw - 1 && dvalid_last < 32) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m |= (8 * q + k < dvalid_last ? 0xFu : 0u) << (4 * k);
+            o4[q] &= m;
+          }
+        }
+      }
+      *reinterpret_cast<uint4*>(base + ((size_t)(w - (w0k - (w0k % KC))) * rows + row) * 16) =
+          make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+  };
+
+  uint32_t stage_uses = 0;  // global stage counter (for mbarrier parity)
+  uint32_t acc_uses = 0;
+  if ((int)blockIdx.x < ntiles) load_stage((int)blockIdx.x * 128, 0);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int img0 = tile * 128;
+    for (int st = 0; st < nstage; ++st, ++stage_uses) {
+      const int s = stage_uses & 1;
+      if (stage_uses >= 2) tc::mbar_wait(&bar_stage[s], ((stage_uses - 2) >> 1) & 1);
+      uint8_t* a = sA + s * C::A_BYTES;
+      uint8_t* b = sB + s * C::B_BYTES;
+      const int w0 = st * KC;
+#pragma unroll
+      for (int q = 0; q < PA; ++q) {
+        const int i = tid + q * 256;
+        const int r = i & 127, k4 = i >> 7;
+        put4(a, 128, r, w0 + 4 * k4, ra[q], img0 + r < A.n);
+      }
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const int i = tid + q * 256;
+        const int n = i % NT, k4 = i / NT;
+        put4(b, NT, n, w0 + 4 * k4, rb[q], g * NT + n < A.l);
+      }
+      tc::fence_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+      if (tid == 0) {
+        const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(a), 128 * 16, 128);
+        const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(b), NT * 16, 128);
+#pragma unroll
+        for (int i = 0; i < KC / 2; ++i) {
+          tc::mma_mxf4(tmem, ad0 + (uint64_t)(2 * i * 128), bd0 + (uint64_t)(2 * i * NT), idesc, sfa, sfb,
+                       (st > 0 || i > 0) ? 1u : 0u);
+        }
+        tc::commit(&bar_stage[s]);
+        if (st == nstage - 1) tc::commit(&bar_acc);
+      }
+      // prefetch the next stage (next tile's first stage after the last one)
+      if (st + 1 < nstage) load_stage(img0, st + 1);
+      else if (tile + (int)gridDim.x < ntiles) load_stage((tile + (int)gridDim.x) * 128, 0);
+    }
+    // epilogue: warps 0-3, thread = image
+    tc::mbar_wait(&bar_acc, acc_uses & 1);
+    ++acc_uses;
+    tc::fence_after();
+    if (warp < 4) {
+      const int img = img0 + warp * 32 + lane;
+      const bool img_ok = img < A.n;
+      float best = -3.0e38f;
+      int besti = 0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT && g * NT + c0 < A.l; c0 += 32) {
+        int v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+        const int nvalid = min(32, A.l - (g * NT + c0));
+        uint32_t word = 0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) word = __funnelshift_l(__float_as_uint(s_thr[c0 + c] - __int_as_float(v[c])), word, 1);
+        word &= nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
+        if (A.flip != nullptr) {
+          uint32_t fm = 0;
+          for (int c = 0; c < nvalid; ++c) fm |= (A.flip[g * NT + c0 + c] != 0 ? 1u : 0u) << (31 - c);
+          word ^= fm;
+        }
+        if (img_ok) {
+          if (A.y != nullptr) A.y[(int64_t)img * A.lw + ((g * NT + c0) >> 5)] = word;
+          if (A.acc != nullptr)
+            for (int c = 0; c < nvalid; ++c) A.acc[(int64_t)img * A.l + g * NT + c0 + c] = (int32_t)__int_as_float(v[c]);
+          if (A.cls != nullptr) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const float f = __int_as_float(v[c]);
+              if (c < nvalid && f > best) { best = f; besti = g * NT + c0 + c; }  // first maximum wins (R19)
+            }
+          }
+        }
+      }
+      if (A.cls != nullptr && img_ok) A.cls[img] = besti;
+    }
+    tc::fence_before();
+    __syncthreads();  // TMEM accumulator drained before the next tile's first MMA
+    tc::fence_after();
+  }
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+}  // namespace bnn

@@ -144,6 +144,10 @@ def test_conv_first_layer_pooled_tc(cuda, orc, pool_tc, n, h, w, cin, cout, k, t
     (1, 16, 24, 128, 128, 3, 2),  # cw = 4, NT = 128
     (1, 14, 10, 32, 33, 7, 1),    # k = 7
     (5, 24, 16, 64, 64, 5, 1),    # many tiles per CTA (double-buffered TMEM accumulators)
+    (2, 16, 16, 300, 70, 3, 1),   # streamed (big) kernel: cw = 10, partial last stage, pad channels
+    (1, 12, 20, 256, 130, 5, 2),  # big k = 5: cw = 8, two N = 128 channel groups, ragged c_out
+    (1, 10, 10, 64, 40, 7, 1),    # big k = 7
+    (3, 8, 8, 512, 512, 3, 2),    # CIFAR conv6 shape
 ])
 @pytest.mark.parametrize("fp4", [1, 0])
 def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool, fp4):
@@ -257,6 +261,28 @@ def test_dense(cuda, orc, n, d, l):
         ra = orc.dense(xs[i].numpy(), ws.numpy())
         assert np.array_equal(acc[i], ra)
         assert np.array_equal(y[i], orc.pack(orc.binarize(ra[None], t.numpy())[0], 32))
+        assert cls[i] == orc.argmax(ra)
+
+
+@pytest.mark.parametrize("n,d,l,flip", [(300, 18432, 100, False), (256, 2040, 10, True), (400, 1024, 300, True),
+                                        (129, 4096, 129, False)])
+def test_dense_tensor_core(cuda, orc, n, d, l, flip):
+    """Large-batch dense on tcgen05 (kind::mxf4): ragged image tiles, d with a partial last word,
+    l > 256 (two output groups), thresholds + flips, fused argmax (l <= NT) or the argmax kernel."""
+    xs = synth.pm1((n, d), 95 + d)
+    ws = synth.pm1((l, d), 96 + l)
+    t = synth.int_thresholds(l, 97, -40, 41)
+    f = synth.flips(l, 98) if flip else None
+    xp = cuda.pack(dev(xs).view(n, 1, 1, d)).view(n, -1)
+    y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None if f is None else dev(f),
+                             want_acc=True, want_cls=True)
+    torch.cuda.synchronize()
+    acc, y, cls = acc.cpu().numpy(), u32(y), cls.cpu().numpy()
+    for i in range(0, n, 7):
+        ra = orc.dense(xs[i].numpy(), ws.numpy())
+        assert np.array_equal(acc[i], ra)
+        b = orc.binarize(ra[None], t.numpy(), None if f is None else f.numpy())[0]
+        assert np.array_equal(y[i], orc.pack(b, 32))
         assert cls[i] == orc.argmax(ra)
 
 
