@@ -186,11 +186,15 @@ def dominant_roofline(net, spec, mode, stage_ms, stage_launch, images_total, clo
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     peaks = read_peaks()
-    if "_tc_" in kernel:
+    if "_tc" in kernel or "_tma_" in kernel:
+        fp4 = "tc4" in kernel  # kind::mxf4 kernels: fp4 dense peak = 4 x bf16 (nominal ratio), else int8 = 2 x bf16
+        ratio = 4.0 if fp4 else 2.0
         achieved = 2.0 * mac_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3)
-        peak = 2.0 * peaks["bf16_sustained"] * 1e12
-        r = {"bound": "tensor", "pipe": "tcgen05 kind::i8", "unit": "TOPS (int8, 2 x binary MAC)",
-             "peak_basis": "int8 dense = 2 x bf16 sustained %.1f TFLOP/s, %s" % (peaks["bf16_sustained"], peaks["source"]),
+        peak = ratio * peaks["bf16_sustained"] * 1e12
+        r = {"bound": "tensor", "pipe": "tcgen05 kind::mxf4" if fp4 else "tcgen05 kind::i8",
+             "unit": "TOPS (%s, 2 x binary MAC)" % ("fp4" if fp4 else "int8"),
+             "peak_basis": "%s dense = %g x bf16 sustained %.1f TFLOP/s, %s" % (
+                 "fp4" if fp4 else "int8", ratio, peaks["bf16_sustained"], peaks["source"]),
              "popc_equivalent_frac": popc_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3) /
                                      (POPC_PER_CLK_SM * sms * sm_max * 1e6)}
     else:

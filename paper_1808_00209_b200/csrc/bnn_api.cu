@@ -3,6 +3,7 @@
 // Every entry validates before launching, never throws, and reports through bnn_status +
 // the thread-local bnn_last_error().
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -16,6 +17,7 @@
 #include "k_conv.cuh"
 #include "k_conv_tc.cuh"
 #include "k_conv_first_tc.cuh"
+#include "k_conv_first_tma.cuh"
 #include "k_conv_tc4.cuh"
 #include "k_dense_tc4.cuh"
 #include "k_conv_tc4_big.cuh"
@@ -67,6 +69,7 @@ int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
+int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int grid_for(int64_t work, int threads) {
@@ -263,10 +266,67 @@ bnn_status launch_conv_first_tc_pool_t(ConvArgs A, const uint8_t* xu8, const flo
   return check_launch("conv_first_tc_pool_kernel");
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+// TMA-fed pooled first layer: u8 [n, H, W, 3] viewed as a 3-D tensor (W*3 bytes, H rows, n images);
+// the row pitch must be a multiple of 16 bytes and the base 16-byte aligned.
+bool use_first_tma(const ConvArgs& A, int k, const uint8_t* xu8) {
+  return g_opt_first_tma && g_opt_first_pool_tc && A.pool == 2 && A.c_in == 3 && (k == 3 || k == 5) && ((A.W * 3) % 16) == 0 &&
+         aligned16(xu8) && tma_encoder() != nullptr;
+}
+
+template <int K, int NT>
+bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  using C = FirstTmaCfg<K, NT>;
+  auto kfn = conv_first_tma_pool_kernel<K, NT>;
+  static int occ = -1;
+  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
+  const cuuint64_t strides[2] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H * A.W * 3};
+  const cuuint32_t box[3] = {(cuuint32_t)C::RAW_W, (cuuint32_t)C::IR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tma_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xu8), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv_first_tma: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
+  kfn<<<grid, 256, 0, s>>>(A, map, T);
+  return check_launch("conv_first_tma_pool_kernel");
+}
+
 template <int SRC>
 bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   const bool wide = A.c_out > 32;
   const int c = A.c_in;
+  if constexpr (SRC == kSrcThresh) {
+    if (A.n > 0 && use_first_tma(A, k, xu8)) {
+      if (k == 5) return wide ? launch_conv_first_tma_t<5, 64>(A, xu8, T, s) : launch_conv_first_tma_t<5, 32>(A, xu8, T, s);
+      return wide ? launch_conv_first_tma_t<3, 64>(A, xu8, T, s) : launch_conv_first_tma_t<3, 32>(A, xu8, T, s);
+    }
+  }
   if (A.pool == 2 && g_opt_first_pool_tc) {
 #define BNN_FTCP(KK, CC)                                                                          \
   if (k == KK && c == CC)                                                                          \
@@ -591,6 +651,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
+  if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
@@ -1012,6 +1073,14 @@ const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
     const int nn = std::min(n, net->chunk);
     if (use_dense_tc(nn, (P.d + 31) / 32)) return "dense_tc4_kernel";
     return nn <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
+  }
+  if (layer == 0 && fused_input(net)) {
+    if (use_first_tc(P.c_in, P.k, kSrcThresh)) {
+      if (P.pool != 2 || !g_opt_first_pool_tc) return "conv_first_tc_kernel";
+      const bool tma = g_opt_first_tma && P.c_in == 3 && (P.k == 3 || P.k == 5) && (P.W * 3) % 16 == 0 && tma_encoder();
+      return tma ? "conv_first_tma_pool_kernel" : "conv_first_tc_pool_kernel";
+    }
+    return use_first_lp(P.c_in, P.k) ? "conv_first_lp_kernel" : "conv_strip_kernel";
   }
   return conv_kernel_name(P.x_dt, P.c_in, P.k);
 }

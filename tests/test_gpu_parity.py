@@ -386,6 +386,42 @@ def test_forward_input_threshold_edges(cuda, orc, algo, T):
         cuda.set_option("conv_algo", 0)
 
 
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("h,w,k,cout,T,mode", [
+    (96, 96, 5, 32, None, 1),
+    (34, 48, 5, 32, [-128.0, 3.0, -0.5], 1),   # t = (127, -1, 0): out-of-image bytes patched to -1
+    (32, 16, 3, 40, None, 1),                  # NT = 64 group, partial second word
+    (18, 32, 3, 96, [-20.0, -200.0, -90.0], 1),  # two channel groups (64 + 32), ragged tile rows
+    (40, 64, 5, 64, None, 0),                  # SIGN mode: x > 0
+    (2, 16, 5, 32, [1.0, 1.0, 1.0], 1),        # every in-image pixel +1, padding -1
+])
+def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
+    """The fused u8 -> threshold -> conv -> pool first layer (TMA-fed kernel with the thresholds and
+    flips folded into the MMA, and the register-staged kernel) against the oracle, read out through a
+    dense layer whose integer logits change by 2 for any wrong conv output bit."""
+    tail = [dict(kind="conv", k=1, c_out=32, pool=1)] if cout % 32 else []  # dense needs C % 32 == 0
+    spec = dict(h=h, w=w, c=3, layers=[dict(kind="conv", k=k, c_out=cout, pool=2)] + tail + [dict(kind="dense", l=8)])
+    seed = h * 7 + w + k + cout
+    layers = synth.make_weights(spec, mode, seed)
+    layers[0]["thr"] = synth.int_thresholds(cout, seed, -30, 31)
+    layers[0]["flip"] = synth.flips(cout, seed + 1)
+    dl = [dict(L, wt=cuda.pack_weights(dev(L["wt"]))) for L in layers]
+    dl[0]["thr"], dl[0]["flip"] = dev(layers[0]["thr"]), dev(layers[0]["flip"])
+    Tt = None if mode == 0 else (synth.thresholds(3, seed) if T is None else torch.tensor(T, dtype=torch.float32))
+    imgs = synth.images(5, h, w, 3, seed + 2)
+    try:
+        cuda.set_option("first_tma", tma)
+        net = cuda.Net(h, w, 3, cuda.U8, mode, None if Tt is None else dev(Tt), dl, max_batch=8)
+        if tma:
+            assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
+        lg, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("first_tma", 1)
+    ref_l, ref_c = oracle_net(orc, spec, mode, layers, Tt).forward(imgs.numpy(), threads=5)
+    assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+
+
 def test_forward_thresholds_and_chunking(cuda, orc):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
