@@ -289,12 +289,13 @@ bool use_first_tma(const ConvArgs& A, int k, const uint8_t* xu8) {
          aligned16(xu8) && tma_encoder() != nullptr;
 }
 
-template <int K, int NT>
+template <int K>
 bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  using C = FirstTmaCfg<K, NT>;
-  auto kfn = conv_first_tma_pool_kernel<K, NT>;
+  using C = FirstTmaCfg<K>;
+  auto kfn = conv_first_tma_pool_kernel<K>;
+  constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
   static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -312,8 +313,8 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv_first_tma: cuTensorMapEncodeTiled failed (%d)", (int)r);
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
-  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + NT - 1) / NT));
-  kfn<<<grid, 256, 0, s>>>(A, map, T);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
+  kfn<<<grid, 256, smem, s>>>(A, map, T);
   return check_launch("conv_first_tma_pool_kernel");
 }
 
@@ -323,8 +324,7 @@ bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, 
   const int c = A.c_in;
   if constexpr (SRC == kSrcThresh) {
     if (A.n > 0 && use_first_tma(A, k, xu8)) {
-      if (k == 5) return wide ? launch_conv_first_tma_t<5, 64>(A, xu8, T, s) : launch_conv_first_tma_t<5, 32>(A, xu8, T, s);
-      return wide ? launch_conv_first_tma_t<3, 64>(A, xu8, T, s) : launch_conv_first_tma_t<3, 32>(A, xu8, T, s);
+      return k == 5 ? launch_conv_first_tma_t<5>(A, xu8, T, s) : launch_conv_first_tma_t<3>(A, xu8, T, s);
     }
   }
   if (A.pool == 2 && g_opt_first_pool_tc) {

@@ -28,27 +28,30 @@
 
 namespace bnn {
 
-template <int K, int NT>
+template <int K>
 struct FirstTmaCfg {
-  static constexpr int CIN = 3, R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW;
+  static constexpr int CIN = 3, NT = 32, R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW;
   static constexpr int IR = TH + K - 1, IC = TW + K - 1;
   // TMA needs a 16-byte aligned innermost box coordinate (measured: tools/probes/tma_probe.cu), so the
   // box starts XOFF = 16 bytes before the tile's first output column (ox0 * 3, a multiple of 48) and
-  // strip x starts at box byte DELTA + 3x; the builders read aligned words from DELTA - E.
+  // the strip of pooled column px starts at box byte DELTA + 6 px; builders read aligned words.
   static constexpr int XOFF = 16, DELTA = XOFF - 3 * R, E = DELTA & 3;
   static constexpr int C0 = (DELTA - E + 32 * 3 - XOFF) % 3;  // channel of box byte DELTA - E
-  static constexpr int RAW_W = 80;  // box row bytes (>= DELTA + IC * 3 + 4; 80 B pitch spreads smem banks)
+  static constexpr int RAW_W = 80;  // box row bytes (>= DELTA + IC * 3; 80 B pitch spreads smem banks)
   static constexpr uint32_t RAW_BYTES = IR * RAW_W;
   static constexpr uint32_t RAW_STRIDE = (RAW_BYTES + 127) / 128 * 128;  // TMA destinations 128-B aligned
   static constexpr int NRAW = 3;
-  static constexpr int S = K * CIN;
-  static constexpr int NMMA = (K + 1) / 2;
-  static constexpr int SRR = TH + 2 * NMMA - 1;  // strip rows per parity plane
-  static constexpr uint32_t A_BYTES = 2 * SRR * PW * 16;
-  static constexpr uint32_t B_BYTES = NMMA * 2 * NT * 16;
-  static constexpr uint32_t TMEM_COLS = (4 * NT <= 128) ? 128 : 256;
-  static constexpr int GROUPS = IR * (TW / 4);  // 4-strip work items
-  static_assert(S < 16 && DELTA >= 0 && DELTA - E + 12 * (TW / 4 - 1) + 28 <= RAW_W && (TW * CIN) % 16 == 0 && TW % 4 == 0 && NT % 32 == 0 && NT <= 64, "config");
+  static constexpr int KS = K + 1;        // strip rows per MMA group = taps per strip (pool offsets 0/1)
+  static constexpr int SB = KS * CIN;     // data bytes of a strip (18 for K = 5); bytes SB..31 = -1
+  static constexpr int N = 4 * NT;        // MMA N: (dy, dx) pool offsets x NT channels
+  static constexpr int SRR = IR;          // strip rows
+  static constexpr uint32_t PLANE = SRR * PW * 16;  // one 16-byte K chunk of every strip
+  static constexpr uint32_t A_BYTES = 2 * PLANE;
+  static constexpr uint32_t B_BYTES = KS * 2 * N * 16;
+  static constexpr uint32_t TMEM_COLS = 128;
+  static constexpr int GROUPS = IR * (PW / 2);  // 2-strip work items
+  static_assert(SB <= 31 && DELTA >= 0 && DELTA - E + 12 * (PW / 2 - 1) + 32 <= RAW_W && (TW * CIN) % 16 == 0 &&
+                E + 6 + SB <= 32, "config");
 };
 
 BNN_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -77,17 +80,17 @@ BNN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_addr(bar)), "r"(bytes) : "memory");
 }
 
-template <int K, int NT>
+template <int K>
 __global__ void __launch_bounds__(256, 4)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
-  using C = FirstTmaCfg<K, NT>;
+  using C = FirstTmaCfg<K>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W;
-  constexpr int NMMA = C::NMMA, SRR = C::SRR, CIN = C::CIN;
-  __shared__ __align__(128) uint8_t sRaw[C::NRAW][C::RAW_STRIDE];
-  __shared__ __align__(128) uint8_t sA[2][C::A_BYTES];
-  __shared__ __align__(128) uint8_t sB[C::B_BYTES];
+  constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* sRaw = dsm;                                   // NRAW x RAW_STRIDE
+  uint8_t* sA = sRaw + C::NRAW * C::RAW_STRIDE;          // 2 x A_BYTES: [chunk][strip row][px][16 B]
+  uint8_t* sB = sA + 2 * C::A_BYTES;                     // [strip row][chunk][n][16 B]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (for the debug acc output)
-  __shared__ uint32_t s_lut[16];
   __shared__ uint64_t raw_bar[C::NRAW], mma_bar[2];
   __shared__ uint32_t tmem_base_s;
 
@@ -110,13 +113,6 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     O[m] = (uint32_t)(0x7FFF - t[(m + 1) % 3]) | ((uint32_t)(0x7FFF - t[m]) << 16);
   }
 
-  if (tid < 16) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v |= (((tid >> (3 - k)) & 1) ? 0x01u : 0xFFu) << (8 * k);
-    s_lut[tid] = v;
-  }
-  for (int i = tid; i < 2 * (int)C::A_BYTES / 16; i += 256) reinterpret_cast<uint4*>(&sA[0][0])[i] = make_uint4(0, 0, 0, 0);
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
 #pragma unroll
@@ -137,104 +133,120 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     int img, oy0, ox0;
     tile_origin(tile, img, oy0, ox0);
     mbar_expect_tx(&raw_bar[slot], C::RAW_BYTES);
-    tma_load_3d(&sRaw[slot][0], &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_bar[slot]);
+    tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_bar[slot]);
   };
   if (tid == 0) {
     if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
     if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
   }
 
-  // weights: int8 +/-1 (negated for flipped channels), bias thr'+1 in byte 15 of kernel rows 0 and 1
-  for (int i = tid; i < NMMA * 2 * NT; i += 256) {
-    const int n = i % NT, ky = i / NT;
-    const int o = g * NT + n;
+  // weights: column n = q * NT + o holds W[o] shifted by the pool offset q = (dy, dx): strip row s,
+  // tap t of the 6-tap strip -> W[o][s - dy][t - dx] (zero outside the kernel), int8 +/-1, negated
+  // for flipped channels; byte SB of strip row 0 carries the bias thr'+1 against the strips' -1.
+  for (int i = tid; i < KS * 2 * N; i += 256) {
+    const int n = i % N, ch16 = (i / N) & 1, srow = i / (2 * N);
+    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
     const bool ok = o < A.c_out;
     const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
-    uint32_t bits = 0;
-    if (ok && ky < K) {
-#pragma unroll
-      for (int kx = 0; kx < K; ++kx)
-        bits |= (__ldg(A.wt + ((int64_t)o * K + ky) * K + kx) >> (32 - CIN)) << (32 - (kx + 1) * CIN);
-    }
-    uint32_t o4[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) m |= ((4 * q + b < C::S && ok && ky < K) ? 0xFFu : 0u) << (8 * b);
-      o4[q] = s_lut[(bits >> (28 - 4 * q)) & 0xFu] & m;
-      if (f) o4[q] ^= m & 0xFEFEFEFEu;  // +1 <-> -1 on the valid bytes
-    }
+    const int ky = srow - dy;
     // thr' = flip ? -t-1 : t, clamped to [-S_TOT-1, S_TOT] (same decisions: |acc| <= S_TOT)
     int tt = (ok && A.thr != nullptr) ? A.thr[o] : 0;
     tt = max(-S_TOT - 1, min(S_TOT, tt));
     if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
-    const int v = ok ? tt + 1 : 1;  // invalid channels: acc' = -1 -> bit 0
-    const int b0 = v / 2, b1 = v - v / 2;
-    if (ky == 0) { o4[3] = (o4[3] & 0x00FFFFFFu) | ((uint32_t)(b0 & 0xFF) << 24); if (n < NT) s_bias[n] = v; }
-    if (ky == 1) o4[3] = (o4[3] & 0x00FFFFFFu) | ((uint32_t)(b1 & 0xFF) << 24);
-    *reinterpret_cast<uint4*>(sB + ((size_t)ky * NT + n) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    const int bias = ok ? tt + 1 : 1;  // invalid channels: acc' = -1 -> bit 0
+    if (srow == 0 && ch16 == 0 && n < NT) s_bias[n] = bias;
+    uint32_t b[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int el = ch16 * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
+      int v = 0;
+      if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+        const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
+        v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
+        if (f) v = -v;
+      }
+      if (srow == 0 && el == C::SB) v = bias;
+      b[e] = (uint32_t)v & 0xFFu;
+    }
+    uint4 w4;
+    w4.x = b[0] | (b[1] << 8) | (b[2] << 16) | ((uint32_t)b[3] << 24);
+    w4.y = b[4] | (b[5] << 8) | (b[6] << 16) | ((uint32_t)b[7] << 24);
+    w4.z = b[8] | (b[9] << 8) | (b[10] << 16) | ((uint32_t)b[11] << 24);
+    w4.w = b[12] | (b[13] << 8) | (b[14] << 16) | ((uint32_t)b[15] << 24);
+    *reinterpret_cast<uint4*>(sB + ((size_t)(srow * 2 + ch16) * N + n) * 16) = w4;
   }
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  constexpr uint32_t idesc = tc::idesc_i8(128, NT, true);
+  constexpr uint32_t idesc = tc::idesc_i8(128, N, true);
 
-  // 4 strips (columns 4j..4j+3) of strip row r from the raw row bytes [12j, 12j + 24)
-  auto build = [&](int slot, int buf, int r, int j, int img, int oy0, int ox0) {
-    // box byte b = image row byte ox0*3 - XOFF + b; strip x starts at box byte DELTA + 3x
-    constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of group 0
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(&sRaw[slot][r * RAW_W + WB + 12 * j]);
-    uint32_t T[7];
+  // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
+  auto build = [&](int slot, int buf, int r, int j, int oy0, int ox0) {
+    constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
+    uint32_t T[8];
 #pragma unroll
-    for (int w = 0; w < 7; ++w) T[w] = thresh4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
+    for (int w = 0; w < 8; ++w) T[w] = thresh4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
     if (!zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
       const int gy = oy0 - R + r;
       const bool row_ok = gy >= 0 && gy < A.H;
 #pragma unroll
-      for (int w = 0; w < 7; ++w)
+      for (int w = 0; w < 8; ++w)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const int xb = ox0 * CIN - C::XOFF + WB + 12 * j + 4 * w + b;  // image row byte
           if (!row_ok || xb < 0 || xb >= A.W * CIN) T[w] |= 0xFFu << (8 * b);
         }
     }
+    uint8_t* a = sA + buf * C::A_BYTES;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      constexpr int e = C::E;
-      const int o = e + 3 * s, q = o >> 2, sh = 8 * (o & 3);
-      uint32_t v[4];
+    for (int s = 0; s < 2; ++s) {
+      constexpr int e0 = C::E;
+      const int o = e0 + 6 * s, qw = o >> 2, sh = 8 * (o & 3);
+      uint32_t v[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = sh ? __funnelshift_r(T[q + k], T[q + k + 1], sh) : T[q + k];
-      const int x = 4 * j + s;
-      *reinterpret_cast<uint4*>(&sA[buf][(size_t)(((x & 1) * SRR + r) * PW + (x >> 1)) * 16]) =
-          make_uint4(v[0], v[1], v[2], v[3] | 0xFF000000u);
+      for (int k = 0; k < 8; ++k) {
+        const int w = qw + k;
+        const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
+        v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+        // bytes >= SB of the strip: -1 (bias slots / unused K)
+        const int b0 = 4 * k;
+        if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
+        else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+      }
+      const int px = 2 * j + s;
+      *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
     }
   };
 
-  // epilogue of one tile: warp w -> pooled pixels 32 (w % 4) .., channel half w / 4 of each 32
+  // epilogue of one tile: warp w -> pooled pixels 32 (w % 4) .., channel half w / 4.  Everything that
+  // does not depend on the tile is computed once: the TMEM lane address, the 16 channels' valid mask,
+  // and the u16 offset of this thread's output half-word inside a tile.
   const int quarter = warp & 3, half = warp >> 2;
-  const int m_px = quarter * 32 + lane;  // pooled pixel of the tile this thread drains
+  const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;  // pooled pixel in the tile
   const int Ho = A.H >> 1, Wo = A.W >> 1;
-  const int64_t t_off = ((int64_t)(m_px / PW) * Wo + m_px % PW) * A.cwo;
-  auto epilogue = [&](int img, int oy0, int ox0, int buf, uint32_t phase) {
+  const int cb = 16 * half, word = (g * NT + cb) >> 5;
+  const bool has_word = word < A.cwo;
+  const int nvalid = min(16, A.c_out - (g * NT + cb));
+  const uint32_t vmask = nvalid >= 16 ? 0xFFFFu : (nvalid <= 0 ? 0u : (0xFFFFu << (16 - nvalid)) & 0xFFFFu);
+  const int t_off16 = 2 * ((m_py * Wo + m_pxl) * A.cwo + word) + (((cb & 31) == 0) ? 1 : 0);  // high half = ch 0-15
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
+  auto epilogue = [&](int img, int oy0, int ox0, uint16_t* y16, int buf, uint32_t phase) {
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged (warp 4 diverged in build)
     tc::mbar_wait(&mma_bar[buf], phase);
     __syncwarp();
     tc::fence_after();
-    const int py = (oy0 >> 1) + m_px / PW, px = (ox0 >> 1) + m_px % PW;
-    const bool in = py < Ho && px < Wo;
-    uint32_t* ybase = A.y + (((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll 1
-    for (int cb = 16 * half; cb < NT && ((g * NT + cb) >> 5) < A.cwo; cb += 32) {
+    if (has_word) {
+      const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
+      const bool in = py < Ho && px < Wo;
       if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
           int vv[16];
-          tc::tmem_ld16(lane_base + (uint32_t)(q * NT + cb), vv);
+          tc::tmem_ld16(lane_base + (uint32_t)(q * NT), vv);
           tc::tmem_ld_wait();
           const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
           if (in && oy < A.H && ox < A.W) {
@@ -248,24 +260,18 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         }
       }
       int a[16], b[16], c[16];
-      tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), a);
-      tc::tmem_ld16(lane_base + (uint32_t)(1 * NT + cb), b);
+      tc::tmem_ld16(lane_base + (uint32_t)(0 * NT), a);
+      tc::tmem_ld16(lane_base + (uint32_t)(1 * NT), b);
       tc::tmem_ld_wait();
 #pragma unroll
       for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
-      tc::tmem_ld16(lane_base + (uint32_t)(2 * NT + cb), b);
-      tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
+      tc::tmem_ld16(lane_base + (uint32_t)(2 * NT), b);
+      tc::tmem_ld16(lane_base + (uint32_t)(3 * NT), c);
       tc::tmem_ld_wait();
       uint32_t neg = 0;
 #pragma unroll
       for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
-      const int valid = min(16, A.c_out - (g * NT + cb));
-      uint32_t bits = ~neg & 0xFFFFu;
-      bits &= valid >= 16 ? 0xFFFFu : (valid <= 0 ? 0u : (0xFFFFu << (16 - valid)) & 0xFFFFu);
-      if (A.y != nullptr && in) {
-        uint16_t* y16 = reinterpret_cast<uint16_t*>(ybase + ((g * NT + cb) >> 5));
-        y16[((cb & 31) == 0) ? 1 : 0] = (uint16_t)bits;  // channels 0-15 = high half of the LE word
-      }
+      if (A.y != nullptr && in) y16[t_off16] = (uint16_t)(~neg & vmask);
     }
     tc::fence_before();
   };
@@ -273,6 +279,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   int it = 0;
   int64_t prev = -1;
   int p_img = 0, p_oy0 = 0, p_ox0 = 0;  // origin of the previous tile (drained this iteration)
+  uint16_t* p_y16 = nullptr;             // its output words (as u16 halves)
   for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
     const int buf = it & 1, slot = it % C::NRAW;
     if (tid == 0 && tile + 2 * stride < A.total_tiles) issue_raw(tile + 2 * stride, (it + 2) % C::NRAW);
@@ -281,32 +288,30 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     if (tid < C::GROUPS) {
       tc::mbar_wait(&raw_bar[slot], (uint32_t)((it / C::NRAW) & 1));
       if (it >= 2) tc::mbar_wait(&mma_bar[buf], (uint32_t)(((it - 2) >> 1) & 1));
-      build(slot, buf, tid >> 2, tid & 3, img, oy0, ox0);
+      build(slot, buf, tid >> 2, tid & 3, oy0, ox0);
       tc::fence_async_smem();
     }
     // single TMEM accumulator set: drain tile it-1 before tile it's MMAs
-    if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
+    if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
-      const uint32_t a0 = tc::smem_addr(&sA[buf][0]), b0 = tc::smem_addr(sB);
+      // MMA s: strip rows s + 2 * (pooled row) of both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
+      const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int dy = q >> 1, dx = q & 1;
-#pragma unroll
-        for (int p = 0; p < NMMA; ++p) {
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(((dx * SRR + dy + 2 * p) * PW) * 16), PW * 16, 2 * PW * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * NT * 16), NT * 16, 128);
-          tc::mma_i8(tmem + (uint32_t)(q * NT), ad, bd, idesc, p > 0 ? 1u : 0u);
-        }
+      for (int s = 0; s < KS; ++s) {
+        const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
+        const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
+        tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
       }
       tc::commit(&mma_bar[buf]);
     }
     prev = tile;
     p_img = img; p_oy0 = oy0; p_ox0 = ox0;
+    p_y16 = reinterpret_cast<uint16_t*>(A.y) + 2 * ((((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo);
   }
-  if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
+  if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
