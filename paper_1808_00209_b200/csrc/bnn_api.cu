@@ -19,6 +19,7 @@
 #include "k_conv_first_tc.cuh"
 #include "k_conv_first_tma.cuh"
 #include "k_conv_tc4.cuh"
+#include "k_conv_tc4_pool.cuh"
 #include "k_dense_tc4.cuh"
 #include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
@@ -69,6 +70,7 @@ int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
+int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
@@ -423,7 +425,31 @@ bnn_status launch_conv_tc4_t(ConvArgs A, cudaStream_t s) {
   return check_launch("conv_tc4_kernel");
 }
 
+template <int K>
+bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
+  using C = ConvTc4PoolCfg<K>;
+  auto kfn = conv_tc4_pool_kernel<K>;
+  static int occ = -1;
+  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
+  kfn<<<grid, 256, C::SMEM, s>>>(A);
+  return check_launch("conv_tc4_pool_kernel");
+}
+
+bool use_conv_pool_tc(int k, int cw, int pool) {
+  return g_opt_conv_tc_fp4 && g_opt_conv_pool_tc && pool == 2 && cw == 1 && (k == 3 || k == 5);
+}
+
 bnn_status dispatch_conv_tc(int k, int cw, const ConvArgs& A, cudaStream_t s) {
+  if (use_conv_pool_tc(k, cw, A.pool)) return k == 5 ? launch_conv_tc4_pool_t<5>(A, s) : launch_conv_tc4_pool_t<3>(A, s);
   if (g_opt_conv_tc_fp4) {
     if (k == 5 && cw == 1) return launch_conv_tc4_t<5, 1, 32>(A, s);
     if (k == 5 && cw == 2) return launch_conv_tc4_t<5, 2, 64>(A, s);
@@ -567,7 +593,7 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
 }
 
 // The kernel family launch_conv / the fused first layer pick (kept in step with the dispatch above).
-const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
+const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k, int pool) {
   if (x_dt == BNN_U8) return use_first_tc(c_in, k, kSrcReal) ? "conv_first_tc_kernel" : "conv_real_u8_kernel";
   if (x_dt == BNN_F32) return "conv_real_f32_kernel";
   if (use_first_tc(c_in, k, kSrcBits)) return "conv_first_tc_kernel";
@@ -575,6 +601,7 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k) {
   if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) {
     const int cw = (c_in + 31) / 32;
     if (!g_opt_conv_tc_fp4) return "conv_tc_kernel";
+    if (use_conv_pool_tc(k, cw, pool)) return "conv_tc4_pool_kernel";
     const bool small = (k == 5 && cw <= 2) || (k == 3 && (cw <= 2 || cw == 4)) || (k == 7 && cw == 1);
     return small ? "conv_tc4_kernel" : "conv_tc4_big_kernel";
   }
@@ -652,6 +679,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
+  if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
@@ -1082,7 +1110,7 @@ const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
     }
     return use_first_lp(P.c_in, P.k) ? "conv_first_lp_kernel" : "conv_strip_kernel";
   }
-  return conv_kernel_name(P.x_dt, P.c_in, P.k);
+  return conv_kernel_name(P.x_dt, P.c_in, P.k, P.pool);
 }
 
 int bnn_forward_launches(const bnn_net* net, int n) {

@@ -1,0 +1,264 @@
+// k_conv_tc4_pool.cuh -- binary conv + threshold + 2x2 OR-pool on the tensor cores with the pool
+// window folded into the MMA's N dimension (Eq. 3, Eq. 1, Section 3 max-pool; PAPER.md:212-218,
+// 242-244, 327-330), for 32-channel packed inputs (the vehicle conv2 and CIFAR-like 32-channel maps).
+//
+// M = 128 POOLED pixels (16 x 8, a 32 x 16 conv region), N = 4 x 32: column q*32 + o is output
+// channel o at pool offset q = (dy, dx), computed with the weights shifted by (dy, dx) over a
+// (K+1) x (K+1) tap window.  A K-chunk is one (window row s, window column t) position = 32 input
+// channels as 16 bytes of e2m1; for pooled pixel (pr, pc) it is the input pixel (2pr + s, 2pc + t),
+// which sits in parity plane (t & 1) at column half pc + t/2, so 8 consecutive pooled columns are 8
+// consecutive 16-byte rows (one core matrix), SBO = 2 input rows, and one MMA (K = 64) pairs window
+// rows s and s+1 (LBO = one input row).  K = 5: 3 row pairs x 6 columns = 18 MMAs of N = 128 per
+// 512 conv pixels, where the unpooled kernel (k_conv_tc4.cuh) needs 52 MMAs of N = 32 at the same
+// ~46-64 cycle issue cost.
+//
+// Threshold and flip: flipped channels get negated weights (NOT(acc > t) == (-acc) > -t-1), and the
+// accumulator is initialised to -(thr'+1) (tcgen05.st) before the first MMA of a tile, so TMEM ends
+// with acc - thr' - 1 and the pooled bit is max_q(acc'_q) >= 0: a 4-way max (VIMNMX + VIMNMX3 on the
+// fp32 bit patterns -- the integer order of IEEE bit patterns is correct about the sign) and one
+// funnel shift per channel.  fp32 sums of +/-1 products and an integer start value are exact
+// (|acc| <= 2^24, R24).  The epilogue runs on all 8 warps (pixel quarter x channel half) and stores
+// 16 channel bits per pixel as one u16.
+#pragma once
+#include "k_conv_tc4.cuh"
+
+namespace bnn {
+
+template <int K>
+struct ConvTc4PoolCfg {
+  static constexpr int R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW, NT = 32, N = 4 * NT;
+  static constexpr int IR = TH + K - 1, IC = TW + K - 1, CH = (IC + 1) / 2, NPIX = IR * IC;
+  static constexpr int KS = K + 1;                 // window rows / columns
+  static constexpr int SP = KS / 2;                // row pairs per MMA column
+  static constexpr int NMMA = SP * KS;
+  static constexpr uint32_t ROWB = CH * 16, PLANE = IR * ROWB;
+  static constexpr uint32_t A_BYTES = 2 * PLANE;
+  static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
+  static constexpr uint32_t TMEM_COLS = 256;       // N accumulator columns + block scales
+  static constexpr int PF = (NPIX + 255) / 256;
+  static constexpr uint32_t SMEM = B_BYTES + 2 * A_BYTES + 256 * 4 + NT * 4 + 64;
+  static_assert(KS % 2 == 0 && PW + (KS - 1) / 2 <= CH, "window");
+};
+
+BNN_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 2)
+conv_tc4_pool_kernel(const ConvArgs A) {
+  using C = ConvTc4PoolCfg<K>;
+  constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KS = C::KS;
+  constexpr int N = C::N, NT = C::NT;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  uint8_t* sB = dsm;                                              // [mma][K-chunk][N][16]
+  uint8_t* sA = dsm + C::B_BYTES;                                 // 2 x [plane][row][colhalf][16]
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries
+  float* s_init = reinterpret_cast<float*>(s_lut + 256);             // -(thr' + 1) per channel
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tmem_base_s;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = blockIdx.y;
+  const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
+  {
+    uint32_t v = 0;  // tid = 8 channel bits -> 8 e2m1 codes (first channel low nibble)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= (((tid >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+    s_lut[tid] = v;
+  }
+  if (tid < NT) {
+    const int o = g * NT + tid;
+    const bool ok = o < A.c_out;
+    const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
+    int tt = (ok && A.thr != nullptr) ? A.thr[o] : 0;
+    tt = max(-S_TOT - 1, min(S_TOT, tt));
+    if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
+    s_init[tid] = ok ? -(float)(tt + 1) : -1.0f;  // invalid channels: acc' = -1 -> bit 0
+  }
+  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t tmem = tmem_base_s;
+  const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // block scales: all 1.0 (UE8M0 0x7F)
+
+  // weights: MMA i = (row pair sp, window column t), K-chunk kc -> window row s = 2 sp + kc;
+  // column n = q * NT + o: W[o][s - dy][t - dx] as e2m1 (0 outside the kernel / pad channels),
+  // negated (+1 <-> -1 = nibble ^ 8) for flipped channels
+  for (int i = tid; i < C::NMMA * 2 * N; i += 256) {
+    const int n = i % N, kc = (i / N) & 1, mi = i / (2 * N);
+    const int sp = mi / KS, t = mi % KS, s = 2 * sp + kc;
+    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
+    const int ky = s - dy, kx = t - dx;
+    uint32_t o4[4] = {0u, 0u, 0u, 0u};
+    if (o < A.c_out && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+      expand_word_fp4(__ldg(A.wt + ((int64_t)o * K + ky) * K + kx), s_lut, o4);
+      const bool f = A.flip != nullptr && A.flip[o] != 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m |= (8 * w + e < A.c_in ? 0xFu : 0u) << (4 * e);
+        o4[w] &= m;
+        if (f) o4[w] ^= m & 0x88888888u;
+      }
+    }
+    *reinterpret_cast<uint4*>(sB + ((size_t)(mi * 2 + kc) * N + n) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+  }
+  // per-thread epilogue constants: warp w -> TMEM lane quarter w % 4, channel half w / 4
+  const int quarter = warp & 3, half = warp >> 2;
+  const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;
+  const int Ho = A.H >> 1, Wo = A.W >> 1;
+  const int cb = 16 * half, word = (g * NT + cb) >> 5;
+  const bool has_word = word < A.cwo;
+  const int nvalid = min(16, A.c_out - (g * NT + cb));
+  const uint32_t vmask = nvalid >= 16 ? 0xFFFFu : (nvalid <= 0 ? 0u : (0xFFFFu << (16 - nvalid)) & 0xFFFFu);
+  const int t_off16 = 2 * ((m_py * Wo + m_pxl) * A.cwo + word) + (((cb & 31) == 0) ? 1 : 0);
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
+  uint32_t initv[16];
+  __syncthreads();  // s_init
+#pragma unroll
+  for (int k = 0; k < 16; ++k) initv[k] = __float_as_uint(s_init[cb + k]);
+  // accumulator start values for the first tile, block scales
+#pragma unroll
+  for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT), initv);
+  if (warp < 4) {
+    tc::tmem_st8_same(sfa + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
+    tc::tmem_st8_same(sfb + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
+  }
+  tc::tmem_st_wait();
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
+
+  auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
+    int ty, tx;
+    tile_coords(A, tile, img, ty, tx);
+    oy0 = ty * TH;
+    ox0 = tx * TW;
+  };
+  auto epilogue = [&](int img, int oy0, int ox0, uint16_t* y16, int buf, uint32_t phase) {
+    __syncwarp();
+    tc::mbar_wait(&bar[buf], phase);
+    __syncwarp();
+    tc::fence_after();
+    const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
+    const bool in = py < Ho && px < Wo;
+    if (has_word) {
+      if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          int vv[16];
+          tc::tmem_ld16(lane_base + (uint32_t)(q * NT), vv);
+          tc::tmem_ld_wait();
+          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+          if (in && oy < A.H && ox < A.W) {
+            int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
+            for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
+              const int o = g * NT + cb + c;
+              const int a = (int)(__int_as_float(vv[c]) - __uint_as_float(initv[c]));
+              dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+            }
+          }
+        }
+      }
+      int a[16], b[16], c[16];
+      tc::tmem_ld16(lane_base + (uint32_t)(0 * NT), a);
+      tc::tmem_ld16(lane_base + (uint32_t)(1 * NT), b);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
+      tc::tmem_ld16(lane_base + (uint32_t)(2 * NT), b);
+      tc::tmem_ld16(lane_base + (uint32_t)(3 * NT), c);
+      tc::tmem_ld_wait();
+      uint32_t neg = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
+      if (A.y != nullptr && in) y16[t_off16] = (uint16_t)(~neg & vmask);
+    }
+    // start values for the next tile's accumulation (this warp's lanes and channels)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT), initv);
+    tc::tmem_st_wait();
+    tc::fence_before();
+  };
+
+  constexpr int PF = C::PF;
+  uint32_t pref[PF];
+  auto load_tile = [&](int64_t tile) {
+    int img, oy0, ox0;
+    tile_origin(tile, img, oy0, ox0);
+    const uint32_t* xin = A.x + (int64_t)img * A.H * A.W;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int p = tid + q * 256;
+      uint32_t w = 0u;  // outside the map: all -1 (R4)
+      if (p < NPIX) {
+        const int r = p / IC, c = p - r * IC;
+        const int gy = oy0 - R + r, gx = ox0 - R + c;
+        if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) w = __ldg(xin + (int64_t)gy * A.W + gx);
+      }
+      pref[q] = w;
+    }
+  };
+  if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
+
+  int it = 0;
+  int64_t prev = -1;
+  int p_img = 0, p_oy0 = 0, p_ox0 = 0;
+  uint16_t* p_y16 = nullptr;
+  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    int img, oy0, ox0;
+    tile_origin(tile, img, oy0, ox0);
+    if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] free again
+    uint8_t* a = sA + buf * C::A_BYTES;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int p = tid + q * 256;
+      if (p < NPIX) {
+        const int r = p / IC, c = p - r * IC;
+        uint32_t o4[4];
+        expand_word_fp4(pref[q], s_lut, o4);
+        *reinterpret_cast<uint4*>(a + (c & 1) * C::PLANE + r * C::ROWB + (c >> 1) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+      }
+    }
+    tc::fence_async_smem();
+    if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
+    // single accumulator set: drain tile it-1 (and re-initialise it) before tile it's MMAs
+    if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
+#pragma unroll
+      for (int sp = 0; sp < C::SP; ++sp)
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+          const uint32_t off = (uint32_t)((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16);
+          const uint64_t ad = tc::desc_kmajor(a0 + off, C::ROWB, 2 * C::ROWB);
+          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)((sp * KS + t) * 2 * N * 16), N * 16, 128);
+          tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
+        }
+      tc::commit(&bar[buf]);
+    }
+    prev = tile;
+    p_img = img; p_oy0 = oy0; p_ox0 = ox0;
+    p_y16 = reinterpret_cast<uint16_t*>(A.y) + 2 * ((((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo);
+  }
+  if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+}  // namespace bnn

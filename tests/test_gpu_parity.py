@@ -159,6 +159,25 @@ def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool, fp4):
         cuda.set_option("conv_tc_fp4", 1)
 
 
+@pytest.mark.parametrize("n,h,w,cout,k,thr", [
+    (3, 48, 48, 32, 5, True),    # vehicle conv2
+    (2, 20, 36, 70, 5, True),    # ragged pooled tiles (10 x 18 pooled), three channel groups
+    (1, 34, 18, 33, 3, False),   # k = 3, a 1-channel last group
+    (4, 8, 16, 32, 5, True),     # map smaller than the 32 x 16 tile
+    (1, 64, 64, 16, 3, True),    # c_out < 16: the second channel half stores zero pad bits
+])
+@pytest.mark.parametrize("pool_tc", [1, 0])
+def test_conv_pool_tensor_core(cuda, orc, pool_tc, n, h, w, cout, k, thr):
+    """Pooled 32-channel binary conv with the pool window folded into the MMA N dimension (4 shifted
+    weight copies, thresholds as accumulator start values, flips as negated weights) vs the
+    per-pixel tensor-core kernel, both against the oracle (sums, packed pooled bits)."""
+    try:
+        cuda.set_option("conv_pool_tc", pool_tc)
+        conv_case(cuda, orc, n, h, w, 32, cout, k, 2, thr=thr, flip=thr, seed=2100 + h + w + k + cout)
+    finally:
+        cuda.set_option("conv_pool_tc", 1)
+
+
 @pytest.mark.parametrize("cin,k", [(3, 5), (32, 3)])
 def test_conv_threshold_flip(cuda, orc, cin, k):
     conv_case(cuda, orc, 2, 16, 16, cin, 40, k, 2, thr=True, flip=True, seed=7)
