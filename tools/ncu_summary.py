@@ -19,9 +19,14 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-        "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+        "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]
 LAYER_OF = {"conv_first_lp_kernel": "layer0", "conv_strip_kernel": "layer0", "conv_patch_kernel": "layer0",
-            "conv_bin_kernel": "layer1", "dense_kernel": "layer2"}
+            "conv_first_tc_kernel": "layer0", "conv_first_tc_pool_kernel": "layer0",
+            "conv_first_tma_pool_kernel": "layer0", "conv_bin_kernel": "layer1", "conv_tc_kernel": "layer1",
+            "conv_tc4_kernel": "layer1", "conv_tc4_pool_kernel": "layer1", "dense_kernel": "layer2",
+            "dense_tc4_kernel": "layer2"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
