@@ -559,14 +559,14 @@ bool use_patch(int c_in, int k) {
 
 bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c_in, const uint32_t* wt, int c_out,
                        int k, const int32_t* thr, const uint8_t* flip, int pool, uint32_t* y, void* acc,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint8_t* bimg = nullptr) {
   if ((int64_t)n * h * w == 0) return BNN_OK;
   const bool small = (w <= 8 || h <= 8);
   if (x_dt == BNN_BITS) {
     ConvArgs A{};
     A.x = (const uint32_t*)x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = (int32_t*)acc;
     A.n = n; A.H = h; A.W = w; A.cw = (c_in + 31) / 32; A.c_in = c_in; A.c_out = c_out;
-    A.cwo = (c_out + 31) / 32; A.pool = pool;
+    A.cwo = (c_out + 31) / 32; A.pool = pool; A.bimg = bimg;
     if (use_first_tc(c_in, k, kSrcBits)) return dispatch_conv_first_tc<kSrcBits>(k, A, nullptr, nullptr, s);
     if (use_first_lp(c_in, k)) return dispatch_conv_first_lp<false>(k, strip_words(c_in, k), A, nullptr, nullptr, s);
     if (c_in >= 32 && tc_supported(k, A.cw)) return dispatch_conv_tc(k, A.cw, A, s);
@@ -758,6 +758,7 @@ struct LayerPlan {
   const int32_t* thr;
   const uint8_t* flip;
   int64_t out_words_per_img;  // packed output words per image (hidden layers)
+  uint8_t* bimg = nullptr;    // pre-expanded weight operand image (pool-in-N tensor-core kernels) or null
 };
 
 struct bnn_net {
@@ -801,6 +802,7 @@ namespace {
 
 void net_free(bnn_net* net) {
   if (!net) return;
+  for (LayerPlan& P : net->L) cudaFree(P.bimg);
   cudaFree(net->packed_in);
   cudaFree(net->buf[0]);
   cudaFree(net->buf[1]);
@@ -882,7 +884,7 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     ConvArgs A{};
     A.x = nullptr; A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.y = net->buf[0]; A.acc = nullptr;
     A.n = nb; A.H = P.H; A.W = P.W; A.cw = 1; A.c_in = P.c_in; A.c_out = P.c_out;
-    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool;
+    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool; A.bimg = P.bimg;
     const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
     const bool small = (P.W <= 8 || P.H <= 8);
     bnn_status st;
@@ -911,7 +913,8 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     ProfScope ps(net, i + 1, s);
     if (P.kind == 1) {
       uint32_t* out = net->buf[i & 1];
-      st = launch_conv(cur, cur_dt, nb, P.H, P.W, P.c_in, P.wt, P.c_out, P.k, P.thr, P.flip, P.pool, out, nullptr, s);
+      st = launch_conv(cur, cur_dt, nb, P.H, P.W, P.c_in, P.wt, P.c_out, P.k, P.thr, P.flip, P.pool, out, nullptr, s,
+                       cur_dt == BNN_BITS && P.c_in == 32 ? P.bimg : nullptr);
       cur = out;
       cur_dt = BNN_BITS;
     } else if (!last) {
@@ -1018,6 +1021,33 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
   if (e != cudaSuccess) {
     net_free(net);
     return fail(BNN_E_CUDA, "bnn_net_create: workspace allocation: %s", cudaGetErrorString(e));
+  }
+  // Weight operands of the pool-in-N tensor-core kernels, expanded once here (the kernels then stage
+  // them with one bulk copy per CTA instead of re-expanding the packed weights in every CTA).
+  for (size_t i = 0; i < net->L.size() && e == cudaSuccess; ++i) {
+    LayerPlan& P = net->L[i];
+    if (P.kind != 1 || P.pool != 2 || (P.k != 3 && P.k != 5)) continue;
+    ConvArgs A{};
+    A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.c_in = P.c_in; A.c_out = P.c_out;
+    const int groups = (P.c_out + 31) / 32;
+    const bool first_u8 = i == 0 && net->in_dt == BNN_U8 && net->c == 3 && (net->mode == BNN_SIGN || net->mode == BNN_THRESH_RGB);
+    if (first_u8) {
+      const size_t bytes = (size_t)groups * (P.k == 5 ? FirstTmaCfg<5>::B_BYTES : FirstTmaCfg<3>::B_BYTES);
+      if ((e = cudaMalloc(&P.bimg, bytes)) != cudaSuccess) break;
+      if (P.k == 5) prep_first_tma_kernel<5><<<groups, 256>>>(A, P.bimg);
+      else prep_first_tma_kernel<3><<<groups, 256>>>(A, P.bimg);
+    } else if (P.x_dt == BNN_BITS && P.c_in == 32) {
+      const size_t bytes = (size_t)groups * (P.k == 5 ? ConvTc4PoolCfg<5>::B_BYTES : ConvTc4PoolCfg<3>::B_BYTES);
+      if ((e = cudaMalloc(&P.bimg, bytes)) != cudaSuccess) break;
+      if (P.k == 5) prep_tc4_pool_kernel<5><<<groups, 256>>>(A, P.bimg);
+      else prep_tc4_pool_kernel<3><<<groups, 256>>>(A, P.bimg);
+    }
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    net_free(net);
+    return fail(BNN_E_CUDA, "bnn_net_create: weight image preparation: %s", cudaGetErrorString(e));
   }
   *out = net;
   return BNN_OK;

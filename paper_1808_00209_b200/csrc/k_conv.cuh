@@ -34,6 +34,7 @@ struct ConvArgs {
   int64_t total_tiles;  // < 2^31 (checked by the host)
   int tiles_per_cta;
   FastDiv fd_img, fd_tx;  // division by tiles_x * tiles_y and by tiles_x
+  const uint8_t* bimg;    // pre-expanded shared-memory image of the weight operand (per channel group) or null
 };
 
 // tile index -> (image, tile row, tile column), two multiply-high divisions

@@ -80,6 +80,62 @@ BNN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_addr(bar)), "r"(bytes) : "memory");
 }
 
+// thr'+1 of output channel o: thr' = flip ? -t-1 : t, clamped to [-S_TOT-1, S_TOT] (the same
+// decisions: |acc| <= S_TOT); invalid channels get 1 (acc' = -1 -> bit 0)
+template <int K>
+BNN_DEV int first_tma_bias(const ConvArgs& A, int o) {
+  constexpr int S_TOT = K * K * 3;
+  if (o >= A.c_out) return 1;
+  const bool f = A.flip != nullptr && A.flip[o] != 0;
+  int tt = A.thr != nullptr ? A.thr[o] : 0;
+  tt = max(-S_TOT - 1, min(S_TOT, tt));
+  if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
+  return tt + 1;
+}
+
+// The shared-memory image of the weight operand for channel group g ([strip row][K chunk][n][16 B]):
+// column n = q * NT + o holds W[o] shifted by the pool offset q = (dy, dx): strip row s, tap t of the
+// 6-tap strip -> W[o][s - dy][t - dx] (zero outside the kernel), int8 +/-1, negated for flipped
+// channels; byte SB of strip row 0 carries the bias thr'+1 against the strips' -1.  Written by the
+// kernel itself, or once per net by prep_first_tma_kernel (then bulk-copied per CTA).
+template <int K>
+BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, int step) {
+  using C = FirstTmaCfg<K>;
+  constexpr int N = C::N, NT = C::NT, CIN = C::CIN, KS = C::KS;
+  for (int i = i0; i < KS * 2 * N; i += step) {
+    const int n = i % N, ch16 = (i / N) & 1, srow = i / (2 * N);
+    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
+    const bool ok = o < A.c_out;
+    const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
+    const int ky = srow - dy;
+    const int bias = first_tma_bias<K>(A, o);
+    uint32_t b[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int el = ch16 * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
+      int v = 0;
+      if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+        const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
+        v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
+        if (f) v = -v;
+      }
+      if (srow == 0 && el == C::SB) v = bias;
+      b[e] = (uint32_t)v & 0xFFu;
+    }
+    uint4 w4;
+    w4.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+    w4.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
+    w4.z = b[8] | (b[9] << 8) | (b[10] << 16) | (b[11] << 24);
+    w4.w = b[12] | (b[13] << 8) | (b[14] << 16) | (b[15] << 24);
+    *reinterpret_cast<uint4*>(dst + ((size_t)(srow * 2 + ch16) * N + n) * 16) = w4;
+  }
+}
+
+template <int K>
+__global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
+  stage_b_first_tma<K>(A, blockIdx.x, out + (size_t)blockIdx.x * FirstTmaCfg<K>::B_BYTES, threadIdx.x, blockDim.x);
+}
+
 template <int K>
 __global__ void __launch_bounds__(256, 4)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
@@ -91,13 +147,12 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   uint8_t* sA = sRaw + C::NRAW * C::RAW_STRIDE;          // 2 x A_BYTES: [chunk][strip row][px][16 B]
   uint8_t* sB = sA + 2 * C::A_BYTES;                     // [strip row][chunk][n][16 B]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (for the debug acc output)
-  __shared__ uint64_t raw_bar[C::NRAW], mma_bar[2];
+  __shared__ uint64_t raw_bar[C::NRAW], mma_bar[2], w_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
   const int64_t stride = gridDim.x;
-  constexpr int S_TOT = K * K * CIN;  // |acc| <= S_TOT
 
   int t[CIN];
   bool zero_ok = true;  // an all-zero (out-of-image) byte thresholds to -1 for every channel
@@ -119,6 +174,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     for (int i = 0; i < C::NRAW; ++i) tc::mbar_init(&raw_bar[i], 1);
     tc::mbar_init(&mma_bar[0], 1);
     tc::mbar_init(&mma_bar[1], 1);
+    tc::mbar_init(&w_bar, 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -140,40 +196,11 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
   }
 
-  // weights: column n = q * NT + o holds W[o] shifted by the pool offset q = (dy, dx): strip row s,
-  // tap t of the 6-tap strip -> W[o][s - dy][t - dx] (zero outside the kernel), int8 +/-1, negated
-  // for flipped channels; byte SB of strip row 0 carries the bias thr'+1 against the strips' -1.
-  for (int i = tid; i < KS * 2 * N; i += 256) {
-    const int n = i % N, ch16 = (i / N) & 1, srow = i / (2 * N);
-    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
-    const bool ok = o < A.c_out;
-    const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
-    const int ky = srow - dy;
-    // thr' = flip ? -t-1 : t, clamped to [-S_TOT-1, S_TOT] (same decisions: |acc| <= S_TOT)
-    int tt = (ok && A.thr != nullptr) ? A.thr[o] : 0;
-    tt = max(-S_TOT - 1, min(S_TOT, tt));
-    if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
-    const int bias = ok ? tt + 1 : 1;  // invalid channels: acc' = -1 -> bit 0
-    if (srow == 0 && ch16 == 0 && n < NT) s_bias[n] = bias;
-    uint32_t b[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int el = ch16 * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
-      int v = 0;
-      if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
-        const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
-        v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
-        if (f) v = -v;
-      }
-      if (srow == 0 && el == C::SB) v = bias;
-      b[e] = (uint32_t)v & 0xFFu;
-    }
-    uint4 w4;
-    w4.x = b[0] | (b[1] << 8) | (b[2] << 16) | ((uint32_t)b[3] << 24);
-    w4.y = b[4] | (b[5] << 8) | (b[6] << 16) | ((uint32_t)b[7] << 24);
-    w4.z = b[8] | (b[9] << 8) | (b[10] << 16) | ((uint32_t)b[11] << 24);
-    w4.w = b[12] | (b[13] << 8) | (b[14] << 16) | ((uint32_t)b[15] << 24);
-    *reinterpret_cast<uint4*>(sB + ((size_t)(srow * 2 + ch16) * N + n) * 16) = w4;
+  if (tid < NT) s_bias[tid] = first_tma_bias<K>(A, g * NT + tid);
+  if (A.bimg != nullptr) {
+    if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
+  } else {
+    stage_b_first_tma<K>(A, g, sB, tid, 256);
   }
   tc::fence_async_smem();
   tc::fence_before();
@@ -297,6 +324,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
+      if (it == 0 && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       // MMA s: strip rows s + 2 * (pooled row) of both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
       const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
 #pragma unroll

@@ -47,6 +47,51 @@ BNN_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
+// The shared-memory image of the weight operand for channel group g ([mma][K chunk][N][16 B]):
+// MMA i = (row pair sp, window column t), K-chunk kc -> window row s = 2 sp + kc; column
+// n = q * NT + o: W[o][s - dy][t - dx] as e2m1 (0 outside the kernel / pad channels), negated
+// (+1 <-> -1 = nibble ^ 8) for flipped channels.  lut: the 256-entry bits -> e2m1 table.
+template <int K>
+BNN_DEV void stage_b_tc4_pool(const ConvArgs& A, int g, uint8_t* dst, const uint32_t* lut, int i0, int step) {
+  using C = ConvTc4PoolCfg<K>;
+  constexpr int N = C::N, NT = C::NT, KS = C::KS;
+  for (int i = i0; i < C::NMMA * 2 * N; i += step) {
+    const int n = i % N, kc = (i / N) & 1, mi = i / (2 * N);
+    const int sp = mi / KS, t = mi % KS, s = 2 * sp + kc;
+    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
+    const int ky = s - dy, kx = t - dx;
+    uint32_t o4[4] = {0u, 0u, 0u, 0u};
+    if (o < A.c_out && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+      expand_word_fp4(__ldg(A.wt + ((int64_t)o * K + ky) * K + kx), lut, o4);
+      const bool f = A.flip != nullptr && A.flip[o] != 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m |= (8 * w + e < A.c_in ? 0xFu : 0u) << (4 * e);
+        o4[w] &= m;
+        if (f) o4[w] ^= m & 0x88888888u;
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + ((size_t)(mi * 2 + kc) * N + n) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+  }
+}
+
+BNN_DEV void fill_lut_fp4(uint32_t* lut, int tid) {
+  uint32_t v = 0;  // tid = 8 channel bits -> 8 e2m1 codes (first channel low nibble)
+#pragma unroll
+  for (int k = 0; k < 8; ++k) v |= (((tid >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+  lut[tid] = v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) prep_tc4_pool_kernel(const ConvArgs A, uint8_t* out) {
+  __shared__ uint32_t lut[256];
+  fill_lut_fp4(lut, threadIdx.x);
+  __syncthreads();
+  stage_b_tc4_pool<K>(A, blockIdx.x, out + (size_t)blockIdx.x * ConvTc4PoolCfg<K>::B_BYTES, lut, threadIdx.x, 256);
+}
+
 template <int K>
 __global__ void __launch_bounds__(256, 2)
 conv_tc4_pool_kernel(const ConvArgs A) {
@@ -58,18 +103,13 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   uint8_t* sA = dsm + C::B_BYTES;                                 // 2 x [plane][row][colhalf][16]
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries
   float* s_init = reinterpret_cast<float*>(s_lut + 256);             // -(thr' + 1) per channel
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[2], w_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
   const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
-  {
-    uint32_t v = 0;  // tid = 8 channel bits -> 8 e2m1 codes (first channel low nibble)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v |= (((tid >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
-    s_lut[tid] = v;
-  }
+  fill_lut_fp4(s_lut, tid);
   if (tid < NT) {
     const int o = g * NT + tid;
     const bool ok = o < A.c_out;
@@ -83,34 +123,17 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&w_bar, 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
   const uint32_t tmem = tmem_base_s;
   const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // block scales: all 1.0 (UE8M0 0x7F)
 
-  // weights: MMA i = (row pair sp, window column t), K-chunk kc -> window row s = 2 sp + kc;
-  // column n = q * NT + o: W[o][s - dy][t - dx] as e2m1 (0 outside the kernel / pad channels),
-  // negated (+1 <-> -1 = nibble ^ 8) for flipped channels
-  for (int i = tid; i < C::NMMA * 2 * N; i += 256) {
-    const int n = i % N, kc = (i / N) & 1, mi = i / (2 * N);
-    const int sp = mi / KS, t = mi % KS, s = 2 * sp + kc;
-    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
-    const int ky = s - dy, kx = t - dx;
-    uint32_t o4[4] = {0u, 0u, 0u, 0u};
-    if (o < A.c_out && ky >= 0 && ky < K && kx >= 0 && kx < K) {
-      expand_word_fp4(__ldg(A.wt + ((int64_t)o * K + ky) * K + kx), s_lut, o4);
-      const bool f = A.flip != nullptr && A.flip[o] != 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint32_t m = 0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) m |= (8 * w + e < A.c_in ? 0xFu : 0u) << (4 * e);
-        o4[w] &= m;
-        if (f) o4[w] ^= m & 0x88888888u;
-      }
-    }
-    *reinterpret_cast<uint4*>(sB + ((size_t)(mi * 2 + kc) * N + n) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+  if (A.bimg != nullptr) {
+    if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
+  } else {
+    stage_b_tc4_pool<K>(A, g, sB, s_lut, tid, 256);
   }
   // per-thread epilogue constants: warp w -> TMEM lane quarter w % 4, channel half w / 4
   const int quarter = warp & 3, half = warp >> 2;
@@ -240,6 +263,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
+      if (it == 0 && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
 #pragma unroll
       for (int sp = 0; sp < C::SP; ++sp)

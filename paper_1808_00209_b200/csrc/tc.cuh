@@ -66,6 +66,23 @@ BNN_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase));
 }
 
+// 1-D bulk copy global -> this CTA's shared memory (16-byte aligned, size % 16 == 0), completing
+// `bytes` transactions on `bar` (arm it with expect_tx first)
+BNN_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+BNN_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+// Stages `bytes` of a pre-expanded operand image into shared memory (thread 0 issues; wait on bar)
+BNN_DEV void stage_image(void* dst, const uint8_t* src, uint32_t bytes, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, bytes);
+  constexpr uint32_t CH = 16384;
+  for (uint32_t o = 0; o < bytes; o += CH) bulk_g2s(static_cast<uint8_t*>(dst) + o, src + o, bytes - o < CH ? bytes - o : CH, bar);
+}
+
 BNN_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;"); }
 BNN_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;"); }
 BNN_DEV void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;"); }
