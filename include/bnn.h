@@ -91,6 +91,16 @@ BNN_API int bnn_version(void);
  *                   kernel (lane = channel); 4 = strip kernel (lane = pixel).
  *   "tiles_per_cta" 0 = automatic (default); k > 0 = every conv CTA walks k output tiles.
  *   "gemv_max_n"    dense layers over n <= value images use the GEMV kernel (default 16).
+ *   "conv_tc"       1 (default): binary convs run on tcgen05 tensor cores where an instantiation
+ *                   exists; 0: XOR-popcount integer pipe only (Eq. 4).
+ *   "conv_tc_fp4"   1 (default): tensor-core convs use packed e2m1 operands (kind::mxf4); 0: int8.
+ *   "conv_pool_tc"  1 (default): pooled 32-channel convs fold the 2x2 window into the MMA N.
+ *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
+ *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
+ *   "dense_tc"      1 (default): dense layers over n >= 256 images run on tensor cores.
+ *   "pdl"           1 (default): forward-path kernels use programmatic dependent launch.
+ *   "fused_max_n"   forward chunks of n <= value images (default 0 = off) of a vehicle-shaped net run as
+ *                   one cooperative kernel (whole-network fusion); 0 disables it.
  * Results are bit-identical for every setting (tiling invariance is a parity test).
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */
 BNN_API int bnn_set_option(const char* key, int value);

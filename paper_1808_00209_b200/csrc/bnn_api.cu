@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -23,6 +24,7 @@
 #include "k_dense_tc4.cuh"
 #include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
+#include "k_fused_small.cuh"
 #include "k_pack.cuh"
 
 using namespace bnn;
@@ -73,6 +75,27 @@ int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (ki
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
+
+int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
+int g_opt_pdl = 1;  // 1: forward-path kernels are launched with programmatic dependent launch
+
+// Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
+// stream predecessor is still running; it runs its prologue (barriers, TMEM, weight images) and then
+// blocks in griddep_wait() before touching activations (see common.cuh).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kfn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_opt_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kfn, std::forward<Args>(args)...);
+}
 
 int grid_for(int64_t work, int threads) {
   int64_t b = (work + threads - 1) / threads;
@@ -316,7 +339,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv_first_tma: cuTensorMapEncodeTiled failed (%d)", (int)r);
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
-  kfn<<<grid, 256, smem, s>>>(A, map, T);
+  launch_pdl(kfn, grid, dim3(256), smem, s, A, map, T);
   return check_launch("conv_first_tma_pool_kernel");
 }
 
@@ -440,7 +463,7 @@ bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
   A.tiles_per_cta = 0;
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
-  kfn<<<grid, 256, C::SMEM, s>>>(A);
+  launch_pdl(kfn, grid, dim3(256), C::SMEM, s, A);
   return check_launch("conv_tc4_pool_kernel");
 }
 
@@ -633,30 +656,30 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
       int& flag = (nt == 128) ? set_nt128 : set_nt256;
       if (!flag) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); flag = 1; }
       dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)((l + nt - 1) / nt));
-      kfn<<<grid, 256, smem, s>>>(A);
+      launch_pdl(kfn, grid, dim3(256), smem, s, A);
     };
     if (wide) launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM, 256);
     else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM, 128);
     st = check_launch("dense_tc4_kernel");
     if (st != BNN_OK) return st;
     if (cls != nullptr && A.cls == nullptr) {
-      argmax_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, s>>>(acc, n, l, cls);
+      launch_pdl(argmax_kernel, dim3(grid_for((int64_t)n * 32, 256)), dim3(256), 0, s, (const int32_t*)acc, n, l, cls);
       return check_launch("argmax_kernel");
     }
     return BNN_OK;
   }
   if (n <= g_opt_gemv_max_n) {
     const int warps = std::min(32, l);
-    dense_gemv_kernel<<<dim3((unsigned)n, (unsigned)A.lw), warps * 32, 0, s>>>(A);
+    launch_pdl(dense_gemv_kernel, dim3((unsigned)n, (unsigned)A.lw), dim3(warps * 32), 0, s, A);
     st = check_launch("dense_gemv_kernel");
   } else {
     dim3 grid((unsigned)((n + PI * NWARP - 1) / (PI * NWARP)), (unsigned)A.lw);
-    dense_kernel<PI, NWARP, DC><<<grid, NWARP * 32, 0, s>>>(A);
+    launch_pdl(dense_kernel<PI, NWARP, DC>, grid, dim3(NWARP * 32), 0, s, A);
     st = check_launch("dense_kernel");
   }
   if (st != BNN_OK) return st;
   if (cls != nullptr && l > 32) {
-    argmax_kernel<<<grid_for((int64_t)n * 32, 256), 256, 0, s>>>(acc, n, l, cls);
+    launch_pdl(argmax_kernel, dim3(grid_for((int64_t)n * 32, 256)), dim3(256), 0, s, (const int32_t*)acc, n, l, cls);
     return check_launch("argmax_kernel");
   }
   return BNN_OK;
@@ -679,6 +702,8 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
+  if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
+  if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
@@ -775,6 +800,8 @@ struct bnn_net {
   uint32_t* packed_in = nullptr;
   uint32_t* buf[2] = {nullptr, nullptr};
   int32_t* logits_tmp = nullptr;
+  unsigned* fused_ctr = nullptr;  // grid-barrier counter of fused_small_kernel
+  uint32_t* fused_w1 = nullptr;   // [32, 3] densely packed conv1 weights for fused_small_kernel
   // host-pipeline resources (lazy)
   int hchunk = 0;
   void* d_in[2] = {nullptr, nullptr};
@@ -807,6 +834,8 @@ void net_free(bnn_net* net) {
   cudaFree(net->buf[0]);
   cudaFree(net->buf[1]);
   cudaFree(net->logits_tmp);
+  cudaFree(net->fused_ctr);
+  cudaFree(net->fused_w1);
   for (int i = 0; i < 2; ++i) {
     cudaFree(net->d_in[i]);
     cudaFree(net->d_logits[i]);
@@ -872,7 +901,49 @@ bool fused_input(const bnn_net* net) {
   return use_first_tc(net->c, net->L[0].k, kSrcThresh) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
 }
 
+// Small batches of a vehicle-shaped net run as one cooperative kernel (k_fused_small.cuh).
+bool use_fused_small(const bnn_net* net, int nb) {
+  if (nb < 1 || nb > g_opt_fused_max_n || net->fused_ctr == nullptr || net->fused_w1 == nullptr) return false;
+  if (net->in_dt != BNN_U8 || (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) || net->c > 4) return false;
+  if (net->L.size() != 5 || (net->h % 4) != 0 || (net->w % 4) != 0) return false;
+  const LayerPlan &a = net->L[0], &b = net->L[1], &d1 = net->L[2], &d2 = net->L[3], &d3 = net->L[4];
+  if (a.kind != 1 || a.c_out != 32 || a.pool != 2 || a.k * a.k * net->c > 96) return false;
+  if (b.kind != 1 || b.c_in != 32 || b.c_out != 32 || b.pool != 2 || (b.k != 1 && b.k != 3 && b.k != 5)) return false;
+  if (d1.kind != 2 || d2.kind != 2 || d3.kind != 2) return false;
+  if (net->buf_words < (int64_t)(net->h / 4) * (net->w / 4) + (d1.l + 31) / 32) return false;  // y2 + h1 in buf[1]
+  if (d1.l > kFusedMaxL || d2.l > kFusedMaxL || d3.l > 32) return false;
+  return true;
+}
+
+bnn_status launch_fused_small(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
+  const LayerPlan &a = net->L[0], &b = net->L[1], &d1 = net->L[2], &d2 = net->L[3], &d3 = net->L[4];
+  FusedSmallArgs A{};
+  A.x = (const uint8_t*)images; A.T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
+  A.n = nb; A.H = net->h; A.W = net->w; A.C = net->c; A.K1 = a.k; A.K2 = b.k;
+  A.w1 = a.wt; A.w1p = net->fused_w1; A.thr1 = a.thr; A.flip1 = a.flip; A.w2 = b.wt; A.thr2 = b.thr; A.flip2 = b.flip;
+  A.f1 = d1.wt; A.f2 = d2.wt; A.f3 = d3.wt; A.thr_f1 = d1.thr; A.thr_f2 = d2.thr; A.flip_f1 = d1.flip; A.flip_f2 = d2.flip;
+  A.l1 = d1.l; A.l2 = d2.l; A.l3 = d3.l;
+  A.y1 = net->buf[0]; A.y2 = net->buf[1]; A.h1 = net->buf[1] + (int64_t)nb * (net->h / 4) * (net->w / 4); A.logits = logits; A.cls = cls; A.barrier = net->fused_ctr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)num_sms());
+  cfg.blockDim = dim3(kFusedWarps * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // co-residency of the whole grid (grid barriers)
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (b.k == 5) cudaLaunchKernelEx(&cfg, fused_small_kernel<5>, A);
+  else if (b.k == 3) cudaLaunchKernelEx(&cfg, fused_small_kernel<3>, A);
+  else cudaLaunchKernelEx(&cfg, fused_small_kernel<1>, A);
+  return check_launch("fused_small_kernel");
+}
+
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
+  if (use_fused_small(net, nb)) {
+    ProfScope ps(net, 1, s);
+    return launch_fused_small(net, images, nb, logits, cls, s);
+  }
   const void* cur = images;
   bnn_dtype cur_dt = net->in_dt;
   const int nl = (int)net->L.size();
@@ -936,7 +1007,8 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
   return BNN_OK;
 }
 
-int launches_per_chunk(const bnn_net* net, bool want_cls) {
+int launches_per_chunk(const bnn_net* net, bool want_cls, int nb) {
+  if (use_fused_small(net, nb)) return 1;
   int n = (net->mode != BNN_MODE_NONE && !fused_input(net) ? 1 : 0) + (int)net->L.size();
   if (want_cls && net->L.back().l > 32) n += 1;
   return n;
@@ -1018,6 +1090,13 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
   if (e == cudaSuccess) e = cudaMalloc(&net->buf[0], (size_t)(net->buf_words * max_batch * 4));
   if (e == cudaSuccess) e = cudaMalloc(&net->buf[1], (size_t)(net->buf_words * max_batch * 4));
   if (e == cudaSuccess) e = cudaMalloc(&net->logits_tmp, (size_t)net->L.back().l * max_batch * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&net->fused_ctr, 2 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(net->fused_ctr, 0, 2 * sizeof(unsigned));
+  if (e == cudaSuccess && net->L[0].kind == 1 && net->L[0].c_out == 32 && net->L[0].k * net->L[0].k * net->c <= 96 &&
+      net->c <= 4) {
+    e = cudaMalloc(&net->fused_w1, 32 * 3 * sizeof(uint32_t));
+    if (e == cudaSuccess) prep_fused_w1_kernel<<<1, 32>>>(net->L[0].wt, net->L[0].k, net->c, net->fused_w1);
+  }
   if (e != cudaSuccess) {
     net_free(net);
     return fail(BNN_E_CUDA, "bnn_net_create: workspace allocation: %s", cudaGetErrorString(e));
@@ -1146,7 +1225,9 @@ const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
 int bnn_forward_launches(const bnn_net* net, int n) {
   if (!net || n <= 0) return 0;
   const int chunks = (n + net->chunk - 1) / net->chunk;
-  return chunks * launches_per_chunk(net, true);
+  int total = 0;
+  for (int c = 0; c < chunks; ++c) total += launches_per_chunk(net, true, std::min(net->chunk, n - c * net->chunk));
+  return total;
 }
 
 bnn_status bnn_forward_host(bnn_net* net, const void* h_images, int n, int32_t* h_logits, int32_t* h_cls,

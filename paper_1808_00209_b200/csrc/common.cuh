@@ -46,6 +46,13 @@ BNN_DEV int u8_threshold(float t) {
   return (int)floorf(t);
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic-serialization
+// attribute may start while its predecessor runs; every thread calls griddep_wait() before touching
+// memory the predecessor writes or reads (activations), griddep_launch() lets the successor start
+// its prologue early.  Both are no-ops for kernels launched without the attribute.
+BNN_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+BNN_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 BNN_DEV int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 BNN_DEV int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 

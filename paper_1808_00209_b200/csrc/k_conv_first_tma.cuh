@@ -139,6 +139,7 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
 template <int K>
 __global__ void __launch_bounds__(256, 4)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
+  griddep_launch();
   using C = FirstTmaCfg<K>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W;
   constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN;
@@ -191,16 +192,17 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     mbar_expect_tx(&raw_bar[slot], C::RAW_BYTES);
     tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_bar[slot]);
   };
-  if (tid == 0) {
-    if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
-    if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
-  }
 
   if (tid < NT) s_bias[tid] = first_tma_bias<K>(A, g * NT + tid);
   if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
     stage_b_first_tma<K>(A, g, sB, tid, 256);
+  }
+  griddep_wait();  // the image buffer and the output buffer belong to the predecessors' stream order
+  if (tid == 0) {
+    if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
+    if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
   }
   tc::fence_async_smem();
   tc::fence_before();

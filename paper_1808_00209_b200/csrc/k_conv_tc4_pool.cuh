@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256) prep_tc4_pool_kernel(const ConvArgs A, ui
 template <int K>
 __global__ void __launch_bounds__(256, 2)
 conv_tc4_pool_kernel(const ConvArgs A) {
+  griddep_launch();
   using C = ConvTc4PoolCfg<K>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KS = C::KS;
   constexpr int N = C::N, NT = C::NT;
@@ -233,6 +234,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       pref[q] = w;
     }
   };
+  griddep_wait();  // the input map is the predecessor's output
   if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
 
   int it = 0;

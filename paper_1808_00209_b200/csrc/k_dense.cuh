@@ -28,6 +28,8 @@ struct DenseArgs {
 template <int PI, int NWARP, int DC>
 __global__ void __launch_bounds__(NWARP * 32)
 dense_kernel(const DenseArgs A) {
+  griddep_launch();
+  griddep_wait();
   constexpr int NT = NWARP * 32;
   constexpr int NIMG = PI * NWARP;
   constexpr int XP = DC + 4;  // row pitch of the activation tile (keeps 16 B alignment)
@@ -100,6 +102,8 @@ dense_kernel(const DenseArgs A) {
 // and takes the argmax.  No image slots are wasted at n = 1 (the GEMM kernel computes 64 per CTA).
 __global__ void __launch_bounds__(1024)
 dense_gemv_kernel(const DenseArgs A) {
+  griddep_launch();
+  griddep_wait();
   __shared__ int part[32];
   const int img = blockIdx.x, g = blockIdx.y;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -145,6 +149,8 @@ dense_gemv_kernel(const DenseArgs A) {
 
 // argmax over int32 logits [n, l], first maximum wins (R19).  One warp per image.
 __global__ void argmax_kernel(const int32_t* __restrict__ logits, int n, int l, int32_t* __restrict__ cls) {
+  griddep_launch();
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   for (int64_t img = gtid() >> 5; img < n; img += gstride() >> 5) {
     int bv = INT_MIN, bi = INT_MAX;

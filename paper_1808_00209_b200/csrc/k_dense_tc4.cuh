@@ -26,6 +26,7 @@ struct DenseTc4Cfg {
 template <int NT>
 __global__ void __launch_bounds__(256, 1)
 dense_tc4_kernel(const DenseArgs A) {
+  griddep_launch();
   using C = DenseTc4Cfg<NT>;
   constexpr int KC = C::KC;
   extern __shared__ __align__(1024) uint8_t dsm[];
@@ -120,6 +121,7 @@ dense_tc4_kernel(const DenseArgs A) {
 
   uint32_t stage_uses = 0;  // global stage counter (for mbarrier parity)
   uint32_t acc_uses = 0;
+  griddep_wait();  // activations of the predecessor layer
   if ((int)blockIdx.x < ntiles) load_stage((int)blockIdx.x * 128, 0);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int img0 = tile * 128;

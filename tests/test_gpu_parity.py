@@ -347,12 +347,23 @@ def oracle_net(orc, spec, mode, layers, T):
     return orc.Net(spec["h"], spec["w"], spec["c"], om, None if T is None else T.numpy(), ol)
 
 
+@pytest.mark.parametrize("fused", [8, 0])
 @pytest.mark.parametrize("mode", [1, 2, 3, -1, 0])
-def test_forward_vehicle(cuda, orc, mode):
+def test_forward_vehicle(cuda, orc, mode, fused):
+    """All input modes end to end; fused = 8: batches of <= 8 images run as the single cooperative
+    whole-network kernel (RGB / SIGN), fused = 0: layer by layer."""
+    forward_vehicle_case(cuda, orc, mode, fused)
+
+
+def forward_vehicle_case(cuda, orc, mode, fused):
     net, layers, T = build_net(cuda, synth.VEHICLE, mode, 500 + mode)
     imgs = synth.images(6, 96, 96, 3, 600 + mode)
-    logits, cls = net.forward(dev(imgs))
-    torch.cuda.synchronize()
+    try:
+        cuda.set_option("fused_max_n", fused)
+        logits, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("fused_max_n", 0)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=6)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
@@ -364,7 +375,7 @@ def test_forward_vehicle_unfused_first_layer(cuda, orc, mode, algo):
     """The same net through the separate pack kernel + generic (1) / dense-patch (2) first layer."""
     try:
         cuda.set_option("conv_algo", algo)
-        test_forward_vehicle(cuda, orc, mode)
+        forward_vehicle_case(cuda, orc, mode, 0)
     finally:
         cuda.set_option("conv_algo", 0)
 
@@ -441,12 +452,32 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
 
-def test_forward_thresholds_and_chunking(cuda, orc):
+def test_forward_pooled_layers_weight_images(cuda, orc):
+    """Nets whose pool-in-N layers stage weight images prepared once by bnn_net_create (first layer
+    with two channel groups, a 32-channel conv with two channel groups), thresholds and flips on
+    every hidden layer, integer logits out of a dense layer."""
+    spec = dict(h=32, w=32, c=3, layers=[dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="conv", k=3, c_out=64, pool=2),
+                                         dict(kind="dense", l=8)])
+    net, layers, T = build_net(cuda, spec, 1, 3100, max_batch=4, thr=True)
+    assert net.layer_kernel(0, 4) == "conv_first_tma_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool_kernel"
+    imgs = synth.images(7, 32, 32, 3, 3101)  # two chunks
+    lg, cls = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref_l, ref_c = oracle_net(orc, spec, 1, layers, T).forward(imgs.numpy(), threads=7)
+    assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+
+
+@pytest.mark.parametrize("fused", [8, 0])
+def test_forward_thresholds_and_chunking(cuda, orc, fused):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
     imgs = synth.images(5, 96, 96, 3, 778)
-    logits, cls = net.forward(dev(imgs))
-    torch.cuda.synchronize()
+    try:
+        cuda.set_option("fused_max_n", fused)
+        logits, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("fused_max_n", 0)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
@@ -462,20 +493,28 @@ def test_forward_host_equals_forward(cuda):
     assert cuda.forward_launches(net, 9000) == 3 * 5
 
 
-def test_forward_staged_graph(cuda, orc):
+@pytest.mark.parametrize("fused", [8, 0])
+@pytest.mark.parametrize("pdl", [1, 0])
+def test_forward_staged_graph(cuda, orc, pdl, fused):
     """The graph-replayed latency path (config 1) equals the oracle, for n = 1 and n = 3, and a
     replay after new images were staged uses the new images."""
-    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 1400, max_batch=64)
-    onet = oracle_net(orc, synth.VEHICLE, 1, layers, T)
-    st_in, st_lg, st_cls = net.staging(4)
-    for n, seed in [(1, 1401), (3, 1402), (1, 1403), (3, 1404)]:
-        imgs = synth.images(n, 96, 96, 3, seed)
-        st_in[:n].copy_(imgs.cuda())
-        net.forward_staged(n)
-        torch.cuda.synchronize()
-        ref_l, ref_c = onet.forward(imgs.numpy(), threads=n)
-        assert np.array_equal(st_lg[:n].cpu().numpy(), ref_l)
-        assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
+    cuda.set_option("pdl", pdl)  # programmatic dependent launch between the graph's kernels
+    cuda.set_option("fused_max_n", fused)  # one cooperative whole-network kernel per replay
+    try:
+        net, layers, T = build_net(cuda, synth.VEHICLE, 1, 1400, max_batch=64)
+        onet = oracle_net(orc, synth.VEHICLE, 1, layers, T)
+        st_in, st_lg, st_cls = net.staging(4)
+        for n, seed in [(1, 1401), (3, 1402), (1, 1403), (3, 1404)]:
+            imgs = synth.images(n, 96, 96, 3, seed)
+            st_in[:n].copy_(imgs.cuda())
+            net.forward_staged(n)
+            torch.cuda.synchronize()
+            ref_l, ref_c = onet.forward(imgs.numpy(), threads=n)
+            assert np.array_equal(st_lg[:n].cpu().numpy(), ref_l)
+            assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
+    finally:
+        cuda.set_option("pdl", 1)
+        cuda.set_option("fused_max_n", 0)
 
 
 def test_forward_cifar(cuda, orc):
