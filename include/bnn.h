@@ -101,6 +101,10 @@ BNN_API int bnn_version(void);
  *   "pdl"           1 (default): forward-path kernels use programmatic dependent launch.
  *   "fused_max_n"   forward chunks of n <= value images (default 0 = off) of a vehicle-shaped net run as
  *                   one cooperative kernel (whole-network fusion); 0 disables it.
+ *   "alg1"          0 (default); 1: bnn_forward runs the paper's own design instead -- Alg. 1
+ *                   im2col + packing (B = k*k), tiled XOR-popcount GEMM, int32 max-pool, 64-segment
+ *                   FC -- as a comparison baseline (u8 SIGN / THRESH_RGB nets,
+ *                   k <= 5, no thresholds / flips; else BNN_E_UNSUPPORTED).
  * Results are bit-identical for every setting (tiling invariance is a parity test).
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */
 BNN_API int bnn_set_option(const char* key, int value);

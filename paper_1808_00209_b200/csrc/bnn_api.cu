@@ -25,6 +25,7 @@
 #include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
 #include "k_fused_small.cuh"
+#include "k_alg1.cuh"
 #include "k_pack.cuh"
 
 using namespace bnn;
@@ -77,7 +78,8 @@ int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
-int g_opt_pdl = 1;  // 1: forward-path kernels are launched with programmatic dependent launch
+int g_opt_pdl = 1;
+int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
 // stream predecessor is still running; it runs its prologue (barriers, TMEM, weight images) and then
@@ -703,6 +705,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
+  if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
@@ -802,6 +805,13 @@ struct bnn_net {
   int32_t* logits_tmp = nullptr;
   unsigned* fused_ctr = nullptr;  // grid-barrier counter of fused_small_kernel
   uint32_t* fused_w1 = nullptr;   // [32, 3] densely packed conv1 weights for fused_small_kernel
+  // the paper's design (bnn_set_option("alg1", 1)), allocated on first use
+  int alg1_chunk = 0;
+  uint32_t* alg1_patch = nullptr;             // [chunk, H, W, C] Alg. 1 packed patches
+  int32_t* alg1_f = nullptr;                  // [chunk, H, W, C_out] GEMM-conv output
+  int32_t* alg1_g[2] = {nullptr, nullptr};    // pooled maps (ping-pong)
+  uint32_t* alg1_bits[2] = {nullptr, nullptr};  // packed dense inputs / outputs
+  std::vector<uint32_t*> alg1_w;              // per conv layer: Wp [c_out, C]
   // host-pipeline resources (lazy)
   int hchunk = 0;
   void* d_in[2] = {nullptr, nullptr};
@@ -836,6 +846,10 @@ void net_free(bnn_net* net) {
   cudaFree(net->logits_tmp);
   cudaFree(net->fused_ctr);
   cudaFree(net->fused_w1);
+  cudaFree(net->alg1_patch);
+  cudaFree(net->alg1_f);
+  for (int i = 0; i < 2; ++i) { cudaFree(net->alg1_g[i]); cudaFree(net->alg1_bits[i]); }
+  for (uint32_t* w : net->alg1_w) cudaFree(w);
   for (int i = 0; i < 2; ++i) {
     cudaFree(net->d_in[i]);
     cudaFree(net->d_logits[i]);
@@ -1132,6 +1146,126 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
   return BNN_OK;
 }
 
+}  // extern "C" (reopened below)
+
+namespace {
+
+// ---- the paper's design as a comparison pipeline (k_alg1.cuh): supported for u8 SIGN / THRESH_RGB
+// nets whose conv layers have k <= 5 (B = k*k <= 32 bits per channel word) and no thresholds/flips
+bool alg1_supported(const bnn_net* net) {
+  if (net->in_dt != BNN_U8 || (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) || net->w > 512) return false;
+  for (size_t i = 0; i < net->L.size(); ++i) {
+    const LayerPlan& P = net->L[i];
+    if (P.kind == 1 && (P.k > 5 || P.thr != nullptr || P.flip != nullptr)) return false;
+    if (P.kind == 2 && i + 1 < net->L.size() && (P.thr != nullptr || P.flip != nullptr)) return false;
+  }
+  return true;
+}
+
+bnn_status alg1_prepare(bnn_net* net) {
+  if (net->alg1_chunk > 0) return BNN_OK;
+  const int chunk = std::min(net->chunk, 256);
+  int64_t patch = 0, f = 0, g = 0, bits = 0;
+  for (const LayerPlan& P : net->L) {
+    if (P.kind == 1) {
+      patch = std::max<int64_t>(patch, (int64_t)P.H * P.W * P.c_in);
+      f = std::max<int64_t>(f, (int64_t)P.H * P.W * P.c_out);
+      g = std::max<int64_t>(g, (int64_t)(P.H / P.pool) * (P.W / P.pool) * P.c_out);
+    } else {
+      bits = std::max<int64_t>(bits, std::max<int64_t>((P.d + 31) / 32, (P.l + 31) / 32));
+    }
+  }
+  cudaError_t e = cudaMalloc(&net->alg1_patch, (size_t)(patch * chunk * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->alg1_f, (size_t)(f * chunk * 4));
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&net->alg1_g[i], (size_t)(g * chunk * 4));
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMalloc(&net->alg1_bits[i], (size_t)(bits * chunk * 4));
+  for (const LayerPlan& P : net->L) {
+    if (P.kind != 1 || e != cudaSuccess) continue;
+    uint32_t* wp = nullptr;
+    e = cudaMalloc(&wp, (size_t)P.c_out * P.c_in * 4);
+    if (e == cudaSuccess) {
+      net->alg1_w.push_back(wp);
+      alg1_prep_weights_kernel<<<grid_for((int64_t)P.c_out * P.c_in, 256), 256>>>(P.wt, P.c_out, P.k, P.c_in, wp);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(BNN_E_CUDA, "alg1: workspace: %s", cudaGetErrorString(e));
+  net->alg1_chunk = chunk;
+  return BNN_OK;
+}
+
+bnn_status alg1_forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
+  const void* cur = images;
+  bool cur_u8 = true;
+  int g = 0, conv_i = 0;
+  const uint32_t* xbits = nullptr;
+  int64_t xd = 0;
+  for (size_t i = 0; i < net->L.size(); ++i) {
+    const LayerPlan& P = net->L[i];
+    ProfScope ps(net, (int)i + 1, s);
+    if (P.kind == 1) {
+      const int R = (P.k - 1) / 2;
+      const size_t smem = (size_t)(kAlg1S + 2 * R) * (P.W + 2 * R) * sizeof(int);
+      dim3 grid((unsigned)((P.H + kAlg1S - 1) / kAlg1S), (unsigned)nb), block((unsigned)P.W, kAlg1S);
+      if (cur_u8)
+        alg1_im2col_pack_kernel<true><<<grid, block, smem, s>>>(cur, net->mode == BNN_THRESH_RGB ? net->T : nullptr,
+                                                                P.H, P.W, P.c_in, P.k, net->alg1_patch);
+      else
+        alg1_im2col_pack_kernel<false><<<grid, block, smem, s>>>(cur, nullptr, P.H, P.W, P.c_in, P.k, net->alg1_patch);
+      bnn_status st = check_launch("alg1_im2col_pack_kernel");
+      if (st != BNN_OK) return st;
+      const int64_t M = (int64_t)nb * P.H * P.W;
+      dim3 gg((unsigned)((M + kAlg1Tile - 1) / kAlg1Tile), (unsigned)((P.c_out + kAlg1Tile - 1) / kAlg1Tile));
+      alg1_gemm_conv_kernel<<<gg, dim3(kAlg1Tile, kAlg1Tile), 0, s>>>(net->alg1_patch, net->alg1_w[conv_i], M, P.c_in,
+                                                                      P.c_out, P.k * P.k, net->alg1_f);
+      if ((st = check_launch("alg1_gemm_conv_kernel")) != BNN_OK) return st;
+      if (P.pool == 2) {
+        alg1_maxpool_kernel<<<grid_for((int64_t)nb * (P.H / 2) * (P.W / 2) * P.c_out, 256), 256, 0, s>>>(
+            net->alg1_f, nb, P.H, P.W, P.c_out, net->alg1_g[g]);
+        if ((st = check_launch("alg1_maxpool_kernel")) != BNN_OK) return st;
+        cur = net->alg1_g[g];
+        g ^= 1;
+      } else {
+        // unpooled: the GEMM output is the next layer's map; copy so alg1_f can be rewritten
+        cudaMemcpyAsync(net->alg1_g[g], net->alg1_f, (size_t)M * P.c_out * 4, cudaMemcpyDeviceToDevice, s);
+        cur = net->alg1_g[g];
+        g ^= 1;
+      }
+      cur_u8 = false;
+      ++conv_i;
+      continue;
+    }
+    // dense: pack the previous map first (Table 2 "including packing")
+    if (xbits == nullptr) {
+      alg1_pack_kernel<<<grid_for((int64_t)nb * ((P.d + 31) / 32), 256), 256, 0, s>>>((const int32_t*)cur, nb, P.d,
+                                                                                       net->alg1_bits[0]);
+      bnn_status st = check_launch("alg1_pack_kernel");
+      if (st != BNN_OK) return st;
+      xbits = net->alg1_bits[0];
+    }
+    xd = P.d;
+    const bool last = i + 1 == net->L.size();
+    uint32_t* ybits = net->alg1_bits[xbits == net->alg1_bits[0] ? 1 : 0];
+    int32_t* lg = logits != nullptr ? logits : net->logits_tmp;
+    if (!last) cudaMemsetAsync(ybits, 0, (size_t)nb * ((P.l + 31) / 32) * 4, s);
+    alg1_fc_kernel<<<dim3((unsigned)P.l, (unsigned)nb), 64, 0, s>>>(xbits, xd, P.wt, P.l, last ? nullptr : ybits,
+                                                                    last ? lg : nullptr);
+    bnn_status st = check_launch("alg1_fc_kernel");
+    if (st != BNN_OK) return st;
+    if (last && cls != nullptr) {
+      argmax_kernel<<<grid_for((int64_t)nb * 32, 256), 256, 0, s>>>(lg, nb, P.l, cls);
+      if ((st = check_launch("argmax_kernel")) != BNN_OK) return st;
+    }
+    xbits = ybits;
+  }
+  return BNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits, int32_t* cls, bnn_stream_t stream) {
   if (net == nullptr) return fail(BNN_E_ARG, "bnn_forward: null net");
   if (n < 0) return fail(BNN_E_ARG, "bnn_forward: n < 0");
@@ -1140,6 +1274,19 @@ bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits,
   BNN_REQUIRE_ALIGNED(logits, "bnn_forward logits");
   BNN_REQUIRE_ALIGNED(cls, "bnn_forward cls");
   const int L = net->L.back().l;
+  if (g_opt_alg1) {
+    if (!alg1_supported(net)) return fail(BNN_E_UNSUPPORTED, "bnn_forward (alg1): net not supported by the paper pipeline");
+    bnn_status st = alg1_prepare(net);
+    if (st != BNN_OK) return st;
+    for (int s0 = 0; s0 < n; s0 += net->alg1_chunk) {
+      const int nb = std::min(net->alg1_chunk, n - s0);
+      const void* x = (const uint8_t*)images + (int64_t)s0 * net->img_bytes;
+      st = alg1_forward_chunk(net, x, nb, logits ? logits + (int64_t)s0 * L : nullptr, cls ? cls + s0 : nullptr,
+                              (cudaStream_t)stream);
+      if (st != BNN_OK) return st;
+    }
+    return BNN_OK;
+  }
   for (int s0 = 0; s0 < n; s0 += net->chunk) {
     const int nb = std::min(net->chunk, n - s0);
     const void* x = (const uint8_t*)images + (int64_t)s0 * net->img_bytes;

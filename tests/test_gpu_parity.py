@@ -467,6 +467,25 @@ def test_forward_pooled_layers_weight_images(cuda, orc):
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
 
+@pytest.mark.parametrize("spec_name,mode,n", [("vehicle", 1, 3), ("vehicle", 0, 2), ("small_cifar", 1, 3)])
+def test_forward_alg1_pipeline(cuda, orc, spec_name, mode, n):
+    """The paper's own design (Alg. 1 im2col + packing, tiled XOR-popcount GEMM, int32 max-pool,
+    64-segment FC) run through bnn_forward equals the oracle bit for bit."""
+    spec = synth.VEHICLE if spec_name == "vehicle" else dict(h=16, w=16, c=3, layers=[
+        dict(kind="conv", k=3, c_out=40, pool=1), dict(kind="conv", k=3, c_out=64, pool=2),
+        dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="dense", l=70), dict(kind="dense", l=10)])
+    net, layers, T = build_net(cuda, spec, mode, 3300 + n)
+    imgs = synth.images(n, spec["h"], spec["w"], 3, 3301 + n)
+    try:
+        cuda.set_option("alg1", 1)
+        lg, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("alg1", 0)
+    ref_l, ref_c = oracle_net(orc, spec, mode, layers, T).forward(imgs.numpy(), threads=n)
+    assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+
+
 @pytest.mark.parametrize("fused", [8, 0])
 def test_forward_thresholds_and_chunking(cuda, orc, fused):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
