@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", type=int, default=8, help="sampled images checked against the oracle after timing")
-    ap.add_argument("--config", default="vehicle", choices=["vehicle", "latency", "modes", "cifar", "sweep"],
+    ap.add_argument("--config", default="vehicle", choices=["vehicle", "latency", "modes", "cifar", "sweep", "alg1"],
                     help="vehicle = the headline (default); latency = BASELINE config 1 (batch 1, 1000 images); "
                          "modes = config 2 (batch 4096, every input binarization); cifar = config 4; "
                          "sweep = config 3 (single binary conv layers)")
@@ -257,7 +257,8 @@ def main():
     if a.impl == "reference":
         return run_reference(a, rank, world)
     if a.config != "vehicle":
-        return {"latency": run_latency, "modes": run_modes, "cifar": run_cifar, "sweep": run_sweep}[a.config](a)
+        return {"latency": run_latency, "modes": run_modes, "cifar": run_cifar, "sweep": run_sweep,
+                "alg1": run_alg1}[a.config](a)
 
     import torch
     import torch.distributed as dist
@@ -483,6 +484,41 @@ def run_modes(a):
             "ms_per_step": ms, "binary_or_int_mac_per_s": sum(macs) * B / (ms * 1e-3),
             "stage_ms": [round(x / n_calls, 4) for x, c in zip(sms, cnt) if c]})
         net.close()
+
+
+def run_alg1(a):
+    """Speed-up context: the paper's own design (Alg. 1 im2col + packing, tiled XOR-popcount
+    GEMM-conv, int32 max-pool, 64-segment FC; bnn_set_option("alg1", 1)) against this framework's path,
+    same B200, same vehicle net (THRESH_RGB, no BN thresholds), batch 4096 and batch 1."""
+    import torch
+    import paper_1808_00209_b200 as bnn
+    from paper_1808_00209_b200 import synth
+    dev = torch.device("cuda", 0)
+    B = 4096
+    net, _, _ = _net_for(synth.VEHICLE, 1, a.seed, dev, B)
+    imgs = synth.images(B, 96, 96, 3, a.seed + 1, device=dev)
+    lg = torch.empty((B, 4), dtype=torch.int32, device=dev)
+    cls = torch.empty((B,), dtype=torch.int32, device=dev)
+    res = {}
+    for name, flag in [("paper_alg1", 1), ("framework", 0)]:
+        bnn.set_option("alg1", flag)
+        net.profile(True)
+        ms = _timed(lambda: net.forward(imgs, lg, cls), a.steps, a.warmup)
+        sms, cnt = net.profile_read()
+        net.profile(False)
+        n_calls = a.steps + a.warmup
+        one = imgs[:1]
+        lat = _timed(lambda: net.forward(one, lg[:1], cls[:1]), 200, 20) * 1e3
+        res[name] = {"images_per_s": B / (ms * 1e-3), "ms_per_4096": ms, "batch1_us_stream": lat,
+                     "stage_ms": [round(x / n_calls, 4) for x, c in zip(sms, cnt) if c]}
+    bnn.set_option("alg1", 0)
+    net.close()
+    _emit({"metric": "images/s", "value": res["paper_alg1"]["images_per_s"], "unit": "images/s",
+           "config": {"workload": "paper design (Alg. 1 + GEMM-conv + int32 max-pool + 64-segment FC) on the vehicle "
+                                  "net, THRESH_RGB, batch 4096, same B200"},
+           "paper_design": res["paper_alg1"], "framework": res["framework"],
+           "speedup_framework_over_paper_design": res["framework"]["images_per_s"] / res["paper_alg1"]["images_per_s"],
+           "context": "paper Table 2 (GTX 1080, batch 1): 42.58 us binarized layers total (PAPER.md:325-331)"})
 
 
 def run_cifar(a):
