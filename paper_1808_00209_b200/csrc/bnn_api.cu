@@ -234,13 +234,13 @@ bnn_status dispatch_conv_first_lp(int k, int nw, const ConvArgs& A, const uint8_
 // Resident CTAs per SM of a 256-thread tcgen05 kernel: registers, shared memory (227 KB usable,
 // ~1 KB reserved per CTA) and TMEM columns (512 per SM).
 template <typename F>
-int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols) {
+int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols, int threads = 256) {
   if (dyn_smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
   cudaFuncAttributes fa;
   int regs = 128, static_smem = 2048;
   if (cudaFuncGetAttributes(&fa, kfn) == cudaSuccess) { regs = fa.numRegs; static_smem = (int)fa.sharedSizeBytes; }
   (void)cudaGetLastError();
-  const int by_regs = 65536 / (((regs + 7) & ~7) * 256);
+  const int by_regs = 65536 / (((regs + 7) & ~7) * threads);
   const int by_smem = (227 * 1024) / ((int)dyn_smem + static_smem + 1024);
   const int by_tmem = 512 / (int)tmem_cols;
   return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_tmem, 8)));
@@ -322,7 +322,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   auto kfn = conv_first_tma_pool_kernel<K>;
   constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
   static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS);
+  if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -341,7 +341,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv_first_tma: cuTensorMapEncodeTiled failed (%d)", (int)r);
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
-  launch_pdl(kfn, grid, dim3(256), smem, s, A, map, T);
+  launch_pdl(kfn, grid, dim3(kFirstTmaThreads), smem, s, A, map, T);
   return check_launch("conv_first_tma_pool_kernel");
 }
 

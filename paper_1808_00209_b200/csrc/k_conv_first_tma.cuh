@@ -136,45 +136,46 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
   stage_b_first_tma<K>(A, blockIdx.x, out + (size_t)blockIdx.x * FirstTmaCfg<K>::B_BYTES, threadIdx.x, blockDim.x);
 }
 
+// Warp roles (no block-wide barrier in the tile loop; mbarriers carry every hand-off):
+//   warp 0, one thread : TMA producer (raw box of tile it+2 into the 3-deep ring) and MMA issuer
+//   warps 1-5          : builders (144 two-strip items of a tile)
+//   warps 6-9          : epilogue (TMEM lane quarter warp % 4, all 32 channels of a pooled pixel)
+// raw_full[s]   TMA complete_tx              -> builders          raw_empty[s] builders (5) -> producer
+// a_full[b]     builders (5)                 -> MMA issuer        mma_done[b]  MMA commit   -> epilogue, builders (A[b] reuse)
+// acc_empty     epilogue (4)                 -> MMA issuer (single TMEM accumulator set)
+constexpr int kFirstTmaThreads = 320;
+
 template <int K>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(kFirstTmaThreads, 3)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
   using C = FirstTmaCfg<K>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W;
-  constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN;
+  constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN, NB = 5;  // builder warps
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sRaw = dsm;                                   // NRAW x RAW_STRIDE
   uint8_t* sA = sRaw + C::NRAW * C::RAW_STRIDE;          // 2 x A_BYTES: [chunk][strip row][px][16 B]
   uint8_t* sB = sA + 2 * C::A_BYTES;                     // [strip row][chunk][n][16 B]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (for the debug acc output)
-  __shared__ uint64_t raw_bar[C::NRAW], mma_bar[2], w_bar;
+  __shared__ uint64_t raw_full[C::NRAW], raw_empty[C::NRAW], a_full[2], mma_done[2], acc_empty, w_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
   const int64_t stride = gridDim.x;
 
-  int t[CIN];
-  bool zero_ok = true;  // an all-zero (out-of-image) byte thresholds to -1 for every channel
-#pragma unroll
-  for (int c = 0; c < CIN; ++c) {
-    t[c] = (Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
-    zero_ok = zero_ok && t[c] >= 0;
-  }
-  uint32_t E[3], O[3];
-#pragma unroll
-  for (int m = 0; m < 3; ++m) {
-    E[m] = (uint32_t)(0x7FFF - t[m]) | ((uint32_t)(0x7FFF - t[(m + 2) % 3]) << 16);
-    O[m] = (uint32_t)(0x7FFF - t[(m + 1) % 3]) | ((uint32_t)(0x7FFF - t[m]) << 16);
-  }
-
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
 #pragma unroll
-    for (int i = 0; i < C::NRAW; ++i) tc::mbar_init(&raw_bar[i], 1);
-    tc::mbar_init(&mma_bar[0], 1);
-    tc::mbar_init(&mma_bar[1], 1);
+    for (int i = 0; i < C::NRAW; ++i) {
+      tc::mbar_init(&raw_full[i], 1);
+      tc::mbar_init(&raw_empty[i], NB);
+    }
+    tc::mbar_init(&a_full[0], NB);
+    tc::mbar_init(&a_full[1], NB);
+    tc::mbar_init(&mma_done[0], 1);
+    tc::mbar_init(&mma_done[1], 1);
+    tc::mbar_init(&acc_empty, 4);
     tc::mbar_init(&w_bar, 1);
     tc::fence_mbar_init();
   }
@@ -186,162 +187,186 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     oy0 = ty * TH;
     ox0 = tx * TW;
   };
-  auto issue_raw = [&](int64_t tile, int slot) {
-    int img, oy0, ox0;
-    tile_origin(tile, img, oy0, ox0);
-    mbar_expect_tx(&raw_bar[slot], C::RAW_BYTES);
-    tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_bar[slot]);
-  };
 
   if (tid < NT) s_bias[tid] = first_tma_bias<K>(A, g * NT + tid);
   if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
-    stage_b_first_tma<K>(A, g, sB, tid, 256);
+    stage_b_first_tma<K>(A, g, sB, tid, kFirstTmaThreads);
   }
   griddep_wait();  // the image buffer and the output buffer belong to the predecessors' stream order
-  if (tid == 0) {
-    if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
-    if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
-  }
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
-  constexpr uint32_t idesc = tc::idesc_i8(128, N, true);
 
-  // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
-  auto build = [&](int slot, int buf, int r, int j, int oy0, int ox0) {
-    constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
-    uint32_t T[8];
-#pragma unroll
-    for (int w = 0; w < 8; ++w) T[w] = thresh4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
-    if (!zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
-      const int gy = oy0 - R + r;
-      const bool row_ok = gy >= 0 && gy < A.H;
-#pragma unroll
-      for (int w = 0; w < 8; ++w)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int xb = ox0 * CIN - C::XOFF + WB + 12 * j + 4 * w + b;  // image row byte
-          if (!row_ok || xb < 0 || xb >= A.W * CIN) T[w] |= 0xFFu << (8 * b);
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer + MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_i8(128, N, true);
+      auto issue_raw = [&](int64_t tile, int slot) {
+        int img, oy0, ox0;
+        tile_origin(tile, img, oy0, ox0);
+        mbar_expect_tx(&raw_full[slot], C::RAW_BYTES);
+        tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_full[slot]);
+      };
+      if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
+      if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
+      if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+        const int buf = it & 1;
+        if (tile + 2 * stride < A.total_tiles) {
+          const int slot2 = (it + 2) % C::NRAW;  // last used by tile it-1
+          if (it >= 1) tc::mbar_wait(&raw_empty[slot2], (uint32_t)(((it - 1) / C::NRAW) & 1));
+          issue_raw(tile + 2 * stride, slot2);
         }
-    }
-    uint8_t* a = sA + buf * C::A_BYTES;
+        tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));         // strips of tile it staged
+        if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // tile it-1 drained
+        tc::fence_after();
+        // MMA s: strip rows s + 2 * (pooled row) of both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
+        const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      constexpr int e0 = C::E;
-      const int o = e0 + 6 * s, qw = o >> 2, sh = 8 * (o & 3);
-      uint32_t v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int w = qw + k;
-        const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
-        v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
-        // bytes >= SB of the strip: -1 (bias slots / unused K)
-        const int b0 = 4 * k;
-        if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
-        else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+        for (int s = 0; s < KS; ++s) {
+          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
+          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
+          tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+        }
+        tc::commit(&mma_done[buf]);
       }
-      const int px = 2 * j + s;
-      *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
     }
-  };
-
-  // epilogue of one tile: warp w -> pooled pixels 32 (w % 4) .., channel half w / 4.  Everything that
-  // does not depend on the tile is computed once: the TMEM lane address, the 16 channels' valid mask,
-  // and the u16 offset of this thread's output half-word inside a tile.
-  const int quarter = warp & 3, half = warp >> 2;
-  const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;  // pooled pixel in the tile
-  const int Ho = A.H >> 1, Wo = A.W >> 1;
-  const int cb = 16 * half, word = (g * NT + cb) >> 5;
-  const bool has_word = word < A.cwo;
-  const int nvalid = min(16, A.c_out - (g * NT + cb));
-  const uint32_t vmask = nvalid >= 16 ? 0xFFFFu : (nvalid <= 0 ? 0u : (0xFFFFu << (16 - nvalid)) & 0xFFFFu);
-  const int t_off16 = 2 * ((m_py * Wo + m_pxl) * A.cwo + word) + (((cb & 31) == 0) ? 1 : 0);  // high half = ch 0-15
-  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
-  auto epilogue = [&](int img, int oy0, int ox0, uint16_t* y16, int buf, uint32_t phase) {
-    __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged (warp 4 diverged in build)
-    tc::mbar_wait(&mma_bar[buf], phase);
     __syncwarp();
-    tc::fence_after();
-    if (has_word) {
+  } else if (warp <= NB) {
+    // ------------------------------------------------------------ builders
+    int t[CIN];
+    bool zero_ok = true;  // an all-zero (out-of-image) byte thresholds to -1 for every channel
+#pragma unroll
+    for (int c = 0; c < CIN; ++c) {
+      t[c] = (Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
+      zero_ok = zero_ok && t[c] >= 0;
+    }
+    uint32_t E[3], O[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      E[m] = (uint32_t)(0x7FFF - t[m]) | ((uint32_t)(0x7FFF - t[(m + 2) % 3]) << 16);
+      O[m] = (uint32_t)(0x7FFF - t[(m + 1) % 3]) | ((uint32_t)(0x7FFF - t[m]) << 16);
+    }
+    const int bt = tid - 32;  // item: strip row r = bt / 4, pooled columns 2j, 2j+1 with j = bt % 4
+    const int r = bt >> 2, j = bt & 3;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      const int buf = it & 1, slot = it % C::NRAW;
+      tc::mbar_wait(&raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
+      if (it >= 2) tc::mbar_wait(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      if (bt < C::GROUPS) {
+        // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
+        constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
+        uint32_t T[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) T[w] = thresh4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
+        if (!zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
+          int img, oy0, ox0;
+          tile_origin(tile, img, oy0, ox0);
+          const int gy = oy0 - R + r;
+          const bool row_ok = gy >= 0 && gy < A.H;
+#pragma unroll
+          for (int w = 0; w < 8; ++w)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int xb = ox0 * CIN - C::XOFF + WB + 12 * j + 4 * w + b;  // image row byte
+              if (!row_ok || xb < 0 || xb >= A.W * CIN) T[w] |= 0xFFu << (8 * b);
+            }
+        }
+        uint8_t* a = sA + buf * C::A_BYTES;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          constexpr int e0 = C::E;
+          const int o = e0 + 6 * s, qw = o >> 2, sh = 8 * (o & 3);
+          uint32_t v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int w = qw + k;
+            const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
+            v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+            // bytes >= SB of the strip: -1 (bias slots / unused K)
+            const int b0 = 4 * k;
+            if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
+            else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+          }
+          const int px = 2 * j + s;
+          *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
+        }
+      }
+      tc::fence_async_smem();  // generic-proxy strip writes -> the MMA (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&a_full[buf]);
+        tc::mbar_arrive(&raw_empty[slot]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;  // pooled pixel in the tile
+    const int Ho = A.H >> 1, Wo = A.W >> 1;
+    const int nvalid = min(32, A.c_out - g * NT);
+    const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
+    const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      const int buf = it & 1;
+      int img, oy0, ox0;
+      tile_origin(tile, img, oy0, ox0);
+      tc::mbar_wait(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      __syncwarp();
+      tc::fence_after();
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
       const bool in = py < Ho && px < Wo;
       if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
 #pragma unroll 1
-        for (int q = 0; q < 4; ++q) {
-          int vv[16];
-          tc::tmem_ld16(lane_base + (uint32_t)(q * NT), vv);
-          tc::tmem_ld_wait();
-          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
-          if (in && oy < A.H && ox < A.W) {
-            int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
-            for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
-              const int o = g * NT + cb + c;
-              const int a = vv[c] + s_bias[cb + c];
-              dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+        for (int q = 0; q < 4; ++q)
+#pragma unroll 1
+          for (int cb = 0; cb < NT; cb += 16) {
+            int vv[16];
+            tc::tmem_ld16(lane_base + (uint32_t)(q * NT + cb), vv);
+            tc::tmem_ld_wait();
+            const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+            if (in && oy < A.H && ox < A.W) {
+              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
+              for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
+                const int o = g * NT + cb + c;
+                const int a = vv[c] + s_bias[cb + c];
+                dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+              }
             }
           }
-        }
       }
-      int a[16], b[16], c[16];
-      tc::tmem_ld16(lane_base + (uint32_t)(0 * NT), a);
-      tc::tmem_ld16(lane_base + (uint32_t)(1 * NT), b);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
-      tc::tmem_ld16(lane_base + (uint32_t)(2 * NT), b);
-      tc::tmem_ld16(lane_base + (uint32_t)(3 * NT), c);
-      tc::tmem_ld_wait();
       uint32_t neg = 0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
-      if (A.y != nullptr && in) y16[t_off16] = (uint16_t)(~neg & vmask);
-    }
-    tc::fence_before();
-  };
-
-  int it = 0;
-  int64_t prev = -1;
-  int p_img = 0, p_oy0 = 0, p_ox0 = 0;  // origin of the previous tile (drained this iteration)
-  uint16_t* p_y16 = nullptr;             // its output words (as u16 halves)
-  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
-    const int buf = it & 1, slot = it % C::NRAW;
-    if (tid == 0 && tile + 2 * stride < A.total_tiles) issue_raw(tile + 2 * stride, (it + 2) % C::NRAW);
-    int img, oy0, ox0;
-    tile_origin(tile, img, oy0, ox0);
-    if (tid < C::GROUPS) {
-      tc::mbar_wait(&raw_bar[slot], (uint32_t)((it / C::NRAW) & 1));
-      if (it >= 2) tc::mbar_wait(&mma_bar[buf], (uint32_t)(((it - 2) >> 1) & 1));
-      build(slot, buf, tid >> 2, tid & 3, oy0, ox0);
-      tc::fence_async_smem();
-    }
-    // single TMEM accumulator set: drain tile it-1 before tile it's MMAs
-    if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (tid == 0) {
-      if (it == 0 && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
-      // MMA s: strip rows s + 2 * (pooled row) of both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
-      const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
+      for (int cb = 0; cb < NT; cb += 16) {
+        int a[16], b[16], c[16];
+        tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), a);
+        tc::tmem_ld16(lane_base + (uint32_t)(1 * NT + cb), b);
+        tc::tmem_ld_wait();
 #pragma unroll
-      for (int s = 0; s < KS; ++s) {
-        const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
-        const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
-        tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+        for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
+        tc::tmem_ld16(lane_base + (uint32_t)(2 * NT + cb), b);
+        tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
       }
-      tc::commit(&mma_bar[buf]);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty);  // TMEM may be overwritten by the next tile's MMAs
+      if (A.y != nullptr && in)
+        A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;
     }
-    prev = tile;
-    p_img = img; p_oy0 = oy0; p_ox0 = ox0;
-    p_y16 = reinterpret_cast<uint16_t*>(A.y) + 2 * ((((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo);
   }
-  if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }

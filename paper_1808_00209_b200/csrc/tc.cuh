@@ -83,6 +83,10 @@ BNN_DEV void stage_image(void* dst, const uint8_t* src, uint32_t bytes, uint64_t
   for (uint32_t o = 0; o < bytes; o += CH) bulk_g2s(static_cast<uint8_t*>(dst) + o, src + o, bytes - o < CH ? bytes - o : CH, bar);
 }
 
+BNN_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 BNN_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;"); }
 BNN_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;"); }
 BNN_DEV void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;"); }
