@@ -455,7 +455,7 @@ bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTc4PoolCfg<K>;
   auto kfn = conv_tc4_pool_kernel<K>;
   static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, kTc4PoolThreads);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -465,7 +465,7 @@ bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
   A.tiles_per_cta = 0;
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
-  launch_pdl(kfn, grid, dim3(256), C::SMEM, s, A);
+  launch_pdl(kfn, grid, dim3(kTc4PoolThreads), C::SMEM, s, A);
   return check_launch("conv_tc4_pool_kernel");
 }
 

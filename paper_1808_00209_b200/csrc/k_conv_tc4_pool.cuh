@@ -92,25 +92,37 @@ __global__ void __launch_bounds__(256) prep_tc4_pool_kernel(const ConvArgs A, ui
   stage_b_tc4_pool<K>(A, blockIdx.x, out + (size_t)blockIdx.x * ConvTc4PoolCfg<K>::B_BYTES, lut, threadIdx.x, 256);
 }
 
+// Warp roles (mbarrier hand-offs only, like conv_first_tma_pool_kernel):
+//   warp 0, one thread : MMA issuer
+//   warps 1-4          : loaders (global words of tile it+1 prefetched into registers, then
+//                        expanded to e2m1 in the A buffer of tile it)
+//   warps 5-8          : epilogue (TMEM lane quarter warp % 4, all 32 channels; re-arms the
+//                        accumulator start values after draining)
+// a_full[b]: loaders (4) -> issuer; mma_done[b]: commit -> epilogue, loaders (A[b] reuse);
+// acc_empty: epilogue (4) -> issuer (single accumulator set).
+constexpr int kTc4PoolThreads = 288;
+
 template <int K>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(kTc4PoolThreads, 2)
 conv_tc4_pool_kernel(const ConvArgs A) {
   griddep_launch();
   using C = ConvTc4PoolCfg<K>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KS = C::KS;
-  constexpr int N = C::N, NT = C::NT;
+  constexpr int N = C::N, NT = C::NT, NL = 4;  // loader warps
+  constexpr int PF = (NPIX + NL * 32 - 1) / (NL * 32);
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sB = dsm;                                              // [mma][K-chunk][N][16]
   uint8_t* sA = dsm + C::B_BYTES;                                 // 2 x [plane][row][colhalf][16]
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries
   float* s_init = reinterpret_cast<float*>(s_lut + 256);             // -(thr' + 1) per channel
-  __shared__ uint64_t bar[2], w_bar;
+  __shared__ uint64_t a_full[2], mma_done[2], acc_empty, w_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
+  const int64_t stride = gridDim.x;
   const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
-  fill_lut_fp4(s_lut, tid);
+  if (tid < 256) fill_lut_fp4(s_lut, tid);
   if (tid < NT) {
     const int o = g * NT + tid;
     const bool ok = o < A.c_out;
@@ -122,8 +134,11 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   }
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&a_full[0], NL);
+    tc::mbar_init(&a_full[1], NL);
+    tc::mbar_init(&mma_done[0], 1);
+    tc::mbar_init(&mma_done[1], 1);
+    tc::mbar_init(&acc_empty, 4);
     tc::mbar_init(&w_bar, 1);
     tc::fence_mbar_init();
   }
@@ -134,35 +149,30 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
-    stage_b_tc4_pool<K>(A, g, sB, s_lut, tid, 256);
+    if (tid < 256) stage_b_tc4_pool<K>(A, g, sB, s_lut, tid, 256);
   }
-  // per-thread epilogue constants: warp w -> TMEM lane quarter w % 4, channel half w / 4
-  const int quarter = warp & 3, half = warp >> 2;
-  const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;
-  const int Ho = A.H >> 1, Wo = A.W >> 1;
-  const int cb = 16 * half, word = (g * NT + cb) >> 5;
-  const bool has_word = word < A.cwo;
-  const int nvalid = min(16, A.c_out - (g * NT + cb));
-  const uint32_t vmask = nvalid >= 16 ? 0xFFFFu : (nvalid <= 0 ? 0u : (0xFFFFu << (16 - nvalid)) & 0xFFFFu);
-  const int t_off16 = 2 * ((m_py * Wo + m_pxl) * A.cwo + word) + (((cb & 31) == 0) ? 1 : 0);
-  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)cb;
-  uint32_t initv[16];
-  __syncthreads();  // s_init
+  // accumulator start values of the first tile and the block scales (epilogue warps 5-8 own
+  // lane quarters 1, 2, 3, 0)
+  if (warp >= 5) {
+    const int quarter = warp & 3;
+    const uint32_t lb = tmem + ((uint32_t)(quarter * 32) << 16);
+    uint32_t initv[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) initv[k] = __float_as_uint(s_init[cb + k]);
-  // accumulator start values for the first tile, block scales
+    for (int cb = 0; cb < NT; cb += 16) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT), initv);
-  if (warp < 4) {
-    tc::tmem_st8_same(sfa + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
-    tc::tmem_st8_same(sfb + ((uint32_t)(warp * 32) << 16), 0x7F7F7F7Fu);
+      for (int k = 0; k < 16; ++k) initv[k] = __float_as_uint(s_init[cb + k]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_st16(lb + (uint32_t)(q * NT + cb), initv);
+    }
+    tc::tmem_st8_same(sfa + ((uint32_t)(quarter * 32) << 16), 0x7F7F7F7Fu);
+    tc::tmem_st8_same(sfb + ((uint32_t)(quarter * 32) << 16), 0x7F7F7F7Fu);
+    tc::tmem_st_wait();
   }
-  tc::tmem_st_wait();
+  griddep_wait();  // the input map is the predecessor's output; y is ordered after its readers
   tc::fence_async_smem();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
 
   auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
     int ty, tx;
@@ -170,119 +180,144 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     oy0 = ty * TH;
     ox0 = tx * TW;
   };
-  auto epilogue = [&](int img, int oy0, int ox0, uint16_t* y16, int buf, uint32_t phase) {
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
+      if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
+      int it = 0;
+      for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+        const int buf = it & 1;
+        tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
+        if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // drained and re-armed
+        tc::fence_after();
+        const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
+#pragma unroll
+        for (int sp = 0; sp < C::SP; ++sp)
+#pragma unroll
+          for (int t = 0; t < KS; ++t) {
+            const uint32_t off = (uint32_t)((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16);
+            const uint64_t ad = tc::desc_kmajor(a0 + off, C::ROWB, 2 * C::ROWB);
+            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)((sp * KS + t) * 2 * N * 16), N * 16, 128);
+            tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
+          }
+        tc::commit(&mma_done[buf]);
+      }
+    }
     __syncwarp();
-    tc::mbar_wait(&bar[buf], phase);
-    __syncwarp();
-    tc::fence_after();
-    const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
-    const bool in = py < Ho && px < Wo;
-    if (has_word) {
+  } else if (warp <= NL) {
+    // ------------------------------------------------------------ loaders
+    const int lt = tid - 32;
+    uint32_t pref[PF];
+#define BNN_TC4P_LOAD(TILE)                                                                          \
+  do {                                                                                               \
+    int img_, oy0_, ox0_;                                                                            \
+    tile_origin((TILE), img_, oy0_, ox0_);                                                           \
+    const uint32_t* xin = A.x + (int64_t)img_ * A.H * A.W;                                           \
+    _Pragma("unroll") for (int q = 0; q < PF; ++q) {                                                 \
+      const int p = lt + q * NL * 32;                                                                \
+      uint32_t w = 0u; /* outside the map: all -1 (R4) */                                            \
+      if (p < NPIX) {                                                                                \
+        const int r = p / IC, c = p - r * IC;                                                        \
+        const int gy = oy0_ - R + r, gx = ox0_ - R + c;                                              \
+        if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) w = __ldg(xin + (int64_t)gy * A.W + gx);     \
+      }                                                                                              \
+      pref[q] = w;                                                                                   \
+    }                                                                                                \
+  } while (0)
+    if (blockIdx.x < A.total_tiles) BNN_TC4P_LOAD(blockIdx.x);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      const int buf = it & 1;
+      if (it >= 2) tc::mbar_wait(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      uint8_t* a = sA + buf * C::A_BYTES;
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int p = lt + q * NL * 32;
+        if (p < NPIX) {
+          const int r = p / IC, c = p - r * IC;
+          uint32_t o4[4];
+          expand_word_fp4(pref[q], s_lut, o4);
+          *reinterpret_cast<uint4*>(a + (c & 1) * C::PLANE + r * C::ROWB + (c >> 1) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        }
+      }
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&a_full[buf]);
+      if (tile + stride < A.total_tiles) BNN_TC4P_LOAD(tile + stride);
+    }
+#undef BNN_TC4P_LOAD
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int m_py = (quarter * 32 + lane) / PW, m_pxl = (quarter * 32 + lane) % PW;
+    const int Ho = A.H >> 1, Wo = A.W >> 1;
+    const int nvalid = min(32, A.c_out - g * NT);
+    const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
+    const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      const int buf = it & 1;
+      int img, oy0, ox0;
+      tile_origin(tile, img, oy0, ox0);
+      tc::mbar_wait(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      __syncwarp();
+      tc::fence_after();
+      const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
+      const bool in = py < Ho && px < Wo;
       if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
 #pragma unroll 1
-        for (int q = 0; q < 4; ++q) {
-          int vv[16];
-          tc::tmem_ld16(lane_base + (uint32_t)(q * NT), vv);
-          tc::tmem_ld_wait();
-          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
-          if (in && oy < A.H && ox < A.W) {
-            int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
-            for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
-              const int o = g * NT + cb + c;
-              const int a = (int)(__int_as_float(vv[c]) - __uint_as_float(initv[c]));
-              dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+        for (int q = 0; q < 4; ++q)
+#pragma unroll 1
+          for (int cb = 0; cb < NT; cb += 16) {
+            int vv[16];
+            tc::tmem_ld16(lane_base + (uint32_t)(q * NT + cb), vv);
+            tc::tmem_ld_wait();
+            const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+            if (in && oy < A.H && ox < A.W) {
+              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
+              for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
+                const int o = g * NT + cb + c;
+                const int a = (int)(__int_as_float(vv[c]) - s_init[cb + c]);
+                dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+              }
             }
           }
-        }
       }
-      int a[16], b[16], c[16];
-      tc::tmem_ld16(lane_base + (uint32_t)(0 * NT), a);
-      tc::tmem_ld16(lane_base + (uint32_t)(1 * NT), b);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
-      tc::tmem_ld16(lane_base + (uint32_t)(2 * NT), b);
-      tc::tmem_ld16(lane_base + (uint32_t)(3 * NT), c);
-      tc::tmem_ld_wait();
       uint32_t neg = 0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
-      if (A.y != nullptr && in) y16[t_off16] = (uint16_t)(~neg & vmask);
-    }
-    // start values for the next tile's accumulation (this warp's lanes and channels)
+      for (int cb = 0; cb < NT; cb += 16) {
+        int a[16], b[16], c[16];
+        tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), a);
+        tc::tmem_ld16(lane_base + (uint32_t)(1 * NT + cb), b);
+        tc::tmem_ld_wait();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT), initv);
-    tc::tmem_st_wait();
-    tc::fence_before();
-  };
-
-  constexpr int PF = C::PF;
-  uint32_t pref[PF];
-  auto load_tile = [&](int64_t tile) {
-    int img, oy0, ox0;
-    tile_origin(tile, img, oy0, ox0);
-    const uint32_t* xin = A.x + (int64_t)img * A.H * A.W;
+        for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
+        tc::tmem_ld16(lane_base + (uint32_t)(2 * NT + cb), b);
+        tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
+        tc::tmem_ld_wait();
 #pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int p = tid + q * 256;
-      uint32_t w = 0u;  // outside the map: all -1 (R4)
-      if (p < NPIX) {
-        const int r = p / IC, c = p - r * IC;
-        const int gy = oy0 - R + r, gx = ox0 - R + c;
-        if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) w = __ldg(xin + (int64_t)gy * A.W + gx);
+        for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
       }
-      pref[q] = w;
-    }
-  };
-  griddep_wait();  // the input map is the predecessor's output
-  if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
-
-  int it = 0;
-  int64_t prev = -1;
-  int p_img = 0, p_oy0 = 0, p_ox0 = 0;
-  uint16_t* p_y16 = nullptr;
-  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    int img, oy0, ox0;
-    tile_origin(tile, img, oy0, ox0);
-    if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] free again
-    uint8_t* a = sA + buf * C::A_BYTES;
+      // start values for the next tile's accumulation
 #pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int p = tid + q * 256;
-      if (p < NPIX) {
-        const int r = p / IC, c = p - r * IC;
-        uint32_t o4[4];
-        expand_word_fp4(pref[q], s_lut, o4);
-        *reinterpret_cast<uint4*>(a + (c & 1) * C::PLANE + r * C::ROWB + (c >> 1) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+      for (int cb = 0; cb < NT; cb += 16) {
+        uint32_t initv[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) initv[k] = __float_as_uint(s_init[cb + k]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT + cb), initv);
       }
+      tc::tmem_st_wait();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty);
+      if (A.y != nullptr && in)
+        A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;
     }
-    tc::fence_async_smem();
-    if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
-    // single accumulator set: drain tile it-1 (and re-initialise it) before tile it's MMAs
-    if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (tid == 0) {
-      if (it == 0 && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
-      const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
-#pragma unroll
-      for (int sp = 0; sp < C::SP; ++sp)
-#pragma unroll
-        for (int t = 0; t < KS; ++t) {
-          const uint32_t off = (uint32_t)((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16);
-          const uint64_t ad = tc::desc_kmajor(a0 + off, C::ROWB, 2 * C::ROWB);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)((sp * KS + t) * 2 * N * 16), N * 16, 128);
-          tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
-        }
-      tc::commit(&bar[buf]);
-    }
-    prev = tile;
-    p_img = img; p_oy0 = oy0; p_ox0 = ox0;
-    p_y16 = reinterpret_cast<uint16_t*>(A.y) + 2 * ((((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo);
   }
-  if (prev >= 0) epilogue(p_img, p_oy0, p_ox0, p_y16, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
