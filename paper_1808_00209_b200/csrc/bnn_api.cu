@@ -74,6 +74,7 @@ int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
+int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
@@ -316,10 +317,10 @@ bool use_first_tma(const ConvArgs& A, int k, const uint8_t* xu8) {
          aligned16(xu8) && tma_encoder() != nullptr;
 }
 
-template <int K>
+template <int K, bool FP4>
 bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  using C = FirstTmaCfg<K>;
-  auto kfn = conv_first_tma_pool_kernel<K>;
+  using C = FirstTmaCfg<K, FP4>;
+  auto kfn = conv_first_tma_pool_kernel<K, FP4>;
   constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
   static int occ = -1;
   if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
@@ -351,7 +352,8 @@ bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, 
   const int c = A.c_in;
   if constexpr (SRC == kSrcThresh) {
     if (A.n > 0 && use_first_tma(A, k, xu8)) {
-      return k == 5 ? launch_conv_first_tma_t<5>(A, xu8, T, s) : launch_conv_first_tma_t<3>(A, xu8, T, s);
+      if (g_opt_first_fp4) return k == 5 ? launch_conv_first_tma_t<5, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, true>(A, xu8, T, s);
+      return k == 5 ? launch_conv_first_tma_t<5, false>(A, xu8, T, s) : launch_conv_first_tma_t<3, false>(A, xu8, T, s);
     }
   }
   if (A.pool == 2 && g_opt_first_pool_tc) {
@@ -704,6 +706,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
+  if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
@@ -787,6 +790,7 @@ struct LayerPlan {
   const uint8_t* flip;
   int64_t out_words_per_img;  // packed output words per image (hidden layers)
   uint8_t* bimg = nullptr;    // pre-expanded weight operand image (pool-in-N tensor-core kernels) or null
+  int bimg_fp4 = -1;          // first layer: which operand type the image was built for (1 e2m1, 0 int8)
 };
 
 struct bnn_net {
@@ -969,7 +973,8 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     ConvArgs A{};
     A.x = nullptr; A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.y = net->buf[0]; A.acc = nullptr;
     A.n = nb; A.H = P.H; A.W = P.W; A.cw = 1; A.c_in = P.c_in; A.c_out = P.c_out;
-    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool; A.bimg = P.bimg;
+    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool;
+    A.bimg = (P.bimg_fp4 == (g_opt_first_fp4 ? 1 : 0)) ? P.bimg : nullptr;  // image built for this operand type
     const float* T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
     const bool small = (P.W <= 8 || P.H <= 8);
     bnn_status st;
@@ -1125,10 +1130,18 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
     const int groups = (P.c_out + 31) / 32;
     const bool first_u8 = i == 0 && net->in_dt == BNN_U8 && net->c == 3 && (net->mode == BNN_SIGN || net->mode == BNN_THRESH_RGB);
     if (first_u8) {
-      const size_t bytes = (size_t)groups * (P.k == 5 ? FirstTmaCfg<5>::B_BYTES : FirstTmaCfg<3>::B_BYTES);
-      if ((e = cudaMalloc(&P.bimg, bytes)) != cudaSuccess) break;
-      if (P.k == 5) prep_first_tma_kernel<5><<<groups, 256>>>(A, P.bimg);
-      else prep_first_tma_kernel<3><<<groups, 256>>>(A, P.bimg);
+      const bool fp4 = g_opt_first_fp4 != 0;
+      const size_t bb = P.k == 5 ? (fp4 ? FirstTmaCfg<5, true>::B_BYTES : FirstTmaCfg<5, false>::B_BYTES)
+                                 : (fp4 ? FirstTmaCfg<3, true>::B_BYTES : FirstTmaCfg<3, false>::B_BYTES);
+      if ((e = cudaMalloc(&P.bimg, (size_t)groups * bb)) != cudaSuccess) break;
+      P.bimg_fp4 = fp4 ? 1 : 0;
+      if (P.k == 5) {
+        if (fp4) prep_first_tma_kernel<5, true><<<groups, 256>>>(A, P.bimg);
+        else prep_first_tma_kernel<5, false><<<groups, 256>>>(A, P.bimg);
+      } else {
+        if (fp4) prep_first_tma_kernel<3, true><<<groups, 256>>>(A, P.bimg);
+        else prep_first_tma_kernel<3, false><<<groups, 256>>>(A, P.bimg);
+      }
     } else if (P.x_dt == BNN_BITS && P.c_in == 32) {
       const size_t bytes = (size_t)groups * (P.k == 5 ? ConvTc4PoolCfg<5>::B_BYTES : ConvTc4PoolCfg<3>::B_BYTES);
       if ((e = cudaMalloc(&P.bimg, bytes)) != cudaSuccess) break;

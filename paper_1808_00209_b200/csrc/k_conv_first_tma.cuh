@@ -28,7 +28,7 @@
 
 namespace bnn {
 
-template <int K>
+template <int K, bool FP4 = false>
 struct FirstTmaCfg {
   static constexpr int CIN = 3, NT = 32, R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW;
   static constexpr int IR = TH + K - 1, IC = TW + K - 1;
@@ -45,11 +45,15 @@ struct FirstTmaCfg {
   static constexpr int SB = KS * CIN;     // data bytes of a strip (18 for K = 5); bytes SB..31 = -1
   static constexpr int N = 4 * NT;        // MMA N: (dy, dx) pool offsets x NT channels
   static constexpr int SRR = IR;          // strip rows
-  static constexpr uint32_t PLANE = SRR * PW * 16;  // one 16-byte K chunk of every strip
-  static constexpr uint32_t A_BYTES = 2 * PLANE;
-  static constexpr uint32_t B_BYTES = KS * 2 * N * 16;
-  static constexpr uint32_t TMEM_COLS = 128;
+  // i8: a strip row is 32 int8 = two 16-byte K chunks (planes), one MMA (K = 32) per strip row;
+  // FP4: a strip row is 32 e2m1 nibbles = one 16-byte chunk, one MMA (K = 64) per pair of strip rows
+  static constexpr uint32_t PLANE = SRR * PW * 16;
+  static constexpr uint32_t A_BYTES = FP4 ? PLANE : 2 * PLANE;
+  static constexpr int NMMA = FP4 ? KS / 2 : KS;
+  static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
+  static constexpr uint32_t TMEM_COLS = FP4 ? 256 : 128;  // FP4: + block-scale columns
   static constexpr int GROUPS = IR * (PW / 2);  // 2-strip work items
+  static_assert(!FP4 || (KS % 2 == 0 && KS * (32 - SB) >= K * K * CIN / 6 + 3), "fp4 bias slots");
   static_assert(SB <= 31 && DELTA >= 0 && DELTA - E + 12 * (PW / 2 - 1) + 32 <= RAW_W && (TW * CIN) % 16 == 0 &&
                 E + 6 + SB <= 32, "config");
 };
@@ -66,6 +70,13 @@ BNN_DEV uint32_t thresh4(uint32_t x, uint32_t E, uint32_t O) {
   const uint32_t od = prmt(x, 0u, 0x4341u) + O;
   const uint32_t m = prmt(ev, od, 0xFBD9u);  // sign of lane bit 15 -> 0xFF / 0x00 per byte
   return ~m | 0x01010101u;
+}
+
+// 4 u8 -> per-byte mask 0xFF where x > t (the sign-replicating PRMT of thresh4)
+BNN_DEV uint32_t thresh_mask4(uint32_t x, uint32_t E, uint32_t O) {
+  const uint32_t ev = prmt(x, 0u, 0x4240u) + E;
+  const uint32_t od = prmt(x, 0u, 0x4341u) + O;
+  return prmt(ev, od, 0xFBD9u);
 }
 
 BNN_DEV void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
@@ -93,47 +104,80 @@ BNN_DEV int first_tma_bias(const ConvArgs& A, int o) {
   return tt + 1;
 }
 
-// The shared-memory image of the weight operand for channel group g ([strip row][K chunk][n][16 B]):
+// e2m1 code of a small integer (|v| in {0, 1, 2, 3, 4, 6})
+BNN_DEV uint32_t e2m1_int(int v) {
+  const int a = v < 0 ? -v : v;
+  const uint32_t c = a == 0 ? 0x0u : a == 1 ? 0x2u : a == 2 ? 0x4u : a == 3 ? 0x5u : a == 4 ? 0x6u : 0x7u;
+  return (v < 0 && a != 0) ? (c | 0x8u) : c;
+}
+// FP4 bias: v = thr'+1 spread over bias slot k (0, 1, ...) as 6, 6, ..., remainder (5 = 4 + 1)
+BNN_DEV int fp4_bias_part(int v, int k) {
+  const int a = v < 0 ? -v : v, sg = v < 0 ? -1 : 1;
+  const int full = a / 6, r = a % 6;
+  int part = 0;
+  if (k < full) part = 6;
+  else if (k == full) part = (r == 5) ? 4 : r;
+  else if (k == full + 1 && r == 5) part = 1;
+  return sg * part;
+}
+
+// The shared-memory image of the weight operand for channel group g ([mma][K chunk][n][16 B]):
 // column n = q * NT + o holds W[o] shifted by the pool offset q = (dy, dx): strip row s, tap t of the
-// 6-tap strip -> W[o][s - dy][t - dx] (zero outside the kernel), int8 +/-1, negated for flipped
-// channels; byte SB of strip row 0 carries the bias thr'+1 against the strips' -1.  Written by the
-// kernel itself, or once per net by prep_first_tma_kernel (then bulk-copied per CTA).
-template <int K>
+// 6-tap strip -> W[o][s - dy][t - dx] (zero outside the kernel), +/-1 negated for flipped channels.
+// i8: byte SB of strip row 0 carries the bias thr'+1 against the strips' -1; FP4 (e2m1 nibbles, K
+// chunk = one strip row): the bias is spread over the nibbles SB..31 of the strip rows (values in
+// {6, 4, 3, 2, 1}, all against -1).  Written by the kernel itself, or once per net by
+// prep_first_tma_kernel (then bulk-copied per CTA).
+template <int K, bool FP4>
 BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, int step) {
-  using C = FirstTmaCfg<K>;
-  constexpr int N = C::N, NT = C::NT, CIN = C::CIN, KS = C::KS;
-  for (int i = i0; i < KS * 2 * N; i += step) {
-    const int n = i % N, ch16 = (i / N) & 1, srow = i / (2 * N);
+  using C = FirstTmaCfg<K, FP4>;
+  constexpr int N = C::N, NT = C::NT, CIN = C::CIN;
+  for (int i = i0; i < C::NMMA * 2 * N; i += step) {
+    const int n = i % N, kc = (i / N) & 1, mi = i / (2 * N);
     const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
     const bool ok = o < A.c_out;
     const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
-    const int ky = srow - dy;
     const int bias = first_tma_bias<K>(A, o);
-    uint32_t b[16];
+    uint32_t w4[4] = {0u, 0u, 0u, 0u};
+    if (FP4) {
+      const int srow = 2 * mi + kc, ky = srow - dy;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int el = ch16 * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
-      int v = 0;
-      if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
-        const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
-        v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
-        if (f) v = -v;
+      for (int e = 0; e < 32; ++e) {
+        int v = 0;
+        if (e < C::SB) {
+          const int tap = e / CIN, c = e % CIN, kx = tap - dx;
+          if (ok && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+            const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
+            v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
+            if (f) v = -v;
+          }
+        } else {
+          v = fp4_bias_part(bias, srow * (32 - C::SB) + (e - C::SB));
+        }
+        w4[e >> 3] |= e2m1_int(v) << (4 * (e & 7));
       }
-      if (srow == 0 && el == C::SB) v = bias;
-      b[e] = (uint32_t)v & 0xFFu;
+    } else {
+      const int srow = mi, ky = srow - dy;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int el = kc * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
+        int v = 0;
+        if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+          const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
+          v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
+          if (f) v = -v;
+        }
+        if (srow == 0 && el == C::SB) v = bias;
+        w4[e >> 2] |= ((uint32_t)v & 0xFFu) << (8 * (e & 3));
+      }
     }
-    uint4 w4;
-    w4.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-    w4.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
-    w4.z = b[8] | (b[9] << 8) | (b[10] << 16) | (b[11] << 24);
-    w4.w = b[12] | (b[13] << 8) | (b[14] << 16) | (b[15] << 24);
-    *reinterpret_cast<uint4*>(dst + ((size_t)(srow * 2 + ch16) * N + n) * 16) = w4;
+    *reinterpret_cast<uint4*>(dst + ((size_t)(mi * 2 + kc) * N + n) * 16) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
   }
 }
 
-template <int K>
+template <int K, bool FP4>
 __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
-  stage_b_first_tma<K>(A, blockIdx.x, out + (size_t)blockIdx.x * FirstTmaCfg<K>::B_BYTES, threadIdx.x, blockDim.x);
+  stage_b_first_tma<K, FP4>(A, blockIdx.x, out + (size_t)blockIdx.x * FirstTmaCfg<K, FP4>::B_BYTES, threadIdx.x, blockDim.x);
 }
 
 // Warp roles (no block-wide barrier in the tile loop; mbarriers carry every hand-off):
@@ -145,11 +189,11 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
 // acc_empty     epilogue (4)                 -> MMA issuer (single TMEM accumulator set)
 constexpr int kFirstTmaThreads = 320;
 
-template <int K>
-__global__ void __launch_bounds__(kFirstTmaThreads, 3)
+template <int K, bool FP4>
+__global__ void __launch_bounds__(kFirstTmaThreads, FP4 ? 2 : 3)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
-  using C = FirstTmaCfg<K>;
+  using C = FirstTmaCfg<K, FP4>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W;
   constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN, NB = 5;  // builder warps
   extern __shared__ __align__(1024) uint8_t dsm[];
@@ -157,7 +201,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   uint8_t* sA = sRaw + C::NRAW * C::RAW_STRIDE;          // 2 x A_BYTES: [chunk][strip row][px][16 B]
   uint8_t* sB = sA + 2 * C::A_BYTES;                     // [strip row][chunk][n][16 B]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (for the debug acc output)
-  __shared__ uint64_t raw_full[C::NRAW], raw_empty[C::NRAW], a_full[2], mma_done[2], acc_empty, w_bar;
+  __shared__ uint64_t raw_full[C::NRAW], raw_empty[C::NRAW], a_full[2], mma_done[2], acc_empty, w_bar, scale_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -177,6 +221,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     tc::mbar_init(&mma_done[1], 1);
     tc::mbar_init(&acc_empty, 4);
     tc::mbar_init(&w_bar, 1);
+    tc::mbar_init(&scale_bar, 4);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -192,7 +237,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
-    stage_b_first_tma<K>(A, g, sB, tid, kFirstTmaThreads);
+    stage_b_first_tma<K, FP4>(A, g, sB, tid, kFirstTmaThreads);
   }
   griddep_wait();  // the image buffer and the output buffer belong to the predecessors' stream order
   tc::fence_async_smem();
@@ -204,7 +249,8 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   if (warp == 0) {
     // ------------------------------------------------------------ producer + MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_i8(128, N, true);
+      constexpr uint32_t idesc = FP4 ? tc::idesc_mxf4(128, N) : tc::idesc_i8(128, N, true);
+      const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // FP4 block scales (all 1.0)
       auto issue_raw = [&](int64_t tile, int slot) {
         int img, oy0, ox0;
         tile_origin(tile, img, oy0, ox0);
@@ -214,6 +260,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
       if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
       if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
+      if (FP4) tc::mbar_wait(&scale_bar, 0);            // block scales written by the epilogue warps
       int it = 0;
       for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
         const int buf = it & 1;
@@ -225,13 +272,23 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));         // strips of tile it staged
         if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // tile it-1 drained
         tc::fence_after();
-        // MMA s: strip rows s + 2 * (pooled row) of both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
         const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
+        if (FP4) {
+          // MMA p: strip rows 2p, 2p+1 (+ 2 * pooled row): LBO = one strip row, SBO = 2 strip rows
 #pragma unroll
-        for (int s = 0; s < KS; ++s) {
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
-          tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+          for (int p = 0; p < C::NMMA; ++p) {
+            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(2 * p * PW * 16), PW * 16, 2 * PW * 16);
+            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * N * 16), N * 16, 128);
+            tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, p > 0 ? 1u : 0u);
+          }
+        } else {
+          // MMA s: strip row s + 2 * (pooled row), both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
+            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
+            tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+          }
         }
         tc::commit(&mma_done[buf]);
       }
@@ -263,9 +320,10 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
         const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
-        uint32_t T[8];
+        // M[w]: 0xFF where the byte is +1 (x > t_c, R14), 0x00 where -1
+        uint32_t M[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) T[w] = thresh4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
+        for (int w = 0; w < 8; ++w) M[w] = thresh_mask4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
         if (!zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
           int img, oy0, ox0;
           tile_origin(tile, img, oy0, ox0);
@@ -276,28 +334,63 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               const int xb = ox0 * CIN - C::XOFF + WB + 12 * j + 4 * w + b;  // image row byte
-              if (!row_ok || xb < 0 || xb >= A.W * CIN) T[w] |= 0xFFu << (8 * b);
+              if (!row_ok || xb < 0 || xb >= A.W * CIN) M[w] &= ~(0xFFu << (8 * b));
             }
         }
         uint8_t* a = sA + buf * C::A_BYTES;
+        if (FP4) {
+          // bytes -> e2m1 nibbles (+1 = 0x2, -1 = 0xA): bit 3 of each byte's nibble = "is -1"
+          uint32_t NW[4];
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          constexpr int e0 = C::E;
-          const int o = e0 + 6 * s, qw = o >> 2, sh = 8 * (o & 3);
-          uint32_t v[8];
+          for (int q = 0; q < 4; ++q) {
+            uint32_t h[2];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int w = qw + k;
-            const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
-            v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
-            // bytes >= SB of the strip: -1 (bias slots / unused K)
-            const int b0 = 4 * k;
-            if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
-            else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+            for (int u = 0; u < 2; ++u) {
+              const uint32_t x = ~M[2 * q + u] & 0x08080808u;
+              h[u] = prmt(x | (x >> 4), 0u, 0x4420u);  // nibbles of bytes 0-3 in bits 0-15
+            }
+            NW[q] = prmt(h[0], h[1], 0x5410u) | 0x22222222u;
           }
-          const int px = 2 * j + s;
-          *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
-          *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            constexpr int e0 = C::E;
+            const int o = e0 + 6 * s, qw = o >> 3, sh = 4 * (o & 7);
+            uint32_t v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int w = qw + k;
+              const uint32_t lo = w < 4 ? NW[w] : 0xAAAAAAAAu, hi = w + 1 < 4 ? NW[w + 1] : 0xAAAAAAAAu;
+              v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+              const int n0 = 8 * k;  // nibbles >= SB: -1 (bias slots)
+              if (n0 >= C::SB) v[k] = 0xAAAAAAAAu;
+              else if (n0 + 8 > C::SB) v[k] = (v[k] & ~(0xFFFFFFFFu << (4 * (C::SB - n0)))) | (0xAAAAAAAAu << (4 * (C::SB - n0)));
+            }
+            const int px = 2 * j + s;
+            *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+          }
+        } else {
+          uint32_t T[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) T[w] = ~M[w] | 0x01010101u;  // int8 +1 / -1
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            constexpr int e0 = C::E;
+            const int o = e0 + 6 * s, qw = o >> 2, sh = 8 * (o & 3);
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int w = qw + k;
+              const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
+              v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
+              // bytes >= SB of the strip: -1 (bias slots / unused K)
+              const int b0 = 4 * k;
+              if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
+              else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+            }
+            const int px = 2 * j + s;
+            *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
+          }
         }
       }
       tc::fence_async_smem();  // generic-proxy strip writes -> the MMA (async proxy)
@@ -316,6 +409,14 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
     const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    if (FP4) {  // block scales of the A (lanes = rows) and B operands: 1.0
+      tc::tmem_st8_same(lane_base + (uint32_t)N, 0x7F7F7F7Fu);
+      tc::tmem_st8_same(lane_base + (uint32_t)(N + 8), 0x7F7F7F7Fu);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&scale_bar);
+    }
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
       const int buf = it & 1;
@@ -339,7 +440,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
               int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
               for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
                 const int o = g * NT + cb + c;
-                const int a = vv[c] + s_bias[cb + c];
+                const int a = (FP4 ? (int)__int_as_float(vv[c]) : vv[c]) + s_bias[cb + c];
                 dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
               }
             }

@@ -416,7 +416,7 @@ def test_forward_input_threshold_edges(cuda, orc, algo, T):
         cuda.set_option("conv_algo", 0)
 
 
-@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("tma", [2, 1, 0])
 @pytest.mark.parametrize("h,w,k,cout,T,mode", [
     (96, 96, 5, 32, None, 1),
     (34, 48, 5, 32, [-128.0, 3.0, -0.5], 1),   # t = (127, -1, 0): out-of-image bytes patched to -1
@@ -440,7 +440,8 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     Tt = None if mode == 0 else (synth.thresholds(3, seed) if T is None else torch.tensor(T, dtype=torch.float32))
     imgs = synth.images(5, h, w, 3, seed + 2)
     try:
-        cuda.set_option("first_tma", tma)
+        cuda.set_option("first_tma", 1 if tma else 0)
+        cuda.set_option("first_fp4", 1 if tma == 2 else 0)  # 2: e2m1 operands (kind::mxf4), 1: int8
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if Tt is None else dev(Tt), dl, max_batch=8)
         if tma:
             assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
@@ -448,6 +449,7 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
         torch.cuda.synchronize()
     finally:
         cuda.set_option("first_tma", 1)
+        cuda.set_option("first_fp4", 0)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, Tt).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
