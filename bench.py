@@ -305,7 +305,6 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    net.profile(True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -318,14 +317,22 @@ def main():
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
-    stage_ms, stage_launch = net.profile_read()
-    net.profile(False)
     ms = e0.elapsed_time(e1) / a.steps
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * B / (ms * 1e-3)
+    # per-stage live kernel times: the same steps again with the library's CUDA events around every
+    # launch (kept out of the timed region: events between kernels serialise programmatic launches)
+    bnn.set_option("streams", 1)  # one stream here, so a kernel's event time is its own duration
+    net.profile(True)
+    for _ in range(a.steps):
+        step()
+    torch.cuda.synchronize()
+    stage_ms, stage_launch = net.profile_read()
+    net.profile(False)
+    bnn.set_option("streams", 2)
 
     # ---- roofline of the dominant conv kernel (live CUDA-event times of its launches)
     roofline = dominant_roofline(net, spec, mode, stage_ms, stage_launch, B * a.steps, clocks, dev)

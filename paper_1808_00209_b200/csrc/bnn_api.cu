@@ -80,7 +80,8 @@ int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;
-int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
+int g_opt_alg1 = 0;
+int g_opt_streams = 2;  // bnn_forward over several chunks alternates chunks over 1 or 2 streams  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
 // stream predecessor is still running; it runs its prologue (barriers, TMEM, weight images) and then
@@ -709,6 +710,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
+  if (strcmp(key, "streams") == 0) { g_opt_streams = value; return BNN_OK; }
   if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
@@ -836,6 +838,13 @@ struct bnn_net {
   int32_t* st_logits = nullptr;
   int32_t* st_cls = nullptr;
   cudaStream_t cap_stream = nullptr;
+  // second chunk stream of bnn_forward (chunks alternate streams so one chunk's low-occupancy dense
+  // layers and kernel tails overlap the next chunk's convolutions); its own workspace, lazily created
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  uint32_t* packed_in2 = nullptr;
+  uint32_t* buf2[2] = {nullptr, nullptr};
+  int32_t* logits_tmp2 = nullptr;
   std::vector<cudaGraphExec_t> graphs;  // index n
 };
 
@@ -870,6 +879,13 @@ void net_free(bnn_net* net) {
   cudaFree(net->st_cls);
   if (net->cap_stream) cudaStreamDestroy(net->cap_stream);
   if (net->h2d) cudaStreamDestroy(net->h2d);
+  if (net->s2) cudaStreamDestroy(net->s2);
+  if (net->ev_fork) cudaEventDestroy(net->ev_fork);
+  if (net->ev_join) cudaEventDestroy(net->ev_join);
+  cudaFree(net->packed_in2);
+  cudaFree(net->buf2[0]);
+  cudaFree(net->buf2[1]);
+  cudaFree(net->logits_tmp2);
   if (net->d2h) cudaStreamDestroy(net->d2h);
   delete net;
 }
@@ -1165,6 +1181,37 @@ namespace {
 
 // ---- the paper's design as a comparison pipeline (k_alg1.cuh): supported for u8 SIGN / THRESH_RGB
 // nets whose conv layers have k <= 5 (B = k*k <= 32 bits per channel word) and no thresholds/flips
+bnn_status second_stream_prepare(bnn_net* net) {
+  if (net->s2 != nullptr) return BNN_OK;
+  cudaError_t e = cudaStreamCreateWithFlags(&net->s2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&net->ev_join, cudaEventDisableTiming);
+  const size_t mb = (size_t)net->chunk;
+  if (e == cudaSuccess && net->packed_in_words) e = cudaMalloc(&net->packed_in2, (size_t)(net->packed_in_words * mb * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->buf2[0], (size_t)(net->buf_words * mb * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->buf2[1], (size_t)(net->buf_words * mb * 4));
+  if (e == cudaSuccess) e = cudaMalloc(&net->logits_tmp2, (size_t)net->L.back().l * mb * 4);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail(BNN_E_CUDA, "bnn_forward: second stream workspace: %s", cudaGetErrorString(e));
+  }
+  return BNN_OK;
+}
+
+// forward_chunk on the second workspace (the kernels read the workspace pointers from the net)
+bnn_status forward_chunk_ws2(bnn_net* net, const void* x, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
+  std::swap(net->packed_in, net->packed_in2);
+  std::swap(net->buf[0], net->buf2[0]);
+  std::swap(net->buf[1], net->buf2[1]);
+  std::swap(net->logits_tmp, net->logits_tmp2);
+  bnn_status st = forward_chunk(net, x, nb, logits, cls, s);
+  std::swap(net->packed_in, net->packed_in2);
+  std::swap(net->buf[0], net->buf2[0]);
+  std::swap(net->buf[1], net->buf2[1]);
+  std::swap(net->logits_tmp, net->logits_tmp2);
+  return st;
+}
+
 bool alg1_supported(const bnn_net* net) {
   if (net->in_dt != BNN_U8 || (net->mode != BNN_SIGN && net->mode != BNN_THRESH_RGB) || net->w > 512) return false;
   for (size_t i = 0; i < net->L.size(); ++i) {
@@ -1300,12 +1347,28 @@ bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits,
     }
     return BNN_OK;
   }
-  for (int s0 = 0; s0 < n; s0 += net->chunk) {
-    const int nb = std::min(net->chunk, n - s0);
-    const void* x = (const uint8_t*)images + (int64_t)s0 * net->img_bytes;
-    bnn_status st = forward_chunk(net, x, nb, logits ? logits + (int64_t)s0 * L : nullptr, cls ? cls + s0 : nullptr,
-                                  (cudaStream_t)stream);
+  const int chunks = (n + net->chunk - 1) / net->chunk;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int last_nb = n - (chunks - 1) * net->chunk;
+  const bool fused_any = g_opt_fused_max_n > 0 && (net->chunk <= g_opt_fused_max_n || last_nb <= g_opt_fused_max_n);
+  const bool two = chunks >= 2 && g_opt_streams >= 2 && !fused_any;  // (cooperative chunks stay on one stream)
+  if (two) {
+    bnn_status st = second_stream_prepare(net);
     if (st != BNN_OK) return st;
+    cudaEventRecord(net->ev_fork, s);
+    cudaStreamWaitEvent(net->s2, net->ev_fork, 0);
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const int s0 = c * net->chunk, nb = std::min(net->chunk, n - s0);
+    const void* x = (const uint8_t*)images + (int64_t)s0 * net->img_bytes;
+    int32_t* lg = logits ? logits + (int64_t)s0 * L : nullptr;
+    int32_t* cl = cls ? cls + s0 : nullptr;
+    const bnn_status st = (two && (c & 1)) ? forward_chunk_ws2(net, x, nb, lg, cl, net->s2) : forward_chunk(net, x, nb, lg, cl, s);
+    if (st != BNN_OK) return st;
+  }
+  if (two) {
+    cudaEventRecord(net->ev_join, net->s2);
+    cudaStreamWaitEvent(s, net->ev_join, 0);
   }
   return BNN_OK;
 }

@@ -488,17 +488,19 @@ def test_forward_alg1_pipeline(cuda, orc, spec_name, mode, n):
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
 
-@pytest.mark.parametrize("fused", [8, 0])
-def test_forward_thresholds_and_chunking(cuda, orc, fused):
+@pytest.mark.parametrize("fused,streams", [(8, 2), (0, 2), (0, 1)])
+def test_forward_thresholds_and_chunking(cuda, orc, fused, streams):
     """BN-folded integer thresholds + flips, and n > max_batch (chunked, ragged last chunk)."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 777, max_batch=2, thr=True)
     imgs = synth.images(5, 96, 96, 3, 778)
     try:
         cuda.set_option("fused_max_n", fused)
+        cuda.set_option("streams", streams)  # chunks alternate over two streams / workspaces
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
         cuda.set_option("fused_max_n", 0)
+        cuda.set_option("streams", 2)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
