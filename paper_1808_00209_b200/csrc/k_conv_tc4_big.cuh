@@ -156,23 +156,40 @@ conv_tc4_big_kernel(const ConvArgs A) {
           *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
         }
       }
-      // B: chunk u = (jl, t) -> MMA u / 2, K-chunk u % 2; pad channels, words >= cw, dummy -> 0
-      for (int i = tid; i < C::NMMA * 2 * NT; i += 256) {
+      // B: chunk u = (jl, t) -> MMA u / 2, K-chunk u % 2; pad channels, words >= cw, dummy -> 0.
+      // All of this thread's weight words are loaded first (independent loads in flight), then expanded.
+      constexpr int PB = (C::NMMA * 2 * NT + 255) / 256;
+      uint32_t wv[PB];
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const int i = tid + q * 256;
         const int n = i % NT, u = i / NT;
         const int o = g * NT + n;
-        uint32_t o4[4] = {0u, 0u, 0u, 0u};
-        if (u < U && o < A.c_out) {
+        wv[q] = 0u;
+        if (i < C::NMMA * 2 * NT && u < U && o < A.c_out) {
           const int jl = u / KK, t = u - jl * KK, j = j0 + jl;
-          if (j < A.cw) {
-            expand_word_fp4(__ldg(A.wt + ((int64_t)o * KK + t) * A.cw + j), s_lut, o4);
+          if (j < A.cw) wv[q] = __ldg(A.wt + ((int64_t)o * KK + t) * A.cw + j);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        const int i = tid + q * 256;
+        if (i >= C::NMMA * 2 * NT) break;
+        const int n = i % NT, u = i / NT;
+        uint32_t o4[4] = {0u, 0u, 0u, 0u};
+        if (wv[q] != 0u || u < U) {
+          const int jl = u / KK, j = j0 + jl;
+          const int o = g * NT + n;
+          if (u < U && o < A.c_out && j < A.cw) {
+            expand_word_fp4(wv[q], s_lut, o4);
             const int valid = min(32, A.c_in - 32 * j);
             if (valid < 32) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
+              for (int qq = 0; qq < 4; ++qq) {
                 uint32_t mk = 0;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) mk |= (8 * q + e < valid ? 0xFu : 0u) << (4 * e);
-                o4[q] &= mk;
+                for (int e = 0; e < 8; ++e) mk |= (8 * qq + e < valid ? 0xFu : 0u) << (4 * e);
+                o4[qq] &= mk;
               }
             }
           }
