@@ -81,6 +81,7 @@ int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;
 int g_opt_alg1 = 0;
+int g_opt_csa = 1;  // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
 int g_opt_streams = 2;  // bnn_forward over several chunks alternates chunks over 1 or 2 streams  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
@@ -156,7 +157,8 @@ bnn_status launch_conv_bin_t(ConvArgs A, cudaStream_t s) {
   const int64_t gx = (A.total_tiles + A.tiles_per_cta - 1) / A.tiles_per_cta;
   if (gx > 0x7fffffff) return fail(BNN_E_UNSUPPORTED, "bnn_conv2d: too many tiles");
   dim3 grid((unsigned)gx, (unsigned)((A.c_out + 31) / 32));
-  conv_bin_kernel<K, PR, PC, WY, WX, CWC><<<grid, WY * WX * 32, 0, s>>>(A);
+  if (g_opt_csa) conv_bin_kernel<K, PR, PC, WY, WX, CWC, true><<<grid, WY * WX * 32, 0, s>>>(A);
+  else conv_bin_kernel<K, PR, PC, WY, WX, CWC, false><<<grid, WY * WX * 32, 0, s>>>(A);
   return check_launch("conv_bin_kernel");
 }
 
@@ -710,6 +712,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
+  if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
   if (strcmp(key, "streams") == 0) { g_opt_streams = value; return BNN_OK; }
   if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }

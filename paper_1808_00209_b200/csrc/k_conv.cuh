@@ -95,7 +95,39 @@ BNN_DEV void conv_epilogue(const ConvArgs& A, int img, int oy0, int ox0, int g, 
 // (blockIdx.y) x a TH x TW output tile, TH = WY*PR, TW = WX*PC; the input words are
 // walked in chunks of CWC words per pixel.  When the whole weight slab fits one chunk it is
 // staged once and the CTA loops over tiles_per_cta consecutive tiles.
-template <int K, int PR, int PC, int WY, int WX, int CWC>
+// Carry-save (Harley-Seal style) popcount of K words: full adders built from LOP3
+// (sum = a ^ b ^ c, carry = maj(a, b, c)) compress the K XOR words of one kernel row before the
+// POPC pipe (16 lanes/clk/SM) sees them; LOP3 issues at 64/clk/SM.  K = 5: 3 POPC + 6 LOP3 instead
+// of 5 POPC; K = 3: 2 + 2 instead of 3; K = 7: 3 + 8 instead of 7.  The count is exactly sum popc(x).
+BNN_DEV void full_add(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
+  s = a ^ b ^ c;
+  cy = (a & b) | (c & (a ^ b));
+}
+template <int K>
+BNN_DEV int csa_popc(const uint32_t (&x)[K]) {
+  if constexpr (K == 1) {
+    return popc(x[0]);
+  } else if constexpr (K == 3) {
+    uint32_t s, c;
+    full_add(x[0], x[1], x[2], s, c);
+    return popc(s) + 2 * popc(c);
+  } else if constexpr (K == 5) {
+    uint32_t s1, c1, s2, c2;
+    full_add(x[0], x[1], x[2], s1, c1);
+    full_add(s1, x[3], x[4], s2, c2);
+    return popc(s2) + 2 * popc(c1 ^ c2) + 4 * popc(c1 & c2);
+  } else {
+    static_assert(K == 7, "csa_popc: K in {1, 3, 5, 7}");
+    uint32_t s1, c1, s2, c2, s3, c3, cs, cc;
+    full_add(x[0], x[1], x[2], s1, c1);
+    full_add(s1, x[3], x[4], s2, c2);
+    full_add(s2, x[5], x[6], s3, c3);
+    full_add(c1, c2, c3, cs, cc);
+    return popc(s3) + 2 * popc(cs) + 4 * popc(cc);
+  }
+}
+
+template <int K, int PR, int PC, int WY, int WX, int CWC, bool CSA = false>
 __global__ void __launch_bounds__(WY * WX * 32)
 conv_bin_kernel(const ConvArgs A) {
   constexpr int R = (K - 1) / 2;
@@ -179,10 +211,20 @@ conv_bin_kernel(const ConvArgs A) {
               const uint4 q = src[v];
               rw[4 * v] = q.x; rw[4 * v + 1] = q.y; rw[4 * v + 2] = q.z; rw[4 * v + 3] = q.w;
             }
+            if constexpr (CSA) {
 #pragma unroll
-            for (int kx = 0; kx < K; ++kx)
+              for (int p = 0; p < PC; ++p) {
+                uint32_t xk[K];
 #pragma unroll
-              for (int p = 0; p < PC; ++p) acc[r][p] += popc(rw[p + kx] ^ wr[kx]);
+                for (int kx = 0; kx < K; ++kx) xk[kx] = rw[p + kx] ^ wr[kx];
+                acc[r][p] += csa_popc<K>(xk);
+              }
+            } else {
+#pragma unroll
+              for (int kx = 0; kx < K; ++kx)
+#pragma unroll
+                for (int p = 0; p < PC; ++p) acc[r][p] += popc(rw[p + kx] ^ wr[kx]);
+            }
           }
         }
       }

@@ -178,6 +178,21 @@ def test_conv_pool_tensor_core(cuda, orc, pool_tc, n, h, w, cout, k, thr):
         cuda.set_option("conv_pool_tc", 1)
 
 
+@pytest.mark.parametrize("csa", [1, 0])
+@pytest.mark.parametrize("n,h,w,cin,cout,k,pool", [
+    (2, 48, 48, 32, 32, 5, 2), (1, 13, 11, 64, 40, 3, 1), (1, 14, 10, 32, 33, 7, 2), (1, 9, 7, 300, 70, 1, 1)])
+def test_conv_popc_csa(cuda, orc, csa, n, h, w, cin, cout, k, pool):
+    """The XOR-popcount engine (Eq. 4) with and without the carry-save compression of each kernel
+    row's K words equals the oracle bit for bit."""
+    try:
+        cuda.set_option("conv_tc", 0)
+        cuda.set_option("csa", csa)
+        conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=True, flip=True, seed=2500 + h + k + cin)
+    finally:
+        cuda.set_option("conv_tc", 1)
+        cuda.set_option("csa", 1)
+
+
 @pytest.mark.parametrize("cin,k", [(3, 5), (32, 3)])
 def test_conv_threshold_flip(cuda, orc, cin, k):
     conv_case(cuda, orc, 2, 16, 16, cin, 40, k, 2, thr=True, flip=True, seed=7)
