@@ -314,8 +314,8 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
-      tc::mbar_wait(&raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
-      if (it >= 2) tc::mbar_wait(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      tc::mbar_wait_sleep(&raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
+      if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
       if (bt < C::GROUPS) {
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
@@ -422,7 +422,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
-      tc::mbar_wait(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)((it >> 1) & 1));
       __syncwarp();
       tc::fence_after();
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;

@@ -230,7 +230,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
       const int buf = it & 1;
-      if (it >= 2) tc::mbar_wait(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
       uint8_t* a = sA + buf * C::A_BYTES;
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
@@ -262,7 +262,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
-      tc::mbar_wait(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)((it >> 1) & 1));
       __syncwarp();
       tc::fence_after();
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;

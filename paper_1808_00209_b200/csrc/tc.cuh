@@ -66,6 +66,16 @@ BNN_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase));
 }
 
+// The same wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase
+// completes (or ~1 ms passes) instead of re-issuing try_wait -- for warps that idle a whole MMA.
+BNN_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tBNN_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra BNN_DONES_%=;\n\tbra BNN_WAITS_%=;\n\tBNN_DONES_%=:\n\t}\n" ::"r"(smem_addr(bar)),
+      "r"(phase), "r"(1000000u));
+}
+
 // 1-D bulk copy global -> this CTA's shared memory (16-byte aligned, size % 16 == 0), completing
 // `bytes` transactions on `bar` (arm it with expect_tx first)
 BNN_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
