@@ -100,6 +100,8 @@ BNN_API int bnn_version(void);
  *   "first_fp4"     0 (default): that kernel's operands are int8 (kind::i8); 1: e2m1 (kind::mxf4).
  *   "csa"           1 (default): the XOR-popcount conv compresses each kernel row's K XOR words
  *                   with carry-save adders (LOP3) before POPC; 0: one POPC per word (Eq. 4 as printed).
+ *   "big_img"       1 (default): the streamed wide-channel conv expands its weights once per call
+ *                   (stream-ordered scratch) and bulk-copies a stage per step; 0: expands per tile.
  *   "streams"       2 (default): bnn_forward alternates chunks over the caller's stream and an
  *                   internal second stream (own workspace; joined back before returning); 1: one.
  *   "dense_tc"      1 (default): dense layers over n >= 256 images run on tensor cores.

@@ -81,7 +81,8 @@ int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;
 int g_opt_alg1 = 0;
-int g_opt_csa = 1;  // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
+int g_opt_csa = 1;      // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
+int g_opt_big_img = 1;  // 1: the streamed wide-channel conv stages a per-call pre-expanded weight image
 int g_opt_streams = 2;  // bnn_forward over several chunks alternates chunks over 1 or 2 streams  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
@@ -432,8 +433,23 @@ bnn_status launch_conv_tc4_big_t(ConvArgs A, cudaStream_t s) {
   const int64_t per_group = std::max<int64_t>(1, num_sms() / groups);
   const int64_t gx = std::min<int64_t>(A.total_tiles, per_group);
   dim3 grid((unsigned)gx, (unsigned)groups);
+  // the weight operand, expanded once for this call (stream-ordered scratch), then one bulk copy per
+  // stage in the kernel instead of an expansion per stage and tile
+  uint8_t* img = nullptr;
+  const int nstage = (A.cw + CG - 1) / CG;
+  if (g_opt_big_img && A.bimg == nullptr && A.total_tiles > (int64_t)gx) {
+    if (cudaMallocAsync(&img, (size_t)groups * nstage * C::B_BYTES, s) == cudaSuccess) {
+      prep_tc4_big_kernel<K, CG, NT><<<dim3((unsigned)nstage, (unsigned)groups), 256, 0, s>>>(A, img);
+      A.bimg = img;
+    } else {
+      (void)cudaGetLastError();
+      img = nullptr;
+    }
+  }
   kfn<<<grid, 256, C::SMEM, s>>>(A);
-  return check_launch("conv_tc4_big_kernel");
+  bnn_status st = check_launch("conv_tc4_big_kernel");
+  if (img != nullptr) cudaFreeAsync(img, s);
+  return st;
 }
 
 template <int K, int CW, int NT>
@@ -713,6 +729,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
+  if (strcmp(key, "big_img") == 0) { g_opt_big_img = value; return BNN_OK; }
   if (strcmp(key, "streams") == 0) { g_opt_streams = value; return BNN_OK; }
   if (strcmp(key, "pdl") == 0) { g_opt_pdl = value; return BNN_OK; }
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }

@@ -27,6 +27,71 @@ struct ConvTc4BigCfg {
   static constexpr int PF = (CG * NPIX + 255) / 256;
 };
 
+// One stage's weight operand ([mma][K chunk][NT][16 B]) for channel group g, stage st: chunk
+// u = (jl, t) -> MMA u / 2, K-chunk u % 2; pad channels, words >= cw, the dummy chunk -> 0.  All of a
+// thread's weight words are loaded first (independent loads in flight), then expanded.
+template <int K, int CG, int NT>
+BNN_DEV void stage_b_tc4_big(const ConvArgs& A, int g, int st, uint8_t* b, const uint32_t* lut, int tid, int nthr) {
+  using C = ConvTc4BigCfg<K, CG, NT>;
+  constexpr int KK = C::KK, U = C::U;
+  constexpr int PB = (C::NMMA * 2 * NT + 255) / 256;
+  const int j0 = st * CG;
+  for (int base = 0; base < C::NMMA * 2 * NT; base += PB * nthr) {
+    uint32_t wv[PB];
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      const int i = base + tid + q * nthr;
+      const int n = i % NT, u = i / NT;
+      const int o = g * NT + n;
+      wv[q] = 0u;
+      if (i < C::NMMA * 2 * NT && u < U && o < A.c_out) {
+        const int jl = u / KK, t = u - jl * KK, j = j0 + jl;
+        if (j < A.cw) wv[q] = __ldg(A.wt + ((int64_t)o * KK + t) * A.cw + j);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < PB; ++q) {
+      const int i = base + tid + q * nthr;
+      if (i >= C::NMMA * 2 * NT) break;
+      const int n = i % NT, u = i / NT;
+      uint32_t o4[4] = {0u, 0u, 0u, 0u};
+      const int jl = u / KK, j = j0 + jl;
+      const int o = g * NT + n;
+      if (u < U && o < A.c_out && j < A.cw) {
+        expand_word_fp4(wv[q], lut, o4);
+        const int valid = min(32, A.c_in - 32 * j);
+        if (valid < 32) {
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint32_t mk = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mk |= (8 * qq + e < valid ? 0xFu : 0u) << (4 * e);
+            o4[qq] &= mk;
+          }
+        }
+      }
+      *reinterpret_cast<uint4*>(b + ((size_t)(u >> 1) * 2 + (u & 1)) * NT * 16 + n * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+  }
+}
+
+// The whole layer's weight operand, stage by stage ([group][stage] x B_BYTES), built once per call
+// so the conv kernel stages it with one bulk copy per stage instead of re-expanding it per tile.
+template <int K, int CG, int NT>
+__global__ void __launch_bounds__(256) prep_tc4_big_kernel(const ConvArgs A, uint8_t* out) {
+  __shared__ uint32_t lut[256];
+  {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= (((threadIdx.x >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+    lut[threadIdx.x] = v;
+  }
+  __syncthreads();
+  const int st = blockIdx.x, g = blockIdx.y, nstage = gridDim.x;
+  stage_b_tc4_big<K, CG, NT>(A, g, st, out + ((size_t)g * nstage + st) * ConvTc4BigCfg<K, CG, NT>::B_BYTES, lut,
+                             threadIdx.x, 256);
+}
+
 template <int K, int CG, int NT>
 __global__ void __launch_bounds__(256, 1)
 conv_tc4_big_kernel(const ConvArgs A) {
@@ -35,7 +100,7 @@ conv_tc4_big_kernel(const ConvArgs A) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   float* s_thr = reinterpret_cast<float*>(dsm + 2 * C::STAGE_BYTES);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);
-  __shared__ uint64_t bar_stage[2], bar_acc[2];
+  __shared__ uint64_t bar_stage[2], bar_acc[2], w_bar[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ uint32_t s_flip[NT / 32];
 
@@ -64,6 +129,8 @@ conv_tc4_big_kernel(const ConvArgs A) {
     tc::mbar_init(&bar_stage[1], 1);
     tc::mbar_init(&bar_acc[0], 1);
     tc::mbar_init(&bar_acc[1], 1);
+    tc::mbar_init(&w_bar[0], 1);
+    tc::mbar_init(&w_bar[1], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -141,6 +208,8 @@ conv_tc4_big_kernel(const ConvArgs A) {
       uint8_t* a = dsm + s * C::STAGE_BYTES;
       uint8_t* b = a + C::A_BYTES;
       const int j0 = st * CG;
+      if (A.bimg != nullptr && tid == 0)
+        tc::stage_image(b, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES, &w_bar[s]);
       // A: halo words j0 .. j0+CG-1 -> planes [jl][p] (16 B = 32 channels as e2m1)
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
@@ -156,51 +225,17 @@ conv_tc4_big_kernel(const ConvArgs A) {
           *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
         }
       }
-      // B: chunk u = (jl, t) -> MMA u / 2, K-chunk u % 2; pad channels, words >= cw, dummy -> 0.
-      // All of this thread's weight words are loaded first (independent loads in flight), then expanded.
-      constexpr int PB = (C::NMMA * 2 * NT + 255) / 256;
-      uint32_t wv[PB];
-#pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        const int i = tid + q * 256;
-        const int n = i % NT, u = i / NT;
-        const int o = g * NT + n;
-        wv[q] = 0u;
-        if (i < C::NMMA * 2 * NT && u < U && o < A.c_out) {
-          const int jl = u / KK, t = u - jl * KK, j = j0 + jl;
-          if (j < A.cw) wv[q] = __ldg(A.wt + ((int64_t)o * KK + t) * A.cw + j);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        const int i = tid + q * 256;
-        if (i >= C::NMMA * 2 * NT) break;
-        const int n = i % NT, u = i / NT;
-        uint32_t o4[4] = {0u, 0u, 0u, 0u};
-        if (wv[q] != 0u || u < U) {
-          const int jl = u / KK, j = j0 + jl;
-          const int o = g * NT + n;
-          if (u < U && o < A.c_out && j < A.cw) {
-            expand_word_fp4(wv[q], s_lut, o4);
-            const int valid = min(32, A.c_in - 32 * j);
-            if (valid < 32) {
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
-                uint32_t mk = 0;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) mk |= (8 * qq + e < valid ? 0xFu : 0u) << (4 * e);
-                o4[qq] &= mk;
-              }
-            }
-          }
-        }
-        *reinterpret_cast<uint4*>(b + ((size_t)(u >> 1) * 2 + (u & 1)) * NT * 16 + n * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+      if (A.bimg != nullptr) {
+        // B: this stage's pre-expanded weight image, one bulk copy (issued before the A expansion)
+      } else {
+        stage_b_tc4_big<K, CG, NT>(A, g, st, b, s_lut, tid, 256);
       }
       tc::fence_async_smem();
       tc::fence_before();
       __syncthreads();
       tc::fence_after();
       if (tid == 128) {
+        if (A.bimg != nullptr) tc::mbar_wait(&w_bar[s], (stage_uses >> 1) & 1);  // weight stage landed
         const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(b);
         const uint32_t d_tmem = tmem + (uint32_t)(buf * NT);
 #pragma unroll

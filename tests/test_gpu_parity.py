@@ -149,14 +149,17 @@ def test_conv_first_layer_pooled_tc(cuda, orc, pool_tc, n, h, w, cin, cout, k, t
     (1, 10, 10, 64, 40, 7, 1),    # big k = 7
     (3, 8, 8, 512, 512, 3, 2),    # CIFAR conv6 shape
 ])
-@pytest.mark.parametrize("fp4", [1, 0])
+@pytest.mark.parametrize("fp4", [2, 1, 0])
 def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool, fp4):
-    """fp4 = 1: kind::mxf4 (packed e2m1, two taps per MMA); fp4 = 0: kind::i8."""
+    """fp4 = 1: kind::mxf4 (packed e2m1, two taps per MMA; the streamed wide kernel stages a per-call
+    weight image); fp4 = 2: the same with the weights expanded in-kernel; fp4 = 0: kind::i8."""
     try:
-        cuda.set_option("conv_tc_fp4", fp4)
+        cuda.set_option("conv_tc_fp4", 1 if fp4 else 0)
+        cuda.set_option("big_img", 0 if fp4 == 2 else 1)
         conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=True, flip=True, seed=900 + h + k)
     finally:
         cuda.set_option("conv_tc_fp4", 1)
+        cuda.set_option("big_img", 1)
 
 
 @pytest.mark.parametrize("n,h,w,cout,k,thr", [
