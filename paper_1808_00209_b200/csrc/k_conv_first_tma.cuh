@@ -206,7 +206,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
-  const int64_t stride = gridDim.x;
+  const int stride = gridDim.x, ntiles = (int)A.total_tiles;  // < 2^31 (host check)
 
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
@@ -226,7 +226,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   }
   __syncthreads();
 
-  auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
+  auto tile_origin = [&](int tile, int& img, int& oy0, int& ox0) {
     int ty, tx;
     tile_coords(A, tile, img, ty, tx);
     oy0 = ty * TH;
@@ -251,20 +251,20 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     if (lane == 0) {
       constexpr uint32_t idesc = FP4 ? tc::idesc_mxf4(128, N) : tc::idesc_i8(128, N, true);
       const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // FP4 block scales (all 1.0)
-      auto issue_raw = [&](int64_t tile, int slot) {
+      auto issue_raw = [&](int tile, int slot) {
         int img, oy0, ox0;
         tile_origin(tile, img, oy0, ox0);
         mbar_expect_tx(&raw_full[slot], C::RAW_BYTES);
         tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_full[slot]);
       };
-      if (blockIdx.x < A.total_tiles) issue_raw(blockIdx.x, 0);
-      if (blockIdx.x + stride < A.total_tiles) issue_raw(blockIdx.x + stride, 1);
+      if ((int)blockIdx.x < ntiles) issue_raw(blockIdx.x, 0);
+      if ((int)blockIdx.x + stride < ntiles) issue_raw(blockIdx.x + stride, 1);
       if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       if (FP4) tc::mbar_wait(&scale_bar, 0);            // block scales written by the epilogue warps
       int it = 0;
-      for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
         const int buf = it & 1;
-        if (tile + 2 * stride < A.total_tiles) {
+        if (tile + 2 * stride < ntiles) {
           const int slot2 = (it + 2) % C::NRAW;  // last used by tile it-1
           if (it >= 1) tc::mbar_wait(&raw_empty[slot2], (uint32_t)(((it - 1) / C::NRAW) & 1));
           issue_raw(tile + 2 * stride, slot2);
@@ -312,7 +312,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     const int bt = tid - 32;  // item: strip row r = bt / 4, pooled columns 2j, 2j+1 with j = bt % 4
     const int r = bt >> 2, j = bt & 3;
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
       tc::mbar_wait_sleep(&raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
       if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
@@ -418,7 +418,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       if (lane == 0) tc::mbar_arrive(&scale_bar);
     }
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);

@@ -120,7 +120,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
-  const int64_t stride = gridDim.x;
+  const int stride = gridDim.x, ntiles = (int)A.total_tiles;  // < 2^31 (host check)
   const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
   if (tid < 256) fill_lut_fp4(s_lut, tid);
   if (tid < NT) {
@@ -174,7 +174,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   __syncthreads();
   tc::fence_after();
 
-  auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
+  auto tile_origin = [&](int tile, int& img, int& oy0, int& ox0) {
     int ty, tx;
     tile_coords(A, tile, img, ty, tx);
     oy0 = ty * TH;
@@ -187,7 +187,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
       if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       int it = 0;
-      for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+      for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
         const int buf = it & 1;
         tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
         if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // drained and re-armed
@@ -226,9 +226,9 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       pref[q] = w;                                                                                   \
     }                                                                                                \
   } while (0)
-    if (blockIdx.x < A.total_tiles) BNN_TC4P_LOAD(blockIdx.x);
+    if ((int)blockIdx.x < ntiles) BNN_TC4P_LOAD(blockIdx.x);
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1;
       if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
       uint8_t* a = sA + buf * C::A_BYTES;
@@ -245,7 +245,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&a_full[buf]);
-      if (tile + stride < A.total_tiles) BNN_TC4P_LOAD(tile + stride);
+      if (tile + stride < ntiles) BNN_TC4P_LOAD(tile + stride);
     }
 #undef BNN_TC4P_LOAD
   } else {
@@ -258,7 +258,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += stride, ++it) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
