@@ -98,6 +98,7 @@ BNN_API int bnn_version(void);
  *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
  *   "first_fp4"     0 (default): that kernel's operands are int8 (kind::i8); 1: e2m1 (kind::mxf4).
+ *   "first_db"      0 (default); 1: that (int8) kernel double-buffers its TMEM accumulators.
  *   "csa"           1 (default): the XOR-popcount conv compresses each kernel row's K XOR words
  *                   with carry-save adders (LOP3) before POPC; 0: one POPC per word (Eq. 4 as printed).
  *   "big_img"       1 (default): the streamed wide-channel conv expands its weights once per call

@@ -75,6 +75,7 @@ int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-orde
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
+int g_opt_first_db = 0;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
@@ -321,10 +322,10 @@ bool use_first_tma(const ConvArgs& A, int k, const uint8_t* xu8) {
          aligned16(xu8) && tma_encoder() != nullptr;
 }
 
-template <int K, bool FP4>
+template <int K, bool FP4, bool DB = false>
 bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  using C = FirstTmaCfg<K, FP4>;
-  auto kfn = conv_first_tma_pool_kernel<K, FP4>;
+  using C = FirstTmaCfg<K, FP4, DB>;
+  auto kfn = conv_first_tma_pool_kernel<K, FP4, DB>;
   constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
   static int occ = -1;
   if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
@@ -357,6 +358,7 @@ bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, 
   if constexpr (SRC == kSrcThresh) {
     if (A.n > 0 && use_first_tma(A, k, xu8)) {
       if (g_opt_first_fp4) return k == 5 ? launch_conv_first_tma_t<5, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, true>(A, xu8, T, s);
+      if (g_opt_first_db) return k == 5 ? launch_conv_first_tma_t<5, false, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, false, true>(A, xu8, T, s);
       return k == 5 ? launch_conv_first_tma_t<5, false>(A, xu8, T, s) : launch_conv_first_tma_t<3, false>(A, xu8, T, s);
     }
   }
@@ -726,6 +728,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
+  if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }

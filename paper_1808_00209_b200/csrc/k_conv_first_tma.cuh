@@ -28,7 +28,7 @@
 
 namespace bnn {
 
-template <int K, bool FP4 = false>
+template <int K, bool FP4 = false, bool DB = false>
 struct FirstTmaCfg {
   static constexpr int CIN = 3, NT = 32, R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW;
   static constexpr int IR = TH + K - 1, IC = TW + K - 1;
@@ -51,7 +51,10 @@ struct FirstTmaCfg {
   static constexpr uint32_t A_BYTES = FP4 ? PLANE : 2 * PLANE;
   static constexpr int NMMA = FP4 ? KS / 2 : KS;
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
-  static constexpr uint32_t TMEM_COLS = FP4 ? 256 : 128;  // FP4: + block-scale columns
+  // FP4: + block-scale columns; DB (int8 only): two accumulator sets, so tile it+1's MMAs run while
+  // tile it is drained
+  static constexpr uint32_t TMEM_COLS = (FP4 || DB) ? 256 : 128;
+  static_assert(!(FP4 && DB), "e2m1 + double buffering needs > 256 TMEM columns");
   static constexpr int GROUPS = IR * (PW / 2);  // 2-strip work items
   static_assert(!FP4 || (KS % 2 == 0 && KS * (32 - SB) >= K * K * CIN / 6 + 3), "fp4 bias slots");
   static_assert(SB <= 31 && DELTA >= 0 && DELTA - E + 12 * (PW / 2 - 1) + 32 <= RAW_W && (TW * CIN) % 16 == 0 &&
@@ -186,14 +189,14 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
 //   warps 6-9          : epilogue (TMEM lane quarter warp % 4, all 32 channels of a pooled pixel)
 // raw_full[s]   TMA complete_tx              -> builders          raw_empty[s] builders (5) -> producer
 // a_full[b]     builders (5)                 -> MMA issuer        mma_done[b]  MMA commit   -> epilogue, builders (A[b] reuse)
-// acc_empty     epilogue (4)                 -> MMA issuer (single TMEM accumulator set)
+// acc_empty[b]  epilogue (4)                 -> MMA issuer (one or two TMEM accumulator sets)
 constexpr int kFirstTmaThreads = 320;
 
-template <int K, bool FP4>
-__global__ void __launch_bounds__(kFirstTmaThreads, FP4 ? 2 : 3)
+template <int K, bool FP4, bool DB = false>
+__global__ void __launch_bounds__(kFirstTmaThreads, (FP4 || DB) ? 2 : 3)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
-  using C = FirstTmaCfg<K, FP4>;
+  using C = FirstTmaCfg<K, FP4, DB>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W;
   constexpr int KS = C::KS, N = C::N, NT = C::NT, CIN = C::CIN, NB = 5;  // builder warps
   extern __shared__ __align__(1024) uint8_t dsm[];
@@ -201,7 +204,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   uint8_t* sA = sRaw + C::NRAW * C::RAW_STRIDE;          // 2 x A_BYTES: [chunk][strip row][px][16 B]
   uint8_t* sB = sA + 2 * C::A_BYTES;                     // [strip row][chunk][n][16 B]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (for the debug acc output)
-  __shared__ uint64_t raw_full[C::NRAW], raw_empty[C::NRAW], a_full[2], mma_done[2], acc_empty, w_bar, scale_bar;
+  __shared__ uint64_t raw_full[C::NRAW], raw_empty[C::NRAW], a_full[2], mma_done[2], acc_empty[2], w_bar, scale_bar;
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -219,7 +222,8 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     tc::mbar_init(&a_full[1], NB);
     tc::mbar_init(&mma_done[0], 1);
     tc::mbar_init(&mma_done[1], 1);
-    tc::mbar_init(&acc_empty, 4);
+    tc::mbar_init(&acc_empty[0], 4);
+    tc::mbar_init(&acc_empty[1], 4);
     tc::mbar_init(&w_bar, 1);
     tc::mbar_init(&scale_bar, 4);
     tc::fence_mbar_init();
@@ -270,7 +274,12 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           issue_raw(tile + 2 * stride, slot2);
         }
         tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));         // strips of tile it staged
-        if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // tile it-1 drained
+        if (DB) {
+          if (it >= 2) tc::mbar_wait(&acc_empty[buf], (uint32_t)(((it - 2) >> 1) & 1));  // tile it-2 drained
+        } else if (it >= 1) {
+          tc::mbar_wait(&acc_empty[0], (uint32_t)((it - 1) & 1));  // tile it-1 drained
+        }
+        const uint32_t d_tmem = tmem + (DB ? (uint32_t)(buf * N) : 0u);
         tc::fence_after();
         const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
         if (FP4) {
@@ -279,7 +288,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           for (int p = 0; p < C::NMMA; ++p) {
             const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(2 * p * PW * 16), PW * 16, 2 * PW * 16);
             const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * N * 16), N * 16, 128);
-            tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, p > 0 ? 1u : 0u);
+            tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, p > 0 ? 1u : 0u);
           }
         } else {
           // MMA s: strip row s + 2 * (pooled row), both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
@@ -287,7 +296,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           for (int s = 0; s < KS; ++s) {
             const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
             const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
-            tc::mma_i8(tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+            tc::mma_i8(d_tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
           }
         }
         tc::commit(&mma_done[buf]);
@@ -425,6 +434,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)((it >> 1) & 1));
       __syncwarp();
       tc::fence_after();
+      const uint32_t acc_base = lane_base + (DB ? (uint32_t)(buf * N) : 0u);
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
       const bool in = py < Ho && px < Wo;
       if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
@@ -433,7 +443,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
 #pragma unroll 1
           for (int cb = 0; cb < NT; cb += 16) {
             int vv[16];
-            tc::tmem_ld16(lane_base + (uint32_t)(q * NT + cb), vv);
+            tc::tmem_ld16(acc_base + (uint32_t)(q * NT + cb), vv);
             tc::tmem_ld_wait();
             const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
             if (in && oy < A.H && ox < A.W) {
@@ -450,20 +460,20 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
         int a[16], b[16], c[16];
-        tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), a);
-        tc::tmem_ld16(lane_base + (uint32_t)(1 * NT + cb), b);
+        tc::tmem_ld16(acc_base + (uint32_t)(0 * NT + cb), a);
+        tc::tmem_ld16(acc_base + (uint32_t)(1 * NT + cb), b);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
-        tc::tmem_ld16(lane_base + (uint32_t)(2 * NT + cb), b);
-        tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
+        tc::tmem_ld16(acc_base + (uint32_t)(2 * NT + cb), b);
+        tc::tmem_ld16(acc_base + (uint32_t)(3 * NT + cb), c);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&acc_empty);  // TMEM may be overwritten by the next tile's MMAs
+      if (lane == 0) tc::mbar_arrive(&acc_empty[DB ? buf : 0]);  // TMEM may be overwritten by later MMAs
       if (A.y != nullptr && in)
         A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;
     }

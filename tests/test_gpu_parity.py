@@ -434,7 +434,7 @@ def test_forward_input_threshold_edges(cuda, orc, algo, T):
         cuda.set_option("conv_algo", 0)
 
 
-@pytest.mark.parametrize("tma", [2, 1, 0])
+@pytest.mark.parametrize("tma", [3, 2, 1, 0])
 @pytest.mark.parametrize("h,w,k,cout,T,mode", [
     (96, 96, 5, 32, None, 1),
     (34, 48, 5, 32, [-128.0, 3.0, -0.5], 1),   # t = (127, -1, 0): out-of-image bytes patched to -1
@@ -460,6 +460,7 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     try:
         cuda.set_option("first_tma", 1 if tma else 0)
         cuda.set_option("first_fp4", 1 if tma == 2 else 0)  # 2: e2m1 operands (kind::mxf4), 1: int8
+        cuda.set_option("first_db", 1 if tma == 3 else 0)   # 3: int8 with double-buffered accumulators
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if Tt is None else dev(Tt), dl, max_batch=8)
         if tma:
             assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
@@ -468,6 +469,7 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     finally:
         cuda.set_option("first_tma", 1)
         cuda.set_option("first_fp4", 0)
+        cuda.set_option("first_db", 0)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, Tt).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
