@@ -417,15 +417,15 @@ bool tc_supported(int k, int cw) {
   return (k == 5 && (cw == 1 || cw == 2)) || (k == 3 && (cw == 1 || cw == 2 || cw == 4)) || (k == 7 && cw == 1);
 }
 
-template <int K, int CG, int NT>
+template <int K, int CG, int NT, int P = 1>
 bnn_status launch_conv_tc4_big_t(ConvArgs A, cudaStream_t s) {
-  using C = ConvTc4BigCfg<K, CG, NT>;
-  auto kfn = conv_tc4_big_kernel<K, CG, NT>;
+  using C = ConvTc4BigCfg<K, CG, NT, P>;
+  auto kfn = conv_tc4_big_kernel<K, CG, NT, P>;
   static int set = 0;
   if (!set) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM); set = 1; }
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
-  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  A.total_tiles = (int64_t)((A.n + P - 1) / P) * A.tiles_x * A.tiles_y;  // P images per tile
   if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
   A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
   A.fd_tx = FastDiv((uint32_t)A.tiles_x);
@@ -505,7 +505,7 @@ bnn_status dispatch_conv_tc(int k, int cw, const ConvArgs& A, cudaStream_t s) {
     if (k == 3 && cw == 2) return launch_conv_tc4_t<3, 2, 64>(A, s);
     if (k == 3 && cw == 4) return launch_conv_tc4_t<3, 4, 128>(A, s);
     if (k == 7 && cw == 1) return launch_conv_tc4_t<7, 1, 32>(A, s);
-    if (k == 3) return launch_conv_tc4_big_t<3, 4, 128>(A, s);
+    if (k == 3) return A.W == 8 ? launch_conv_tc4_big_t<3, 4, 128, 2>(A, s) : launch_conv_tc4_big_t<3, 4, 128>(A, s);
     if (k == 5) return launch_conv_tc4_big_t<5, 2, 128>(A, s);
     if (k == 7) return launch_conv_tc4_big_t<7, 1, 128>(A, s);
   }

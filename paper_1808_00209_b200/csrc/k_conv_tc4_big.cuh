@@ -13,10 +13,15 @@
 
 namespace bnn {
 
-template <int K, int CG, int NT>
+// P = images per tile.  P = 2 serves maps exactly 8 wide (CIFAR conv5/6 at 8 x 8): the tile is 8 rows x
+// (2 images x 8 columns), the two images' halos sit side by side in each halo row (ICI = 8 + K - 1
+// columns each), so core-matrix group g = 2 r + h (row r, image h) starts at g * ICI * 16 bytes --
+// the same linear SBO the P = 1 layout has -- and no tile rows are wasted on an 8 x 8 map.
+template <int K, int CG, int NT, int P = 1>
 struct ConvTc4BigCfg {
-  static constexpr int R = (K - 1) / 2, TH = 16, TW = 8;
-  static constexpr int IR = TH + K - 1, IC = TW + K - 1, NPIX = IR * IC, KK = K * K;
+  static constexpr int R = (K - 1) / 2, TH = 16 / P, TW = 8;
+  static constexpr int ICI = TW + K - 1;           // halo columns per image
+  static constexpr int IR = TH + K - 1, IC = P * ICI, NPIX = IR * IC, KK = K * K;
   static constexpr int U = CG * KK;            // chunks per stage (word j, tap t), j-major
   static constexpr int NMMA = (U + 1) / 2;
   static constexpr uint32_t A_BYTES = CG * NPIX * 16 + 256;
@@ -92,11 +97,11 @@ __global__ void __launch_bounds__(256) prep_tc4_big_kernel(const ConvArgs A, uin
                              threadIdx.x, 256);
 }
 
-template <int K, int CG, int NT>
+template <int K, int CG, int NT, int P = 1>
 __global__ void __launch_bounds__(256, 1)
 conv_tc4_big_kernel(const ConvArgs A) {
-  using C = ConvTc4BigCfg<K, CG, NT>;
-  constexpr int R = C::R, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KK = C::KK, U = C::U, PF = C::PF;
+  using C = ConvTc4BigCfg<K, CG, NT, P>;
+  constexpr int R = C::R, TH = C::TH, TW = C::TW, IC = C::IC, ICI = C::ICI, NPIX = C::NPIX, KK = C::KK, U = C::U, PF = C::PF;
   extern __shared__ __align__(1024) uint8_t dsm[];
   float* s_thr = reinterpret_cast<float*>(dsm + 2 * C::STAGE_BYTES);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);
@@ -150,6 +155,7 @@ conv_tc4_big_kernel(const ConvArgs A) {
   auto tile_origin = [&](int64_t tile, int& img, int& oy0, int& ox0) {
     int ty, tx;
     tile_coords(A, tile, img, ty, tx);
+    img *= P;  // first image of the tile
     oy0 = ty * TH;
     ox0 = tx * TW;
   };
@@ -159,8 +165,10 @@ conv_tc4_big_kernel(const ConvArgs A) {
     tc::mbar_wait(&bar_acc[buf], phase);
     tc::fence_after();
     const int m = warp * 32 + lane;
-    const int oy = oy0 + m / TW, ox = ox0 + m % TW;
-    const bool in = oy < A.H && ox < A.W;
+    const int grp = m / TW, ih = grp % P;  // core-matrix group = (row, image)
+    img += ih;
+    const int oy = oy0 + grp / P, ox = ox0 + m % TW;
+    const bool in = oy < A.H && ox < A.W && img < A.n;
 #pragma unroll 1
     for (int c0 = 0; c0 < NT && g * NT + c0 < A.c_out; c0 += 32) {
       int v[32];
@@ -182,9 +190,9 @@ conv_tc4_big_kernel(const ConvArgs A) {
       if (A.y != nullptr) {
         if (A.pool == 2) {
           uint32_t p = word | __shfl_xor_sync(BNN_FULL_MASK, word, 1);
-          p |= __shfl_xor_sync(BNN_FULL_MASK, p, 8);
+          p |= __shfl_xor_sync(BNN_FULL_MASK, p, 8 * P);  // the next output row of the same image
           const int Ho = A.H >> 1, Wo = A.W >> 1;
-          if ((lane & 9) == 0 && (oy >> 1) < Ho && (ox >> 1) < Wo)
+          if ((lane & (1 | 8 * P)) == 0 && img < A.n && (oy >> 1) < Ho && (ox >> 1) < Wo)
             A.y[(((int64_t)img * Ho + (oy >> 1)) * Wo + (ox >> 1)) * A.cwo + wo] = p;
         } else if (in) {
           A.y[(((int64_t)img * A.H + oy) * A.W + ox) * A.cwo + wo] = word;
@@ -216,10 +224,11 @@ conv_tc4_big_kernel(const ConvArgs A) {
         const int i = tid + q * 256;
         if (i < CG * NPIX) {
           const int p = i % NPIX, jl = i / NPIX, j = j0 + jl;
-          const int r = p / IC, c = p - r * IC;
+          const int r = p / IC, cc = p - r * IC, ih = cc / ICI, c = cc - ih * ICI;
           const int gy = oy0 - R + r, gx = ox0 - R + c;
           uint32_t w = 0u;  // outside the map / beyond c_in: -1 bits (weights there are 0 for words >= cw)
-          if (j < A.cw && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) w = __ldg(xin + ((int64_t)gy * A.W + gx) * A.cw + j);
+          if (j < A.cw && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W && img + ih < A.n)
+            w = __ldg(xin + ((int64_t)ih * A.H * A.W + (int64_t)gy * A.W + gx) * A.cw + j);
           uint32_t o4[4];
           expand_word_fp4(w, s_lut, o4);
           *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
@@ -244,7 +253,7 @@ conv_tc4_big_kernel(const ConvArgs A) {
           const int off0 = ((u0 / KK) * NPIX + ((u0 % KK) / K) * IC + (u0 % KK) % K) * 16;
           const int off1 = ((u1 / KK) * NPIX + ((u1 % KK) / K) * IC + (u1 % KK) % K) * 16;
           const uint32_t lbo = (off1 > off0) ? (uint32_t)(off1 - off0) : 16u;
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)off0, lbo, IC * 16);
+          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)off0, lbo, ICI * 16);
           const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(i * 2 * NT * 16), NT * 16, 128);
           tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, (st > 0 || i > 0) ? 1u : 0u);
         }

@@ -147,7 +147,9 @@ def test_conv_first_layer_pooled_tc(cuda, orc, pool_tc, n, h, w, cin, cout, k, t
     (2, 16, 16, 300, 70, 3, 1),   # streamed (big) kernel: cw = 10, partial last stage, pad channels
     (1, 12, 20, 256, 130, 5, 2),  # big k = 5: cw = 8, two N = 128 channel groups, ragged c_out
     (1, 10, 10, 64, 40, 7, 1),    # big k = 7
-    (3, 8, 8, 512, 512, 3, 2),    # CIFAR conv6 shape
+    (3, 8, 8, 512, 512, 3, 2),    # CIFAR conv6 shape (8-wide map: two images per tile, odd n)
+    (5, 8, 8, 256, 130, 3, 1),    # two images per tile, ragged c_out, no pool
+    (2, 12, 8, 256, 64, 3, 2),    # two images per tile, ragged tile rows
 ])
 @pytest.mark.parametrize("fp4", [2, 1, 0])
 def test_conv_tensor_core(cuda, orc, n, h, w, cin, cout, k, pool, fp4):
