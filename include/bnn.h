@@ -98,7 +98,10 @@ BNN_API int bnn_version(void);
  *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
  *   "first_fp4"     0 (default): that kernel's operands are int8 (kind::i8); 1: e2m1 (kind::mxf4).
- *   "first_db"      0 (default); 1: that (int8) kernel double-buffers its TMEM accumulators.
+ *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);
+ *                   0: one accumulator set (3 CTAs/SM).
+ *   "first_exp"     0 (default).  Timing experiments on that kernel (tools/time_first_exp.py); any
+ *                   nonzero value skips work and gives WRONG results.  Never set in production.
  *   "csa"           1 (default): the XOR-popcount conv compresses each kernel row's K XOR words
  *                   with carry-save adders (LOP3) before POPC; 0: one POPC per word (Eq. 4 as printed).
  *   "big_img"       1 (default): the streamed wide-channel conv expands its weights once per call
@@ -113,7 +116,7 @@ BNN_API int bnn_version(void);
  *                   im2col + packing (B = k*k), tiled XOR-popcount GEMM, int32 max-pool, 64-segment
  *                   FC -- as a comparison baseline (u8 SIGN / THRESH_RGB nets,
  *                   k <= 5, no thresholds / flips; else BNN_E_UNSUPPORTED).
- * Results are bit-identical for every setting (tiling invariance is a parity test).
+ * Results are bit-identical for every setting except "first_exp" (tiling invariance is a parity test).
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */
 BNN_API int bnn_set_option(const char* key, int value);
 
@@ -181,6 +184,19 @@ BNN_API bnn_status bnn_dense(const uint32_t* x, int n, int64_t d, const uint32_t
                      const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, bnn_stream_t stream);
 
 /* ---------------------------------------------------------------------------------
+ * bnn_affine -- float output scaling of a last layer's integer logits (SURVEY f4 variant:
+ * BinaryNet's output batch-normalisation folded to a per-class affine map -- BinaryNet is the
+ * paper's BNN reference, PAPER.md:74 -- and XNOR-Net's per-output scaling factor, bias 0):
+ *   score[i, o] = fmaf(scale[o], (float)acc[i, o], bias[o])    (fp32, ONE rounding; |acc| < 2^24)
+ *   cls[i]      = first maximum of score[i, :]  (R19; the decision is taken on the fp32 scores, R25)
+ *   acc : DEVICE int32 [n, l];  scale, bias : DEVICE float32 [l] (finite);  1 <= l <= 1024.
+ *   score : DEVICE float32 [n, l] or NULL;  cls : DEVICE int32 [n] or NULL (not both NULL).
+ * Errors: BNN_E_ARG, BNN_E_ALIGN, BNN_E_CUDA.
+ * ------------------------------------------------------------------------------- */
+BNN_API bnn_status bnn_affine(const int32_t* acc, int n, int l, const float* scale, const float* bias, float* score,
+                              int32_t* cls, bnn_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
  * Network handle: the whole forward pass of Section 2 / Table 2:
  *   [input binarization] -> conv (+threshold, +pool) ... -> dense ... -> int32 logits.
  * ------------------------------------------------------------------------------- */
@@ -216,6 +232,14 @@ BNN_API bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode
  * NULL), cls DEVICE int32 [n] (argmax, first maximum wins; may be NULL).  Asynchronous. */
 BNN_API bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits, int32_t* cls,
                        bnn_stream_t stream);
+
+/* bnn_forward followed by bnn_affine on the last layer's logits: images DEVICE -> logits DEVICE
+ * int32 [n, l_last] (required: the integer logits are kept), scores DEVICE float32 [n, l_last]
+ * (may be NULL), cls DEVICE int32 [n] = first maximum of the fp32 scores (may be NULL; not both
+ * NULL).  scale / bias: DEVICE float32 [l_last].  Asynchronous.  Errors as bnn_forward and
+ * bnn_affine (BNN_E_UNSUPPORTED for l_last > 1024). */
+BNN_API bnn_status bnn_forward_scores(bnn_net* net, const void* images, int n, const float* scale, const float* bias,
+                                      int32_t* logits, float* scores, int32_t* cls, bnn_stream_t stream);
 
 /* End-to-end variant: HOST images (pinned for full speed; pageable works) -> HOST logits /
  * cls.  Copies chunks host->device, runs the forward pass and copies results back,

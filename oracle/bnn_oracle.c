@@ -10,6 +10,7 @@
  */
 #include "bnn_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -232,6 +233,21 @@ void orc_dense(const int8_t* x, int64_t d, const int8_t* W, int l, int64_t* acc)
 }
 
 int orc_argmax_i64(const int64_t* v, int l) {
+  int best = 0;
+  for (int i = 1; i < l; ++i)
+    if (v[i] > v[best]) best = i;
+  return best;
+}
+
+void orc_affine(const int64_t* acc, int l, const float* scale, const float* bias, double* score64,
+                float* score32) {
+  for (int o = 0; o < l; ++o) {
+    if (score64) score64[o] = (double)scale[o] * (double)acc[o] + (double)bias[o];
+    if (score32) score32[o] = fmaf(scale[o], (float)acc[o], bias[o]);
+  }
+}
+
+int orc_argmax_f32(const float* v, int l) {
   int best = 0;
   for (int i = 1; i < l; ++i)
     if (v[i] > v[best]) best = i;

@@ -97,6 +97,19 @@ void orc_dense(const int8_t* x, int64_t d, const int8_t* W, int l, int64_t* acc)
 /* First maximum wins (reading R19). */
 int orc_argmax_i64(const int64_t* v, int l);
 
+/* Float output scaling of the last layer (SURVEY f4 variant): BinaryNet's output batch
+ * normalisation folded to a per-class affine map (BinaryNet is the paper's ref. for BNNs,
+ * PAPER.md:74) and XNOR-Net's per-output scaling factor alpha (bias 0) both take the form
+ *   score[o] = scale[o] * acc[o] + bias[o].
+ * score64: the value in double (the tolerance comparison, 1e-5 relative per north_star);
+ * score32: the same value in fp32 with ONE rounding (fmaf; exact float(acc) for |acc| < 2^24),
+ * the precision the argmax decision is taken in on both sides (R25).  Either may be NULL. */
+void orc_affine(const int64_t* acc, int l, const float* scale, const float* bias, double* score64,
+                float* score32);
+
+/* First maximum wins over fp32 scores (R19, R25). */
+int orc_argmax_f32(const float* v, int l);
+
 /* A network for orc_forward.  kind 1 = conv (k, c_out, pool in {1,2}),
  * kind 2 = dense (l).  Hidden layers are binarized with thr/flip (NULL = Eq. 1);
  * the last layer must be dense and returns integer logits. */

@@ -30,6 +30,7 @@ _c_u32p = ctypes.POINTER(ctypes.c_uint32)
 _c_i32p = ctypes.POINTER(ctypes.c_int32)
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_f64p = ctypes.POINTER(ctypes.c_double)
+_c_f32p = ctypes.POINTER(ctypes.c_float)
 
 
 class OrcLayer(ctypes.Structure):
@@ -43,7 +44,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "bnn_oracle.h"))):
         tmp = _LIB_PATH + ".tmp%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -85,6 +86,10 @@ def lib():
         L.orc_dense.restype = None
         L.orc_argmax_i64.argtypes = [_c_i64p, ctypes.c_int]
         L.orc_argmax_i64.restype = ctypes.c_int
+        L.orc_affine.argtypes = [_c_i64p, ctypes.c_int, _c_f32p, _c_f32p, _c_f64p, _c_f32p]
+        L.orc_affine.restype = None
+        L.orc_argmax_f32.argtypes = [_c_f32p, ctypes.c_int]
+        L.orc_argmax_f32.restype = ctypes.c_int
         L.orc_forward.argtypes = [_c_f64p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_f64p,
                                   ctypes.POINTER(OrcLayer), ctypes.c_int, _c_i64p, _c_i32p]
         L.orc_forward.restype = ctypes.c_int
@@ -250,6 +255,25 @@ def dense(x, W) -> np.ndarray:
 def argmax(v) -> int:
     v = np.ascontiguousarray(v, dtype=np.int64)
     return lib().orc_argmax_i64(_p(v, _c_i64p), v.size)
+
+
+def affine(acc, scale, bias):
+    """Float output scaling of the last layer (f4: BinaryNet output BN folded / XNOR-Net alpha,
+    PAPER.md:74): acc int [..., l] -> (score float64, score float32 with one rounding, class).
+    The class is the first maximum of the fp32 scores (R19, R25)."""
+    acc = np.ascontiguousarray(np.atleast_2d(acc), dtype=np.int64)
+    scale = np.ascontiguousarray(scale, dtype=np.float32)
+    bias = np.ascontiguousarray(bias, dtype=np.float32)
+    n, l = acc.shape
+    assert scale.shape == (l,) and bias.shape == (l,)
+    s64 = np.zeros((n, l), dtype=np.float64)
+    s32 = np.zeros((n, l), dtype=np.float32)
+    cls = np.zeros(n, dtype=np.int32)
+    for i in range(n):
+        lib().orc_affine(_p(acc[i], _c_i64p), l, _p(scale, _c_f32p), _p(bias, _c_f32p), _p(s64[i], _c_f64p),
+                         _p(s32[i], _c_f32p))
+        cls[i] = lib().orc_argmax_f32(_p(s32[i], _c_f32p), l)
+    return s64, s32, cls
 
 
 # ---- whole network -----------------------------------------------------------------------------

@@ -61,6 +61,10 @@ def lib():
         L.bnn_maxpool.restype = i
         L.bnn_dense.argtypes = [vp, i, i64, vp, i, vp, vp, vp, vp, vp, vp]
         L.bnn_dense.restype = i
+        L.bnn_affine.argtypes = [vp, i, i, vp, vp, vp, vp, vp]
+        L.bnn_affine.restype = i
+        L.bnn_forward_scores.argtypes = [vp, vp, i, vp, vp, vp, vp, vp, vp]
+        L.bnn_forward_scores.restype = i
         L.bnn_net_create.argtypes = [i, i, i, i, i, vp, ctypes.POINTER(_Layer), i, i, ctypes.POINTER(vp)]
         L.bnn_net_create.restype = i
         L.bnn_forward.argtypes = [vp, vp, i, vp, vp, vp]
@@ -177,6 +181,18 @@ def dense(x: torch.Tensor, d: int, wt: torch.Tensor, l: int, thr=None, flip=None
     return y, acc, cls
 
 
+def affine(acc: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, want_score=True, want_cls=True, stream=None):
+    """bnn_affine: int32 logits [n, l] -> (fp32 scores [n, l] | None, int32 cls [n] | None)."""
+    for t, nm in ((acc, "acc"), (scale, "scale"), (bias, "bias")):
+        _dev(t, nm)
+    n, l = acc.shape
+    score = torch.empty((n, l), dtype=torch.float32, device=acc.device) if want_score else None
+    cls = torch.empty((n,), dtype=torch.int32, device=acc.device) if want_cls else None
+    _check(lib().bnn_affine(_ptr(acc), n, l, _ptr(scale), _ptr(bias), _ptr(score), _ptr(cls), _stream(stream)),
+           "bnn_affine")
+    return score, cls
+
+
 class _DeviceBuffer:
     """A library-owned device buffer exposed through __cuda_array_interface__ (no copy)."""
 
@@ -230,6 +246,17 @@ class Net:
         _check(lib().bnn_forward(self.handle, _ptr(images), n, _ptr(logits), _ptr(cls), _stream(stream)),
                "bnn_forward")
         return logits, cls
+
+    def forward_scores(self, images: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, stream=None):
+        """bnn_forward_scores: images -> (int32 logits [n, L], fp32 scores [n, L], int32 cls [n])."""
+        _dev(images, "images")
+        n = images.shape[0]
+        logits = torch.empty((n, self.n_classes), dtype=torch.int32, device=images.device)
+        scores = torch.empty((n, self.n_classes), dtype=torch.float32, device=images.device)
+        cls = torch.empty((n,), dtype=torch.int32, device=images.device)
+        _check(lib().bnn_forward_scores(self.handle, _ptr(images), n, _ptr(scale), _ptr(bias), _ptr(logits),
+                                        _ptr(scores), _ptr(cls), _stream(stream)), "bnn_forward_scores")
+        return logits, scores, cls
 
     def forward_host(self, images: torch.Tensor, logits: torch.Tensor | None = None, cls: torch.Tensor | None = None,
                      stream=None):

@@ -75,7 +75,8 @@ int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-orde
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
-int g_opt_first_db = 0;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM)
+int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
+int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (wrong results unless 0)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
@@ -336,6 +337,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
   A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = 0;
+  A.exp = g_opt_first_exp;
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
   const cuuint64_t strides[2] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H * A.W * 3};
@@ -717,7 +719,7 @@ extern "C" {
 
 const char* bnn_last_error(void) { return g_err.c_str(); }
 
-int bnn_version(void) { return 100; }
+int bnn_version(void) { return 101; }
 
 int bnn_set_option(const char* key, int value) {
   if (key == nullptr) return (int)fail(BNN_E_ARG, "bnn_set_option: null key");
@@ -729,6 +731,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
+  if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
@@ -800,6 +803,22 @@ bnn_status bnn_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, in
   BNN_REQUIRE_ALIGNED(acc, "bnn_dense acc");
   BNN_REQUIRE_ALIGNED(cls, "bnn_dense cls");
   return launch_dense(x, n, d, wt, l, thr, flip, y, acc, cls, (cudaStream_t)stream);
+}
+
+bnn_status bnn_affine(const int32_t* acc, int n, int l, const float* scale, const float* bias, float* score,
+                      int32_t* cls, bnn_stream_t stream) {
+  if (n < 0 || l < 1 || l > 1024) return fail(BNN_E_ARG, "bnn_affine: bad sizes (need 1 <= l <= 1024)");
+  if (n > 0 && (acc == nullptr || scale == nullptr || bias == nullptr)) return fail(BNN_E_ARG, "bnn_affine: null pointer");
+  if (n > 0 && score == nullptr && cls == nullptr) return fail(BNN_E_ARG, "bnn_affine: no output");
+  BNN_REQUIRE_ALIGNED(acc, "bnn_affine acc");
+  BNN_REQUIRE_ALIGNED(scale, "bnn_affine scale");
+  BNN_REQUIRE_ALIGNED(bias, "bnn_affine bias");
+  BNN_REQUIRE_ALIGNED(score, "bnn_affine score");
+  BNN_REQUIRE_ALIGNED(cls, "bnn_affine cls");
+  if (n == 0) return BNN_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_pdl(affine_argmax_kernel, dim3(grid_for((int64_t)n * 32, 256)), dim3(256), 0, s, acc, n, l, scale, bias, score, cls);
+  return check_launch("affine_argmax_kernel");
 }
 
 }  // extern "C"
@@ -1394,6 +1413,19 @@ bnn_status bnn_forward(bnn_net* net, const void* images, int n, int32_t* logits,
     cudaStreamWaitEvent(s, net->ev_join, 0);
   }
   return BNN_OK;
+}
+
+bnn_status bnn_forward_scores(bnn_net* net, const void* images, int n, const float* scale, const float* bias,
+                              int32_t* logits, float* scores, int32_t* cls, bnn_stream_t stream) {
+  if (net == nullptr) return fail(BNN_E_ARG, "bnn_forward_scores: null net");
+  if (n > 0 && logits == nullptr) return fail(BNN_E_ARG, "bnn_forward_scores: logits buffer required");
+  const int L = net->L.back().l;
+  if (L > 1024) return fail(BNN_E_UNSUPPORTED, "bnn_forward_scores: more than 1024 classes");
+  if (n > 0 && (scale == nullptr || bias == nullptr)) return fail(BNN_E_ARG, "bnn_forward_scores: null scale / bias");
+  if (n > 0 && scores == nullptr && cls == nullptr) return fail(BNN_E_ARG, "bnn_forward_scores: no output");
+  bnn_status st = bnn_forward(net, images, n, logits, nullptr, stream);
+  if (st != BNN_OK || n == 0) return st;
+  return bnn_affine(logits, n, L, scale, bias, scores, cls, stream);
 }
 
 bnn_status bnn_net_staging(bnn_net* net, int max_staged, void** in, int32_t** logits, int32_t** cls) {

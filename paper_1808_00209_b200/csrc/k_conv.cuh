@@ -35,6 +35,7 @@ struct ConvArgs {
   int tiles_per_cta;
   FastDiv fd_img, fd_tx;  // division by tiles_x * tiles_y and by tiles_x
   const uint8_t* bimg;    // pre-expanded shared-memory image of the weight operand (per channel group) or null
+  int exp;                // timing-experiment bits (bnn_set_option "first_exp"; 0 in production: results exact)
 };
 
 // tile index -> (image, tile row, tile column), two multiply-high divisions

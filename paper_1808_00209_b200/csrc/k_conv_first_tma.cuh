@@ -6,7 +6,7 @@
 // tile, strips of K taps x 3 channels as int8 +/-1, two parity planes, 4 accumulator blocks one per
 // 2x2 pool offset), but every per-pixel instruction that kernel spent is gone or halved:
 //   * the raw u8 halo box (IR rows x 80 B, starting 16 B left of the tile: the innermost TMA box
-//     coordinate must be 16-byte aligned) is one cp.async.bulk.tensor per tile into a 3-deep ring;
+//     coordinate must be 16-byte aligned) is one cp.async.bulk.tensor per tile into an NRAW-deep ring;
 //     out-of-image bytes arrive as 0, which thresholds to -1 = the binary padding whenever every
 //     channel threshold t_c >= 0 (else a uniform slow path patches them);
 //   * the threshold x > t_c (R14) runs 4 bytes at a time: the even / odd bytes are spread into two
@@ -40,7 +40,7 @@ struct FirstTmaCfg {
   static constexpr int RAW_W = 80;  // box row bytes (>= DELTA + IC * 3; 80 B pitch spreads smem banks)
   static constexpr uint32_t RAW_BYTES = IR * RAW_W;
   static constexpr uint32_t RAW_STRIDE = (RAW_BYTES + 127) / 128 * 128;  // TMA destinations 128-B aligned
-  static constexpr int NRAW = 3;
+  static constexpr int NRAW = 8;  // raw-box ring: TMA prefetch distance NRAW - 1 tiles (HBM latency x bandwidth)
   static constexpr int KS = K + 1;        // strip rows per MMA group = taps per strip (pool offsets 0/1)
   static constexpr int SB = KS * CIN;     // data bytes of a strip (18 for K = 5); bytes SB..31 = -1
   static constexpr int N = 4 * NT;        // MMA N: (dy, dx) pool offsets x NT channels
@@ -88,6 +88,12 @@ BNN_DEV void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
           tc::smem_addr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(tc::smem_addr(bar))
       : "memory");
+}
+
+// mbarrier wait of the staging / epilogue warps: sleeping (suspend-time hint) unless exp bit 16
+BNN_DEV void wait_x(int exp, uint64_t* bar, uint32_t phase) {
+  if (exp & 16) tc::mbar_wait(bar, phase);
+  else tc::mbar_wait_sleep(bar, phase);
 }
 
 BNN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -184,7 +190,7 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
 }
 
 // Warp roles (no block-wide barrier in the tile loop; mbarriers carry every hand-off):
-//   warp 0, one thread : TMA producer (raw box of tile it+2 into the 3-deep ring) and MMA issuer
+//   warp 0, one thread : TMA producer (raw box of tile it+NRAW-1 into the ring) and MMA issuer
 //   warps 1-5          : builders (144 two-strip items of a tile)
 //   warps 6-9          : epilogue (TMEM lane quarter warp % 4, all 32 channels of a pooled pixel)
 // raw_full[s]   TMA complete_tx              -> builders          raw_empty[s] builders (5) -> producer
@@ -261,17 +267,18 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         mbar_expect_tx(&raw_full[slot], C::RAW_BYTES);
         tma_load_3d(sRaw + slot * C::RAW_STRIDE, &xmap, ox0 * CIN - C::XOFF, oy0 - R, img, &raw_full[slot]);
       };
-      if ((int)blockIdx.x < ntiles) issue_raw(blockIdx.x, 0);
-      if ((int)blockIdx.x + stride < ntiles) issue_raw(blockIdx.x + stride, 1);
+#pragma unroll 1
+      for (int j = 0; j < C::NRAW - 1; ++j)
+        if ((int)blockIdx.x + j * stride < ntiles) issue_raw(blockIdx.x + j * stride, j);
       if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       if (FP4) tc::mbar_wait(&scale_bar, 0);            // block scales written by the epilogue warps
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
         const int buf = it & 1;
-        if (tile + 2 * stride < ntiles) {
-          const int slot2 = (it + 2) % C::NRAW;  // last used by tile it-1
+        if (tile + (C::NRAW - 1) * stride < ntiles) {
+          const int slot2 = (it + C::NRAW - 1) % C::NRAW;  // last used by tile it-1
           if (it >= 1) tc::mbar_wait(&raw_empty[slot2], (uint32_t)(((it - 1) / C::NRAW) & 1));
-          issue_raw(tile + 2 * stride, slot2);
+          issue_raw(tile + (C::NRAW - 1) * stride, slot2);
         }
         tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));         // strips of tile it staged
         if (DB) {
@@ -294,6 +301,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           // MMA s: strip row s + 2 * (pooled row), both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
+            if ((A.exp & 8) && s > 0) break;
             const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
             const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
             tc::mma_i8(d_tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
@@ -323,9 +331,9 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
-      tc::mbar_wait_sleep(&raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
-      if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
-      if (bt < C::GROUPS) {
+      wait_x(A.exp, &raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
+      if (it >= 2) wait_x(A.exp, &mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      if (bt < C::GROUPS && !(A.exp & 4)) {
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
         const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
@@ -431,7 +439,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
-      tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      wait_x(A.exp, &mma_done[buf], (uint32_t)((it >> 1) & 1));
       __syncwarp();
       tc::fence_after();
       const uint32_t acc_base = lane_base + (DB ? (uint32_t)(buf * N) : 0u);
@@ -457,9 +465,18 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           }
       }
       uint32_t neg = 0;
+      if (!(A.exp & 2))
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
         int a[16], b[16], c[16];
+        if (A.exp & 1) {
+          tc::tmem_ld16(acc_base + (uint32_t)(0 * NT + cb), a);
+          tc::tmem_ld16(acc_base + (uint32_t)(1 * NT + cb), b);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], a[k] ^ k), neg, 1);
+          continue;
+        }
         tc::tmem_ld16(acc_base + (uint32_t)(0 * NT + cb), a);
         tc::tmem_ld16(acc_base + (uint32_t)(1 * NT + cb), b);
         tc::tmem_ld_wait();

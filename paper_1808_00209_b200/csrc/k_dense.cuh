@@ -168,6 +168,40 @@ __global__ void argmax_kernel(const int32_t* __restrict__ logits, int n, int l, 
   }
 }
 
+// Float output scaling of the last layer (BinaryNet's output batch-norm folded to a
+// per-class affine map, XNOR-Net's per-output alpha): score = fmaf(scale[o], (float)acc, bias[o]) --
+// one rounding, exact float(acc) for |acc| < 2^24 (precondition) -- and the first maximum of the fp32
+// scores (R19, R25).  One warp per image, scale / bias staged in shared memory (l <= 1024).
+__global__ void affine_argmax_kernel(const int32_t* __restrict__ acc, int n, int l, const float* __restrict__ scale,
+                                     const float* __restrict__ bias, float* __restrict__ score,
+                                     int32_t* __restrict__ cls) {
+  griddep_launch();
+  __shared__ float s_sc[1024], s_b[1024];
+  for (int o = threadIdx.x; o < l; o += blockDim.x) {
+    s_sc[o] = scale[o];
+    s_b[o] = bias[o];
+  }
+  __syncthreads();
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  for (int64_t img = gtid() >> 5; img < n; img += gstride() >> 5) {
+    float bv = 0.f;
+    int bi = INT_MAX;
+    for (int o = lane; o < l; o += 32) {
+      const float v = __fmaf_rn(s_sc[o], (float)acc[img * l + o], s_b[o]);
+      if (score != nullptr) score[img * l + o] = v;
+      if (bi == INT_MAX || v > bv) { bv = v; bi = o; }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      const float ov = __shfl_xor_sync(BNN_FULL_MASK, bv, s);
+      const int oi = __shfl_xor_sync(BNN_FULL_MASK, bi, s);
+      if (oi != INT_MAX && (bi == INT_MAX || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    if (lane == 0 && cls != nullptr) cls[img] = bi;
+  }
+}
+
 // 2x2 stride-2 OR pooling of a packed map (max over {-1,+1} == OR of the bits).
 __global__ void maxpool_or_kernel(const uint32_t* __restrict__ x, int n, int H, int W, int cw,
                                   uint32_t* __restrict__ y) {

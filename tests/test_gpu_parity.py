@@ -462,7 +462,7 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     try:
         cuda.set_option("first_tma", 1 if tma else 0)
         cuda.set_option("first_fp4", 1 if tma == 2 else 0)  # 2: e2m1 operands (kind::mxf4), 1: int8
-        cuda.set_option("first_db", 1 if tma == 3 else 0)   # 3: int8 with double-buffered accumulators
+        cuda.set_option("first_db", 0 if tma == 1 else 1)   # 1: int8, one accumulator set; 3: int8 double-buffered (default)
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if Tt is None else dev(Tt), dl, max_batch=8)
         if tma:
             assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
@@ -471,7 +471,7 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     finally:
         cuda.set_option("first_tma", 1)
         cuda.set_option("first_fp4", 0)
-        cuda.set_option("first_db", 0)
+        cuda.set_option("first_db", 1)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, Tt).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
@@ -588,3 +588,45 @@ def test_forward_fault_injection(cuda, orc):
     torch.cuda.synchronize()
     ref, _ = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=4)
     assert np.array_equal(lg.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------------------------ f4 output scaling
+@pytest.mark.parametrize("n,l", [(0, 4), (1, 4), (37, 10), (300, 100), (5, 1024)])
+def test_affine(cuda, orc, n, l):
+    """bnn_affine: fp32 scores bit-identical to the oracle's single-rounding fmaf value, within 1e-5
+    relative of the fp64 value (north_star), and the first-maximum class of the fp32 scores (R25)."""
+    g = torch.Generator().manual_seed(n * 1000 + l)
+    acc = (torch.randint(-60, 61, (n, l), generator=g) * 2).to(torch.int32)
+    if n > 1 and l > 3:
+        acc[1, 2] = acc[1, 3] = 500  # a tie under any positive scale with equal bias
+    scale = torch.rand(l, generator=g) * 2 + 0.01
+    bias = torch.randn(l, generator=g)
+    if l > 3:
+        scale[3], bias[3] = scale[2], bias[2]
+    scale[0] = -scale[0]  # a negative per-class scale (flipped BN)
+    score, cls = cuda.affine(dev(acc), dev(scale), dev(bias))
+    torch.cuda.synchronize()
+    s64, s32, rcls = orc.affine(acc.numpy(), scale.numpy(), bias.numpy())
+    if n == 0:
+        return
+    got = score.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), s32.view(np.uint32))
+    assert np.all(np.abs(got - s64) <= 1e-5 * np.maximum(np.abs(s64), 1e-30) + 1e-30)
+    assert np.array_equal(cls.cpu().numpy(), rcls)
+
+
+@pytest.mark.parametrize("mode", [1, -1])
+def test_forward_scores_vehicle(cuda, orc, mode):
+    """bnn_forward_scores = oracle forward pass -> per-class affine (XNOR-Net alpha / folded output BN)."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, mode, 1700 + mode)
+    imgs = synth.images(40, 96, 96, 3, 1710)
+    g = torch.Generator().manual_seed(1720)
+    scale = torch.rand(4, generator=g) + 0.5
+    bias = torch.randn(4, generator=g) * 3
+    logits, scores, cls = net.forward_scores(dev(imgs), dev(scale), dev(bias))
+    torch.cuda.synchronize()
+    ref_logits, _ = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=8)
+    assert np.array_equal(logits.cpu().numpy(), ref_logits)
+    _, s32, rcls = orc.affine(ref_logits, scale.numpy(), bias.numpy())
+    assert np.array_equal(scores.cpu().numpy().view(np.uint32), s32.view(np.uint32))
+    assert np.array_equal(cls.cpu().numpy(), rcls)

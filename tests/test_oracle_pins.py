@@ -421,3 +421,45 @@ def test_conv_point_equals_full(orc):
     acc = orc.conv_binary(x, wt)
     for (y, xx, o) in [(0, 0, 0), (3, 4, 1), (6, 8, 2), (0, 8, 1), (6, 0, 0)]:
         assert orc.conv_binary_point(x, wt[o], y, xx) == acc[y, xx, o]
+
+
+# ----------------------------------------------------------------------------- f4 output scaling
+def test_affine_identity_and_integer_argmax(orc):
+    """scale = 1, bias = 0 reproduces the integer logits and the integer argmax (R19), ties included."""
+    rng = np.random.default_rng(7)
+    acc = rng.integers(-100, 101, size=(200, 10)) * 2
+    acc[:, 3] = acc[:, 7]  # ties -> first maximum
+    s64, s32, cls = orc.affine(acc, np.ones(10), np.zeros(10))
+    assert np.array_equal(s64, acc.astype(np.float64)) and np.array_equal(s32, acc.astype(np.float32))
+    assert np.array_equal(cls, np.array([orc.argmax(a) for a in acc]))
+
+
+def test_affine_negative_scale_is_argmin(orc):
+    """A uniform negative scale turns the decision into the first minimum."""
+    rng = np.random.default_rng(8)
+    acc = rng.integers(-50, 51, size=(100, 4))
+    _, _, cls = orc.affine(acc, np.full(4, -0.25), np.zeros(4))
+    assert np.array_equal(cls, np.argmin(acc, axis=1))
+
+
+def test_affine_closed_form_dyadic(orc):
+    """Dyadic scale/bias (exact in fp32 and fp64): score = scale*acc + bias in closed form, per class."""
+    acc = np.array([[7, -3, 0, 12]])
+    scale = np.array([0.5, -2.0, 4.0, 0.125])
+    bias = np.array([1.25, 0.5, -3.0, 0.0])
+    s64, s32, cls = orc.affine(acc, scale, bias)
+    want = [4.75, 6.5, -3.0, 1.5]
+    assert s64[0].tolist() == want and s32[0].tolist() == want and cls[0] == 1
+
+
+def test_affine_fp32_single_rounding(orc):
+    """score32 is the fp64 value rounded once to fp32 (|acc| < 2^24, so the product is exact in
+    fp64 and the fp64 sum of two fp32-exact terms rounds at most at 2^-53 relative)."""
+    rng = np.random.default_rng(9)
+    acc = rng.integers(-20000, 20001, size=(50, 16))
+    scale = rng.standard_normal(16).astype(np.float32)
+    bias = rng.standard_normal(16).astype(np.float32)
+    s64, s32, _ = orc.affine(acc, scale, bias)
+    exact = scale.astype(np.float64)[None] * acc + bias.astype(np.float64)[None]
+    assert np.array_equal(s64, exact)
+    assert np.max(np.abs(s32.astype(np.float64) - exact) / np.maximum(np.abs(exact), 1e-30)) < 2 ** -23
