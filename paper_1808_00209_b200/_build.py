@@ -45,19 +45,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+TRACE_LIB = os.path.join(PKG, "libbnn_trace.so")  # diagnostics build (-DBNN_TRACE: bnn_set_trace records)
+
+
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    out = TRACE_LIB if trace else LIB
+    if not trace and not force and not needs_build():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp, os.path.join(CSRC, "bnn_api.cu")]
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DBNN_TRACE=1"] if trace else []), "-I", INCLUDE, "-I", CSRC, "-o", tmp,
+           os.path.join(CSRC, "bnn_api.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

@@ -37,21 +37,25 @@ _lib = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # BNN_TRACE_LIB=1 selects the diagnostics build (tools/trace_first.py); same kernels + role timestamps
+    return _build.TRACE_LIB if os.environ.get("BNN_TRACE_LIB") == "1" else _build.LIB
 
 
 def lib():
     """Load libbnn.so (in-tree).  Raises if it has not been built: there is no fallback."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.LIB):
+        path = lib_path()
+        if not os.path.exists(path):
             raise RuntimeError("libbnn.so is not built (%s); run `python -m paper_1808_00209_b200._build` -- "
-                               "there is no CPU fallback" % _build.LIB)
-        L = ctypes.CDLL(_build.LIB)
+                               "there is no CPU fallback" % path)
+        L = ctypes.CDLL(path)
         vp, i, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
         L.bnn_last_error.restype = ctypes.c_char_p
         L.bnn_version.restype = i
         L.bnn_set_option.argtypes = [ctypes.c_char_p, i]
+        L.bnn_set_trace.argtypes = [vp, i]
+        L.bnn_set_trace.restype = i
         L.bnn_set_option.restype = i
         L.bnn_pack.argtypes = [vp, i, i, i, i, i, i, vp, vp, vp]
         L.bnn_pack.restype = i
@@ -115,6 +119,15 @@ def _stream(stream):
 
 def set_option(key: str, value: int):
     _check(lib().bnn_set_option(key.encode(), int(value)), "bnn_set_option")
+
+
+def set_trace(buf: torch.Tensor | None):
+    """bnn_set_trace: register an int64 CUDA tensor as the role-timestamp trace buffer (None disables)."""
+    if buf is None:
+        _check(lib().bnn_set_trace(None, 0), "bnn_set_trace")
+    else:
+        _dev(buf, "trace")
+        _check(lib().bnn_set_trace(_ptr(buf), buf.numel()), "bnn_set_trace")
 
 
 def pack(x: torch.Tensor, mode: int = SIGN, T: torch.Tensor | None = None, out: torch.Tensor | None = None,

@@ -77,7 +77,9 @@ int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool
 int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
 int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (wrong results unless 0)
-int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
+int g_opt_first_tma = 1;
+unsigned long long* g_trace = nullptr;  // bnn_set_trace
+int g_trace_cap = 0;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
@@ -338,6 +340,8 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = 0;
   A.exp = g_opt_first_exp;
+  A.trace = g_trace;
+  A.trace_cap = g_trace_cap;
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
   const cuuint64_t strides[2] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H * A.W * 3};
@@ -720,6 +724,16 @@ extern "C" {
 const char* bnn_last_error(void) { return g_err.c_str(); }
 
 int bnn_version(void) { return 101; }
+
+bnn_status bnn_set_trace(unsigned long long* buf, int cap) {
+  if (cap < 0 || (buf == nullptr) != (cap == 0)) return fail(BNN_E_ARG, "bnn_set_trace: bad buffer / capacity");
+#ifndef BNN_TRACE
+  if (buf != nullptr) return fail(BNN_E_UNSUPPORTED, "bnn_set_trace: this build records no trace (build with --trace)");
+#endif
+  g_trace = buf;
+  g_trace_cap = cap;
+  return BNN_OK;
+}
 
 int bnn_set_option(const char* key, int value) {
   if (key == nullptr) return (int)fail(BNN_E_ARG, "bnn_set_option: null key");

@@ -36,7 +36,18 @@ struct ConvArgs {
   FastDiv fd_img, fd_tx;  // division by tiles_x * tiles_y and by tiles_x
   const uint8_t* bimg;    // pre-expanded shared-memory image of the weight operand (per channel group) or null
   int exp;                // timing-experiment bits (bnn_set_option "first_exp"; 0 in production: results exact)
+  unsigned long long* trace;  // bnn_set_trace buffer (CTA (0,0) role timestamps) or null
+  int trace_cap;
 };
+
+// Role timestamp of tile iteration `it`, event `ev` (< 8) of CTA (0, 0), SM clock (bnn_set_trace)
+template <typename Args>
+BNN_DEV void trace_ev(const Args& A, int it, int ev) {
+#ifdef BNN_TRACE
+  if (A.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it * 8 + ev < A.trace_cap)
+    A.trace[it * 8 + ev] = clock64();
+#endif
+}
 
 // tile index -> (image, tile row, tile column), two multiply-high divisions
 template <typename Args>

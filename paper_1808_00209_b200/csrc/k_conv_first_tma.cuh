@@ -47,7 +47,12 @@ struct FirstTmaCfg {
   static constexpr int SRR = IR;          // strip rows
   // i8: a strip row is 32 int8 = two 16-byte K chunks (planes), one MMA (K = 32) per strip row;
   // FP4: a strip row is 32 e2m1 nibbles = one 16-byte chunk, one MMA (K = 64) per pair of strip rows
-  static constexpr uint32_t PLANE = SRR * PW * 16;
+  // int8 strip-row pitch: one core matrix (PW = 8 strips x 16 B) + 16 B of padding, so the builders'
+  // 16-byte stores of rows r and r+1 land in different banks (a 128-B pitch made every STS.128 of a
+  // quarter-warp a 2-way bank conflict: ncu, half of the shared-memory store wavefronts); the MMA's
+  // core matrices stay contiguous 128 B (SBO = 2 pitches)
+  static constexpr uint32_t ROWP = FP4 ? PW * 16 : PW * 16 + 16;
+  static constexpr uint32_t PLANE = SRR * ROWP;
   static constexpr uint32_t A_BYTES = FP4 ? PLANE : 2 * PLANE;
   static constexpr int NMMA = FP4 ? KS / 2 : KS;
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
@@ -281,12 +286,14 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           issue_raw(tile + (C::NRAW - 1) * stride, slot2);
         }
         tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));         // strips of tile it staged
+        trace_ev(A, it, 0);
         if (DB) {
           if (it >= 2) tc::mbar_wait(&acc_empty[buf], (uint32_t)(((it - 2) >> 1) & 1));  // tile it-2 drained
         } else if (it >= 1) {
           tc::mbar_wait(&acc_empty[0], (uint32_t)((it - 1) & 1));  // tile it-1 drained
         }
         const uint32_t d_tmem = tmem + (DB ? (uint32_t)(buf * N) : 0u);
+        trace_ev(A, it, 1);
         tc::fence_after();
         const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
         if (FP4) {
@@ -302,12 +309,13 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
             if ((A.exp & 8) && s > 0) break;
-            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * PW * 16), C::PLANE, 2 * PW * 16);
+            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * C::ROWP), C::PLANE, 2 * C::ROWP);
             const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
             tc::mma_i8(d_tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
           }
         }
         tc::commit(&mma_done[buf]);
+        trace_ev(A, it, 2);
       }
     }
     __syncwarp();
@@ -332,7 +340,9 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
       wait_x(A.exp, &raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
+      if (tid == 32) trace_ev(A, it, 3);
       if (it >= 2) wait_x(A.exp, &mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      if (tid == 32) trace_ev(A, it, 4);
       if (bt < C::GROUPS && !(A.exp & 4)) {
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
@@ -405,14 +415,15 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
               else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
             }
             const int px = 2 * j + s;
-            *reinterpret_cast<uint4*>(a + (size_t)(r * PW + px) * 16) = make_uint4(v[0], v[1], v[2], v[3]);
-            *reinterpret_cast<uint4*>(a + C::PLANE + (size_t)(r * PW + px) * 16) = make_uint4(v[4], v[5], v[6], v[7]);
+            *reinterpret_cast<uint4*>(a + r * C::ROWP + px * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<uint4*>(a + C::PLANE + r * C::ROWP + px * 16) = make_uint4(v[4], v[5], v[6], v[7]);
           }
         }
       }
       tc::fence_async_smem();  // generic-proxy strip writes -> the MMA (async proxy)
       __syncwarp();
       if (lane == 0) {
+        if (tid == 32) trace_ev(A, it, 5);
         tc::mbar_arrive(&a_full[buf]);
         tc::mbar_arrive(&raw_empty[slot]);
       }
@@ -440,6 +451,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
       wait_x(A.exp, &mma_done[buf], (uint32_t)((it >> 1) & 1));
+      if (tid == 6 * 32) trace_ev(A, it, 6);
       __syncwarp();
       tc::fence_after();
       const uint32_t acc_base = lane_base + (DB ? (uint32_t)(buf * N) : 0u);
@@ -490,6 +502,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       }
       tc::fence_before();
       __syncwarp();
+      if (tid == 6 * 32) trace_ev(A, it, 7);
       if (lane == 0) tc::mbar_arrive(&acc_empty[DB ? buf : 0]);  // TMEM may be overwritten by later MMAs
       if (A.y != nullptr && in)
         A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;

@@ -16,8 +16,10 @@ bnn.set_option("streams", 1)
 exps = sys.argv[1:] or ["0", "1", "2", "4", "8", "6", "10", "12", "0"]
 for a in exps:  # "d<bits>": the same with double-buffered TMEM accumulators (first_db = 1)
     db = a.startswith("d")
-    e = int(a.lstrip("d"))
+    fp4 = a.startswith("f")
+    e = int(a.lstrip("df"))
     bnn.set_option("first_db", 1 if db else 0)
+    bnn.set_option("first_fp4", 1 if fp4 else 0)
     bnn.set_option("first_exp", e)
     for _ in range(3):
         net.forward(x, lg, cls)
@@ -27,5 +29,7 @@ for a in exps:  # "d<bits>": the same with double-buffered TMEM accumulators (fi
         net.forward(x, lg, cls)
     ms, cnt = net.profile_read()
     net.profile(False)
-    print("db=%d first_exp=%2d  conv1 %.4f ms/launch  (launches %d)" % (db, e, ms[1] / cnt[1], cnt[1]), flush=True)
+    print("fp4=%d db=%d first_exp=%2d  conv1 %.4f ms/launch  (launches %d)" % (fp4, db, e, ms[1] / cnt[1], cnt[1]), flush=True)
 bnn.set_option("first_exp", 0)
+bnn.set_option("first_fp4", 0)
+bnn.set_option("first_db", 1)
