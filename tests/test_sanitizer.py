@@ -1,0 +1,27 @@
+"""compute-sanitizer over every kernel family (SURVEY §4 test layer 4, §5 race detection): memcheck,
+racecheck (shared-memory hazards), synccheck (barrier misuse) and initcheck (reads of uninitialised
+device memory, e.g. pad bits) on small forward passes (tools/sanitize_cases.py)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer(cuda, tool):
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([cs, "--tool", tool, "--print-limit", "10", "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_cases.py")], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize cases done" in out, out[-4000:]
+    summary = "RACECHECK SUMMARY: 0 hazards" if tool == "racecheck" else "ERROR SUMMARY: 0 errors"
+    assert summary in out, out[-4000:]
