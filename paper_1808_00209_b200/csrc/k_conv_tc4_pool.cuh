@@ -31,7 +31,10 @@ struct ConvTc4PoolCfg {
   static constexpr int KS = K + 1;                 // window rows / columns
   static constexpr int SP = KS / 2;                // row pairs per MMA column
   static constexpr int NMMA = SP * KS;
-  static constexpr uint32_t ROWB = CH * 16, PLANE = IR * ROWB;
+  // PLANE: one parity plane + 64 B, so a loader quarter-warp's 16-byte stores to the even (plane 0)
+  // and odd (plane 1) columns of a row hit disjoint banks (an unpadded plane is a multiple of 128 B:
+  // every STS.128 was a 2-way conflict, ncu)
+  static constexpr uint32_t ROWB = CH * 16, PLANE = IR * ROWB + 64;
   static constexpr uint32_t A_BYTES = 2 * PLANE;
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
   static constexpr uint32_t TMEM_COLS = 256;       // N accumulator columns + block scales
