@@ -122,9 +122,10 @@ BNN_API int bnn_set_option(const char* key, int value);
 
 /* Tracing (diagnostics, not the hot path): registers a DEVICE buffer of `cap` uint64 (NULL / 0
  * disables).  While set, the pool-in-N TMA first-layer kernel records, for CTA (0,0), the SM clock
- * of 8 role events per tile iteration it at buf[8 * it + ev] (ev 0/1/2: MMA issuer after the A-ready
- * wait / before issuing / after commit; 3/4/5: builder warp after the raw-box wait / after the A-buffer-free
- * wait / at A ready; 6/7: epilogue after the accumulator-ready wait / at accumulator release).
+ * of 16 role events per tile iteration it at buf[16 * it + ev]: 0/1/2 MMA issuer after the A-ready
+ * wait / before issuing / after commit; 3-7 builder warps 1-5 at A ready; 8-11 epilogue warps after
+ * the accumulator-ready wait; 12 builder warp 1 after the A-buffer-free wait; 13 epilogue warp at
+ * accumulator release.
  * Process-wide; not thread-safe against concurrent launches.  Recording is compiled only into the
  * diagnostics build (`python -m paper_1808_00209_b200._build --trace` -> libbnn_trace.so); the
  * production library returns BNN_E_UNSUPPORTED for a non-NULL buffer.  Errors: BNN_E_ARG. */

@@ -40,12 +40,12 @@ struct ConvArgs {
   int trace_cap;
 };
 
-// Role timestamp of tile iteration `it`, event `ev` (< 8) of CTA (0, 0), SM clock (bnn_set_trace)
+// Role timestamp of tile iteration `it`, event `ev` (< 16) of CTA (0, 0), SM clock (bnn_set_trace)
 template <typename Args>
 BNN_DEV void trace_ev(const Args& A, int it, int ev) {
 #ifdef BNN_TRACE
-  if (A.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it * 8 + ev < A.trace_cap)
-    A.trace[it * 8 + ev] = clock64();
+  if (A.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && it * 16 + ev < A.trace_cap)
+    A.trace[it * 16 + ev] = clock64();
 #endif
 }
 

@@ -340,9 +340,8 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
       wait_x(A.exp, &raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
-      if (tid == 32) trace_ev(A, it, 3);
       if (it >= 2) wait_x(A.exp, &mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
-      if (tid == 32) trace_ev(A, it, 4);
+      if (tid == 32) trace_ev(A, it, 12);
       if (bt < C::GROUPS && !(A.exp & 4)) {
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
@@ -423,7 +422,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       tc::fence_async_smem();  // generic-proxy strip writes -> the MMA (async proxy)
       __syncwarp();
       if (lane == 0) {
-        if (tid == 32) trace_ev(A, it, 5);
+        trace_ev(A, it, 2 + warp);  // builder warps 1-5 -> events 3-7
         tc::mbar_arrive(&a_full[buf]);
         tc::mbar_arrive(&raw_empty[slot]);
       }
@@ -451,7 +450,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
       wait_x(A.exp, &mma_done[buf], (uint32_t)((it >> 1) & 1));
-      if (tid == 6 * 32) trace_ev(A, it, 6);
+      if (lane == 0) trace_ev(A, it, 2 + warp);  // epilogue warps 6-9 -> events 8-11
       __syncwarp();
       tc::fence_after();
       const uint32_t acc_base = lane_base + (DB ? (uint32_t)(buf * N) : 0u);
@@ -476,7 +475,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
             }
           }
       }
-      uint32_t neg = 0;
+      uint32_t neg = 0, negp[4] = {0u, 0u, 0u, 0u};
       if (!(A.exp & 2))
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
@@ -498,11 +497,15 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         tc::tmem_ld16(acc_base + (uint32_t)(3 * NT + cb), c);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
+        for (int k = 0; k < 16; ++k) {  // 4 independent 8-channel shift chains (ILP), merged below
+          uint32_t& nk = negp[(cb + k) >> 3];
+          nk = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), nk, 1);
+        }
       }
+      neg = (negp[0] << 24) | (negp[1] << 16) | (negp[2] << 8) | negp[3];
       tc::fence_before();
       __syncwarp();
-      if (tid == 6 * 32) trace_ev(A, it, 7);
+      if (tid == 6 * 32) trace_ev(A, it, 13);
       if (lane == 0) tc::mbar_arrive(&acc_empty[DB ? buf : 0]);  // TMEM may be overwritten by later MMAs
       if (A.y != nullptr && in)
         A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;

@@ -289,7 +289,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
             }
           }
       }
-      uint32_t neg = 0;
+      uint32_t neg = 0, negp[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
         int a[16], b[16], c[16];
@@ -302,8 +302,12 @@ conv_tc4_pool_kernel(const ConvArgs A) {
         tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 16; ++k) neg = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), neg, 1);
+        for (int k = 0; k < 16; ++k) {  // 4 independent 8-channel shift chains (ILP), merged below
+          uint32_t& nk = negp[(cb + k) >> 3];
+          nk = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), nk, 1);
+        }
       }
+      neg = (negp[0] << 24) | (negp[1] << 16) | (negp[2] << 8) | negp[3];
       // start values for the next tile's accumulation
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
