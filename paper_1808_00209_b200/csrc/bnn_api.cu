@@ -80,6 +80,7 @@ int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (wrong
 int g_opt_first_tma = 1;
 unsigned long long* g_trace = nullptr;  // bnn_set_trace
 int g_trace_cap = 0;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
+int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
@@ -668,6 +669,16 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k, int pool) {
 // Dense layers with a real batch and a long reduction run on the tensor cores (kind::mxf4).
 bool use_dense_tc(int n, int64_t dw) { return g_opt_dense_tc && n >= 256 && dw >= 32 && (dw % 4) == 0; }
 
+// K-split factor of dense_tc4_kernel (grid.z): split when the tile grid leaves SMs idle (FC1 at 8192
+// images: 64 tiles -> 2); each split then needs at least 4 stages of 16 words
+int dense_ks(int n, int l, int64_t dw) {
+  if (!use_dense_tc(n, dw) || !g_opt_dense_ksplit) return 1;
+  const int nt = l > 128 ? 256 : 128, groups = (l + nt - 1) / nt;
+  const int ctas = std::min((n + 127) / 128, num_sms()) * groups, nstage = (int)((dw + 15) / 16);
+  if (2 * ctas > num_sms() || nstage < 8) return 1;
+  return std::max(1, std::min(std::min(num_sms() / ctas, nstage / 4), 4));
+}
+
 bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,
                         const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, cudaStream_t s) {
   if (n == 0) return BNN_OK;
@@ -682,16 +693,34 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     const bool wide = l > 128;
     A.cls = (l <= (wide ? 256 : 128)) ? cls : nullptr;
     const int ntiles = (n + 127) / 128;
-    auto launch = [&](auto kfn, uint32_t smem, int nt) {
+    const int nt = wide ? 256 : 128, groups = (l + nt - 1) / nt;
+    A.ks = dense_ks(n, l, A.dw);
+    float* part = nullptr;
+    if (A.ks > 1) {
+      const size_t bytes = (size_t)A.ks * ntiles * 128 * groups * nt * sizeof(float);
+      if (cudaMallocAsync(reinterpret_cast<void**>(&part), bytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        A.ks = 1;
+        part = nullptr;
+      }
+      A.part = part;
+    }
+    if (A.ks > 1) A.cls = cls;  // the reduction kernel takes the argmax over all l
+    auto launch = [&](auto kfn, uint32_t smem) {
       static int set_nt128 = 0, set_nt256 = 0;
       int& flag = (nt == 128) ? set_nt128 : set_nt256;
       if (!flag) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); flag = 1; }
-      dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)((l + nt - 1) / nt));
+      dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)groups, (unsigned)A.ks);
       launch_pdl(kfn, grid, dim3(256), smem, s, A);
     };
-    if (wide) launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM, 256);
-    else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM, 128);
+    if (wide) launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM);
+    else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM);
     st = check_launch("dense_tc4_kernel");
+    if (st == BNN_OK && A.ks > 1) {
+      launch_pdl(dense_tc4_reduce_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, s, A, groups * nt, ntiles * 128);
+      st = check_launch("dense_tc4_reduce_kernel");
+    }
+    if (part != nullptr) cudaFreeAsync(part, s);
     if (st != BNN_OK) return st;
     if (cls != nullptr && A.cls == nullptr) {
       launch_pdl(argmax_kernel, dim3(grid_for((int64_t)n * 32, 256)), dim3(256), 0, s, (const int32_t*)acc, n, l, cls);
@@ -746,6 +775,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
   if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }
+  if (strcmp(key, "dense_ksplit") == 0) { g_opt_dense_ksplit = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
@@ -1102,6 +1132,8 @@ int launches_per_chunk(const bnn_net* net, bool want_cls, int nb) {
   if (use_fused_small(net, nb)) return 1;
   int n = (net->mode != BNN_MODE_NONE && !fused_input(net) ? 1 : 0) + (int)net->L.size();
   if (want_cls && net->L.back().l > 32) n += 1;
+  for (const LayerPlan& P : net->L)  // K-split dense layers add their reduction kernel
+    if (P.kind == 2 && dense_ks(nb, P.l, (P.d + 31) / 32) > 1) n += 1;
   return n;
 }
 

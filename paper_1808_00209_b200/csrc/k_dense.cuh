@@ -23,6 +23,8 @@ struct DenseArgs {
   int32_t* cls;   // [n] or null (only when l <= 32: one group holds all outputs)
   int n, l, lw;
   int64_t d, dw;
+  int ks;        // dense_tc4: K split over gridDim.z (1 = none)
+  float* part;   // ks > 1: partial sums [ks][ntiles * 128][gridDim.y * NT] (stream-ordered scratch)
 };
 
 template <int PI, int NWARP, int DC>

@@ -73,6 +73,11 @@ dense_tc4_kernel(const DenseArgs A) {
   const int nstage = (dw + KC - 1) / KC;
   const int ntiles = (A.n + 127) / 128;
   const int dvalid_last = (int)(A.d - (int64_t)(dw - 1) * 32);  // valid bits of the last word
+  // K split (A.ks > 1, grid.z): this CTA accumulates stages [st0, st1) and publishes fp32 partial sums
+  // (exact integers) for dense_tc4_reduce_kernel; with 64 tiles per 8192-image chunk the unsplit grid
+  // leaves most SMs idle
+  const int z = (int)blockIdx.z;
+  const int st0 = z * nstage / A.ks, st1 = (z + 1) * nstage / A.ks;
 
   // Stage loads are 16-byte vectors (4 words of one image / one output row; requires dw % 4 == 0)
   // prefetched into registers right after the previous stage's MMAs are issued.
@@ -122,10 +127,10 @@ dense_tc4_kernel(const DenseArgs A) {
   uint32_t stage_uses = 0;  // global stage counter (for mbarrier parity)
   uint32_t acc_uses = 0;
   griddep_wait();  // activations of the predecessor layer
-  if ((int)blockIdx.x < ntiles) load_stage((int)blockIdx.x * 128, 0);
+  if ((int)blockIdx.x < ntiles) load_stage((int)blockIdx.x * 128, st0);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int img0 = tile * 128;
-    for (int st = 0; st < nstage; ++st, ++stage_uses) {
+    for (int st = st0; st < st1; ++st, ++stage_uses) {
       const int s = stage_uses & 1;
       if (stage_uses >= 2) tc::mbar_wait(&bar_stage[s], ((stage_uses - 2) >> 1) & 1);
       uint8_t* a = sA + s * C::A_BYTES;
@@ -153,20 +158,34 @@ dense_tc4_kernel(const DenseArgs A) {
 #pragma unroll
         for (int i = 0; i < KC / 2; ++i) {
           tc::mma_mxf4(tmem, ad0 + (uint64_t)(2 * i * 128), bd0 + (uint64_t)(2 * i * NT), idesc, sfa, sfb,
-                       (st > 0 || i > 0) ? 1u : 0u);
+                       (st > st0 || i > 0) ? 1u : 0u);
         }
         tc::commit(&bar_stage[s]);
-        if (st == nstage - 1) tc::commit(&bar_acc);
+        if (st == st1 - 1) tc::commit(&bar_acc);
       }
       // prefetch the next stage (next tile's first stage after the last one)
-      if (st + 1 < nstage) load_stage(img0, st + 1);
-      else if (tile + (int)gridDim.x < ntiles) load_stage((tile + (int)gridDim.x) * 128, 0);
+      if (st + 1 < st1) load_stage(img0, st + 1);
+      else if (tile + (int)gridDim.x < ntiles) load_stage((tile + (int)gridDim.x) * 128, st0);
     }
     // epilogue: warps 0-3, thread = image
     tc::mbar_wait(&bar_acc, acc_uses & 1);
     ++acc_uses;
     tc::fence_after();
-    if (warp < 4) {
+    if (A.ks > 1 && warp < 4) {  // partial sums of this K range, thread = image, 32 columns per load
+      const int img = img0 + warp * 32 + lane;
+      const int LP = (int)gridDim.y * NT;
+      float* dst = A.part + ((int64_t)z * ntiles * 128 + img) * LP + g * NT;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT && g * NT + c0 < A.l; c0 += 32) {
+        int v[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)
+          __stcg(reinterpret_cast<float4*>(dst + c0 + c), make_float4(__int_as_float(v[c]), __int_as_float(v[c + 1]),
+                                                                       __int_as_float(v[c + 2]), __int_as_float(v[c + 3])));
+      }
+    } else if (A.ks == 1 && warp < 4) {
       const int img = img0 + warp * 32 + lane;
       const bool img_ok = img < A.n;
       float best = -3.0e38f;
@@ -207,6 +226,45 @@ dense_tc4_kernel(const DenseArgs A) {
   }
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// Reduction + epilogue of a K-split dense_tc4_kernel: one warp per image, lane = output column of a
+// 32-column chunk (coalesced partial loads); sums the ks partials (exact: integers < 2^24 in fp32),
+// then the fused epilogue's threshold (bit = acc > thr, as a ballot: lane c -> bit 31 - c, MSB-first),
+// flips, acc output and first-maximum argmax (R19) over all l outputs.
+__global__ void __launch_bounds__(256) dense_tc4_reduce_kernel(const DenseArgs A, int LP, int npad) {
+  griddep_launch();
+  griddep_wait();
+  const int lane = threadIdx.x & 31;
+  const int img = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (img >= A.n) return;
+  float best = -3.0e38f;
+  int besti = INT_MAX;
+  for (int c0 = 0; c0 < A.l; c0 += 32) {
+    const int o = c0 + lane;
+    const bool ok = o < A.l;
+    float f = 0.f;
+    if (ok)
+      for (int z = 0; z < A.ks; ++z) f += __ldcg(A.part + ((int64_t)z * npad + img) * LP + o);
+    const int t = (ok && A.thr != nullptr) ? max(-(1 << 24), min(1 << 24, A.thr[o])) : 0;
+    bool bit = ok && f > (float)t;
+    if (ok && A.flip != nullptr && A.flip[o] != 0) bit = !bit;
+    const uint32_t word = __brev(__ballot_sync(0xFFFFFFFFu, bit));
+    if (A.y != nullptr && lane == 0) A.y[(int64_t)img * A.lw + (c0 >> 5)] = word;
+    if (ok) {
+      if (A.acc != nullptr) A.acc[(int64_t)img * A.l + o] = (int32_t)f;
+      if (f > best) { best = f; besti = o; }
+    }
+  }
+  if (A.cls != nullptr) {
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {  // first maximum wins (R19): larger value, then lower index
+      const float ov = __shfl_xor_sync(0xFFFFFFFFu, best, sh);
+      const int oi = __shfl_xor_sync(0xFFFFFFFFu, besti, sh);
+      if (ov > best || (ov == best && oi < besti)) { best = ov; besti = oi; }
+    }
+    if (lane == 0) A.cls[img] = besti;
+  }
 }
 
 }  // namespace bnn

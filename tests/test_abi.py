@@ -95,7 +95,7 @@ def test_validation_errors(L):
     doc = hdr[hdr.index("Process-wide tuning"):hdr.index("BNN_API int bnn_set_option")]
     keys = re.findall(r'\*\s+"(\w+)"', doc)
     assert {"conv_algo", "conv_tc", "conv_tc_fp4", "conv_pool_tc", "first_tma", "pdl"} <= set(keys)
-    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 16, "fused_max_n": 0, "alg1": 0, "first_fp4": 0, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1}
+    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 16, "fused_max_n": 0, "alg1": 0, "first_fp4": 0, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1, "dense_ksplit": 1, "first_exp": 0}
     for k in keys:
         assert L.bnn_set_option(k.encode(), defaults.get(k, 1)) == 0, k
     assert L.bnn_forward_launches(None, 5) == 0

@@ -304,20 +304,26 @@ def test_dense(cuda, orc, n, d, l):
 
 
 @pytest.mark.parametrize("n,d,l,flip", [(300, 18432, 100, False), (256, 2040, 10, True), (400, 1024, 300, True),
-                                        (129, 4096, 129, False)])
-def test_dense_tensor_core(cuda, orc, n, d, l, flip):
+                                        (129, 4096, 129, False), (8192, 18432, 100, True)])
+@pytest.mark.parametrize("ksplit", [1, 0])
+def test_dense_tensor_core(cuda, orc, n, d, l, flip, ksplit):
     """Large-batch dense on tcgen05 (kind::mxf4): ragged image tiles, d with a partial last word,
-    l > 256 (two output groups), thresholds + flips, fused argmax (l <= NT) or the argmax kernel."""
+    l > 256 (two output groups), thresholds + flips, fused argmax (l <= NT) or the argmax kernel;
+    ksplit = 1: K split over grid.z + the reduction kernel where the tile grid is small (FC1 shapes)."""
     xs = synth.pm1((n, d), 95 + d)
     ws = synth.pm1((l, d), 96 + l)
     t = synth.int_thresholds(l, 97, -40, 41)
     f = synth.flips(l, 98) if flip else None
     xp = cuda.pack(dev(xs).view(n, 1, 1, d)).view(n, -1)
-    y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None if f is None else dev(f),
-                             want_acc=True, want_cls=True)
-    torch.cuda.synchronize()
+    try:
+        cuda.set_option("dense_ksplit", ksplit)
+        y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None if f is None else dev(f),
+                                 want_acc=True, want_cls=True)
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("dense_ksplit", 1)
     acc, y, cls = acc.cpu().numpy(), u32(y), cls.cpu().numpy()
-    for i in range(0, n, 7):
+    for i in range(0, n, 7 if n < 1000 else 331):
         ra = orc.dense(xs[i].numpy(), ws.numpy())
         assert np.array_equal(acc[i], ra)
         b = orc.binarize(ra[None], t.numpy(), None if f is None else f.numpy())[0]
@@ -535,7 +541,7 @@ def test_forward_host_equals_forward(cuda):
     torch.cuda.synchronize()
     lg_h, cls_h = net.forward_host(imgs.pin_memory())
     assert torch.equal(lg_h, lg_d.cpu()) and torch.equal(cls_h, cls_d.cpu())
-    assert cuda.forward_launches(net, 9000) == 3 * 5
+    assert cuda.forward_launches(net, 9000) == 3 * 6  # pack-fused conv1, conv2, FC1 (+ K-split reduction), FC2, FC3
 
 
 @pytest.mark.parametrize("fused", [8, 0])
