@@ -67,6 +67,24 @@ int num_sms() {
 }
 
 // tuning / test knobs (bnn_set_option)
+// Stream-ordered scratch (cudaMallocAsync on the launch stream, freed with cudaFreeAsync after the
+// consumer) from the device's default pool, which keeps freed blocks (release threshold = max) so a
+// steady-state allocation is a pool hit, not a new mapping.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static int init_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (init_dev != dev) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    init_dev = dev;
+  }
+  return cudaMallocAsync(p, bytes, s);
+}
+
 int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap conv
 int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
 int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
@@ -447,7 +465,7 @@ bnn_status launch_conv_tc4_big_t(ConvArgs A, cudaStream_t s) {
   uint8_t* img = nullptr;
   const int nstage = (A.cw + CG - 1) / CG;
   if (g_opt_big_img && A.bimg == nullptr && A.total_tiles > (int64_t)gx) {
-    if (cudaMallocAsync(&img, (size_t)groups * nstage * C::B_BYTES, s) == cudaSuccess) {
+    if (scratch_alloc(reinterpret_cast<void**>(&img), (size_t)groups * nstage * C::B_BYTES, s) == cudaSuccess) {
       prep_tc4_big_kernel<K, CG, NT><<<dim3((unsigned)nstage, (unsigned)groups), 256, 0, s>>>(A, img);
       A.bimg = img;
     } else {
@@ -698,7 +716,7 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     float* part = nullptr;
     if (A.ks > 1) {
       const size_t bytes = (size_t)A.ks * ntiles * 128 * groups * nt * sizeof(float);
-      if (cudaMallocAsync(reinterpret_cast<void**>(&part), bytes, s) != cudaSuccess) {
+      if (scratch_alloc(reinterpret_cast<void**>(&part), bytes, s) != cudaSuccess) {
         cudaGetLastError();
         A.ks = 1;
         part = nullptr;
