@@ -376,16 +376,21 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   return check_launch("conv_first_tma_pool_kernel");
 }
 
+// The TMA-fed pooled first layer on a u8 [n, H, W, 3] image (k in {3, 5}), operand type / TMEM
+// buffering per the first_fp4 / first_db options.  A.c_in may be 1 (THRESH_GRAY via luma_u8img4_kernel:
+// channels 1-2 get zero weights).
+bnn_status dispatch_first_tma(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  if (g_opt_first_fp4) return k == 5 ? launch_conv_first_tma_t<5, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, true>(A, xu8, T, s);
+  if (g_opt_first_db) return k == 5 ? launch_conv_first_tma_t<5, false, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, false, true>(A, xu8, T, s);
+  return k == 5 ? launch_conv_first_tma_t<5, false>(A, xu8, T, s) : launch_conv_first_tma_t<3, false>(A, xu8, T, s);
+}
+
 template <int SRC>
 bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   const bool wide = A.c_out > 32;
   const int c = A.c_in;
   if constexpr (SRC == kSrcThresh) {
-    if (A.n > 0 && use_first_tma(A, k, xu8)) {
-      if (g_opt_first_fp4) return k == 5 ? launch_conv_first_tma_t<5, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, true>(A, xu8, T, s);
-      if (g_opt_first_db) return k == 5 ? launch_conv_first_tma_t<5, false, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, false, true>(A, xu8, T, s);
-      return k == 5 ? launch_conv_first_tma_t<5, false>(A, xu8, T, s) : launch_conv_first_tma_t<3, false>(A, xu8, T, s);
-    }
+    if (A.n > 0 && use_first_tma(A, k, xu8)) return dispatch_first_tma(k, A, xu8, T, s);
   }
   if (A.pool == 2 && g_opt_first_pool_tc) {
 #define BNN_FTCP(KK, CC)                                                                          \
@@ -1039,6 +1044,17 @@ bool fused_input(const bnn_net* net) {
   return use_first_tc(net->c, net->L[0].k, kSrcThresh) || use_first_lp(net->c, net->L[0].k) || use_strip(net->c, net->L[0].k);
 }
 
+// THRESH_GRAY / LBP nets whose first layer fits the TMA-fed pooled kernel: luma_u8img4_kernel writes a
+// 0/1 u8 image into the packed-input workspace and the TMA kernel reads it with threshold x > 0.
+bool use_luma_tma(const bnn_net* net) {
+  if (net->mode != BNN_THRESH_GRAY && net->mode != BNN_LBP) return false;
+  if (net->in_dt != BNN_U8 || net->c != 3 || net->L[0].kind != 1) return false;
+  const LayerPlan& P = net->L[0];
+  return g_opt_first_tma && g_opt_first_pool_tc && g_opt_conv_algo == 0 && P.pool == 2 && (P.k == 3 || P.k == 5) &&
+         (P.c_in == 1 || P.c_in == 3) && (P.W * 3) % 16 == 0 && (net->w % 4) == 0 && tma_encoder() != nullptr &&
+         net->packed_in_words * 4 >= (int64_t)P.H * P.W * 3;
+}
+
 // Small batches of a vehicle-shaped net run as one cooperative kernel (k_fused_small.cuh).
 bool use_fused_small(const bnn_net* net, int nb) {
   if (nb < 1 || nb > g_opt_fused_max_n || net->fused_ctr == nullptr || net->fused_w1 == nullptr) return false;
@@ -1105,6 +1121,27 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     else
       st = small ? dispatch_conv_strip<4, 1, true>(P.k, A, (const uint8_t*)images, T, s)
                  : dispatch_conv_strip<4, 2, true>(P.k, A, (const uint8_t*)images, T, s);
+    if (st != BNN_OK) return st;
+    cur = net->buf[0];
+    cur_dt = BNN_BITS;
+    first = 1;
+  } else if (use_luma_tma(net)) {
+    {
+      ProfScope ps(net, 0, s);
+      const int64_t npix = (int64_t)nb * net->h * net->w;
+      luma_u8img4_kernel<<<grid_for(npix / 4, 256), 256, 0, s>>>((const uint8_t*)images, nb, net->h, net->w, net->mode,
+                                                                 net->T, reinterpret_cast<uint8_t*>(net->packed_in));
+      bnn_status st = check_launch("luma_u8img4_kernel");
+      if (st != BNN_OK) return st;
+    }
+    const LayerPlan& P = net->L[0];
+    ProfScope ps(net, 1, s);
+    ConvArgs A{};
+    A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.y = net->buf[0];
+    A.n = nb; A.H = P.H; A.W = P.W; A.cw = 1; A.c_in = P.c_in; A.c_out = P.c_out;
+    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool;
+    A.bimg = (P.bimg_fp4 == (g_opt_first_fp4 ? 1 : 0)) ? P.bimg : nullptr;
+    bnn_status st = dispatch_first_tma(P.k, A, reinterpret_cast<const uint8_t*>(net->packed_in), nullptr, s);
     if (st != BNN_OK) return st;
     cur = net->buf[0];
     cur_dt = BNN_BITS;
@@ -1250,7 +1287,8 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
     ConvArgs A{};
     A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.c_in = P.c_in; A.c_out = P.c_out;
     const int groups = (P.c_out + 31) / 32;
-    const bool first_u8 = i == 0 && net->in_dt == BNN_U8 && net->c == 3 && (net->mode == BNN_SIGN || net->mode == BNN_THRESH_RGB);
+    const bool first_u8 = i == 0 && net->in_dt == BNN_U8 && net->c == 3 &&
+                          (net->mode == BNN_SIGN || net->mode == BNN_THRESH_RGB || use_luma_tma(net));
     if (first_u8) {
       const bool fp4 = g_opt_first_fp4 != 0;
       const size_t bb = P.k == 5 ? (fp4 ? FirstTmaCfg<5, true>::B_BYTES : FirstTmaCfg<5, false>::B_BYTES)
@@ -1553,6 +1591,7 @@ const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
     if (use_dense_tc(nn, (P.d + 31) / 32)) return "dense_tc4_kernel";
     return nn <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
   }
+  if (layer == 0 && use_luma_tma(net)) return "conv_first_tma_pool_kernel";
   if (layer == 0 && fused_input(net)) {
     if (use_first_tc(P.c_in, P.k, kSrcThresh)) {
       if (P.pool != 2 || !g_opt_first_pool_tc) return "conv_first_tc_kernel";

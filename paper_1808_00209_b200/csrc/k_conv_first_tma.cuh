@@ -160,7 +160,7 @@ BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, i
         int v = 0;
         if (e < C::SB) {
           const int tap = e / CIN, c = e % CIN, kx = tap - dx;
-          if (ok && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+          if (ok && c < A.c_in && ky >= 0 && ky < K && kx >= 0 && kx < K) {
             const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
             v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
             if (f) v = -v;
@@ -176,7 +176,7 @@ BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, i
       for (int e = 0; e < 16; ++e) {
         const int el = kc * 16 + e, tap = el / CIN, c = el % CIN, kx = tap - dx;
         int v = 0;
-        if (ok && el < C::SB && ky >= 0 && ky < K && kx >= 0 && kx < K) {
+        if (ok && el < C::SB && c < A.c_in && ky >= 0 && ky < K && kx >= 0 && kx < K) {  // c >= c_in: zero (GRAY)
           const uint32_t wv = __ldg(A.wt + ((int64_t)o * K + ky) * K + kx);
           v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
           if (f) v = -v;

@@ -91,4 +91,66 @@ __global__ void pack_luma_kernel(const uint8_t* __restrict__ x, int n, int h, in
   }
 }
 
+// THRESH_GRAY and LBP feeding the TMA first layer: the same bits as pack_luma_kernel, written as a
+// u8 [n, h, w, 3] image of 0 (-1) / 1 (+1) bytes that conv_first_tma_pool_kernel thresholds with
+// x > 0 (an out-of-image byte 0 is the -1 padding, R4).  GRAY: channel 0 = Y > -T, channels 1-2 = 0
+// (their weights are zero for a c_in = 1 layer); LBP: channel j = n_{3j} > Y (R16, replicate border).
+// Four pixels of a row per thread (w % 4 == 0, 4-byte aligned image): aligned word loads of the
+// centre row (+ the right neighbour) and, for LBP, of the rows above / below (+ the left neighbour),
+// three word stores of the 12 output bytes -- 27,648 B per 96 x 96 image instead of 36,864 B of
+// packed words.
+BNN_DEV int luma3(uint32_t b0, uint32_t b1, uint32_t b2) { return (299 * (int)b0 + 587 * (int)b1 + 114 * (int)b2 + 500) / 1000; }
+BNN_DEV uint32_t byte_of(const uint32_t (&v)[4], int i) { return (v[i >> 2] >> (8 * (i & 3))) & 0xFFu; }
+
+__global__ void luma_u8img4_kernel(const uint8_t* __restrict__ x, int n, int h, int w, int mode,
+                                   const float* __restrict__ Tt, uint8_t* __restrict__ y) {
+  const int64_t ngroups = (int64_t)n * h * (w >> 2);
+  const float t = (mode == kThreshGray) ? -Tt[0] : 0.f;
+  const int wg = w >> 2;
+  for (int64_t q = gtid(); q < ngroups; q += gstride()) {
+    const int64_t row = q / wg;  // image * h + yy
+    const int x0 = (int)(q - row * wg) * 4;
+    const int64_t img = row / h;
+    const int yy = (int)(row - img * h);
+    const uint8_t* base = x + img * (int64_t)h * w * 3;
+    const uint32_t* rc = reinterpret_cast<const uint32_t*>(base + ((int64_t)yy * w + x0) * 3);
+    uint32_t c[4] = {rc[0], rc[1], rc[2], 0u};  // pixels x0..x0+3 (12 bytes)
+    if (x0 + 4 < w) c[3] = rc[3];               // bytes 12..14: pixel x0+4
+    int Y[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) Y[i] = luma3(byte_of(c, 3 * i), byte_of(c, 3 * i + 1), byte_of(c, 3 * i + 2));
+    uint32_t o[3] = {0u, 0u, 0u};
+    if (mode == kThreshGray) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[(3 * i) >> 2] |= (uint32_t)((float)Y[i] > t) << (8 * ((3 * i) & 3));
+    } else {
+      Y[4] = (x0 + 4 < w) ? luma3(byte_of(c, 12), byte_of(c, 13), byte_of(c, 14)) : Y[3];  // R of the last
+      int U[5], D[5];  // rows above / below at x0-1 .. x0+3 (clamped rows and columns)
+      const int ym = max(yy - 1, 0), yp = min(yy + 1, h - 1);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint8_t* rb = base + ((int64_t)(r == 0 ? ym : yp) * w + x0) * 3;
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rb);
+        uint32_t v[4] = {x0 > 0 ? rw[-1] : 0u, rw[0], rw[1], rw[2]};  // bytes of pixels x0-1 (1..3) .. x0+3
+        int* L = r == 0 ? U : D;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) L[i + 1] = luma3(byte_of(v, 4 + 3 * i), byte_of(v, 5 + 3 * i), byte_of(v, 6 + 3 * i));
+        L[0] = x0 > 0 ? luma3(byte_of(v, 1), byte_of(v, 2), byte_of(v, 3)) : L[1];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // clockwise from top-left: n0 = (-1,-1), n3 = (0,+1), n6 = (+1,-1)   (R16)
+        const uint32_t b0 = U[i] > Y[i], b1 = Y[i + 1] > Y[i], b2 = D[i] > Y[i];
+        o[(3 * i) >> 2] |= b0 << (8 * ((3 * i) & 3));
+        o[(3 * i + 1) >> 2] |= b1 << (8 * ((3 * i + 1) & 3));
+        o[(3 * i + 2) >> 2] |= b2 << (8 * ((3 * i + 2) & 3));
+      }
+    }
+    uint32_t* yo = reinterpret_cast<uint32_t*>(y + ((img * h + yy) * (int64_t)w + x0) * 3);
+    yo[0] = o[0];
+    yo[1] = o[1];
+    yo[2] = o[2];
+  }
+}
+
 }  // namespace bnn

@@ -636,3 +636,37 @@ def test_forward_scores_vehicle(cuda, orc, mode):
     _, s32, rcls = orc.affine(ref_logits, scale.numpy(), bias.numpy())
     assert np.array_equal(scores.cpu().numpy().view(np.uint32), s32.view(np.uint32))
     assert np.array_equal(cls.cpu().numpy(), rcls)
+
+
+# ------------------------------------------------------------------------------------ GRAY / LBP first layer
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("h,w,k,cout", [(32, 48, 5, 32), (18, 16, 3, 40), (34, 64, 5, 64)])
+@pytest.mark.parametrize("mode", [2, 3])
+def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, tma):
+    """THRESH_GRAY (c_in = 1: zero weights on the two dummy channels) and LBP through luma_u8img4_kernel
+    + the TMA-fed first layer (tma = 1) or the packed-bit path (tma = 0), with BN thresholds / flips on
+    the first layer, ragged tiles and channel groups, against the oracle."""
+    cin = 1 if mode == 2 else 3
+    tail = [dict(kind="conv", k=1, c_out=32, pool=1)] if cout % 32 else []
+    spec = dict(h=h, w=w, c=3, layers=[dict(kind="conv", k=k, c_out=cout, pool=2)] + tail + [dict(kind="dense", l=10)])
+    seed = 1900 + h + k + mode
+    layers = synth.make_weights(spec, mode, seed)
+    assert layers[0]["wt"].shape[-1] == cin
+    layers[0]["thr"] = synth.int_thresholds(cout, seed, -6, 7)
+    layers[0]["flip"] = synth.flips(cout, seed + 1)
+    dl = [dict(L, wt=cuda.pack_weights(dev(L["wt"]))) for L in layers]
+    dl[0]["thr"], dl[0]["flip"] = dev(layers[0]["thr"]), dev(layers[0]["flip"])
+    T = torch.tensor([-100.0]) if mode == 2 else None  # integer T: Y + T = 0 ties occur
+    imgs = synth.images(5, h, w, 3, seed + 2)
+    imgs[0, :3, :3] = 100
+    try:
+        cuda.set_option("first_tma", tma)
+        net = cuda.Net(h, w, 3, cuda.U8, mode, None if T is None else dev(T), dl, max_batch=8)
+        if tma:
+            assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
+        lg, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("first_tma", 1)
+    ref_l, ref_c = oracle_net(orc, spec, mode, layers, T).forward(imgs.numpy(), threads=5)
+    assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
