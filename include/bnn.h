@@ -98,6 +98,8 @@ BNN_API int bnn_version(void);
  *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
  *   "first_fp4"     0 (default): that kernel's operands are int8 (kind::i8); 1: e2m1 (kind::mxf4).
+ *   "first_real_tma" 1 (default): pooled real-u8 first layers (mode NONE, c_in = 3) use the same TMA
+ *                   kernel with the pixels as the unsigned int8 operand; 0: the register-staged kernel.
  *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);
  *                   0: one accumulator set (3 CTAs/SM).
  *   "first_exp"     0 (default).  Timing experiments on that kernel (tools/time_first_exp.py); any

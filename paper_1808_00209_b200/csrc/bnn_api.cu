@@ -96,6 +96,7 @@ int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind:
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
 int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (wrong results unless 0)
 int g_opt_first_tma = 1;
+int g_opt_first_real_tma = 1;  // 1: real u8 first layers (mode NONE) use the TMA kernel (u8 x +/-1 kind::i8)
 unsigned long long* g_trace = nullptr;  // bnn_set_trace
 int g_trace_cap = 0;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
@@ -344,10 +345,10 @@ bool use_first_tma(const ConvArgs& A, int k, const uint8_t* xu8) {
          aligned16(xu8) && tma_encoder() != nullptr;
 }
 
-template <int K, bool FP4, bool DB = false>
+template <int K, bool FP4, bool DB = false, bool REAL = false>
 bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   using C = FirstTmaCfg<K, FP4, DB>;
-  auto kfn = conv_first_tma_pool_kernel<K, FP4, DB>;
+  auto kfn = conv_first_tma_pool_kernel<K, FP4, DB, REAL>;
   constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
   static int occ = -1;
   if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
@@ -391,6 +392,14 @@ bnn_status dispatch_conv_first_tc(int k, const ConvArgs& A, const uint8_t* xu8, 
   const int c = A.c_in;
   if constexpr (SRC == kSrcThresh) {
     if (A.n > 0 && use_first_tma(A, k, xu8)) return dispatch_first_tma(k, A, xu8, T, s);
+  }
+  if constexpr (SRC == kSrcReal) {  // real u8 pixels (mode NONE): the TMA kernel with an unsigned A operand
+    if (A.n > 0 && g_opt_first_real_tma && use_first_tma(A, k, xu8)) {
+      if (g_opt_first_db) return k == 5 ? launch_conv_first_tma_t<5, false, true, true>(A, xu8, nullptr, s)
+                                        : launch_conv_first_tma_t<3, false, true, true>(A, xu8, nullptr, s);
+      return k == 5 ? launch_conv_first_tma_t<5, false, false, true>(A, xu8, nullptr, s)
+                    : launch_conv_first_tma_t<3, false, false, true>(A, xu8, nullptr, s);
+    }
   }
   if (A.pool == 2 && g_opt_first_pool_tc) {
 #define BNN_FTCP(KK, CC)                                                                          \
@@ -672,7 +681,12 @@ bnn_status launch_conv(const void* x, bnn_dtype x_dt, int n, int h, int w, int c
 
 // The kernel family launch_conv / the fused first layer pick (kept in step with the dispatch above).
 const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k, int pool) {
-  if (x_dt == BNN_U8) return use_first_tc(c_in, k, kSrcReal) ? "conv_first_tc_kernel" : "conv_real_u8_kernel";
+  if (x_dt == BNN_U8) {
+    if (!use_first_tc(c_in, k, kSrcReal)) return "conv_real_u8_kernel";
+    const bool tma = g_opt_first_real_tma && g_opt_first_tma && g_opt_first_pool_tc && pool == 2 && c_in == 3 &&
+                     (k == 3 || k == 5) && tma_encoder() != nullptr;  // (+ 16-byte row pitch, checked at launch)
+    return tma ? "conv_first_tma_pool_kernel" : "conv_first_tc_kernel";
+  }
   if (x_dt == BNN_F32) return "conv_real_f32_kernel";
   if (use_first_tc(c_in, k, kSrcBits)) return "conv_first_tc_kernel";
   if (use_first_lp(c_in, k)) return "conv_first_lp_kernel";
@@ -799,6 +813,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
   if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }
   if (strcmp(key, "dense_ksplit") == 0) { g_opt_dense_ksplit = value; return BNN_OK; }
+  if (strcmp(key, "first_real_tma") == 0) { g_opt_first_real_tma = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }

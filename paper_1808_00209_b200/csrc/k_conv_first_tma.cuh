@@ -107,9 +107,9 @@ BNN_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 // thr'+1 of output channel o: thr' = flip ? -t-1 : t, clamped to [-S_TOT-1, S_TOT] (the same
 // decisions: |acc| <= S_TOT); invalid channels get 1 (acc' = -1 -> bit 0)
-template <int K>
+template <int K, bool REAL = false>
 BNN_DEV int first_tma_bias(const ConvArgs& A, int o) {
-  constexpr int S_TOT = K * K * 3;
+  constexpr int S_TOT = K * K * 3 * (REAL ? 255 : 1);
   if (o >= A.c_out) return 1;
   const bool f = A.flip != nullptr && A.flip[o] != 0;
   int tt = A.thr != nullptr ? A.thr[o] : 0;
@@ -142,7 +142,9 @@ BNN_DEV int fp4_bias_part(int v, int k) {
 // chunk = one strip row): the bias is spread over the nibbles SB..31 of the strip rows (values in
 // {6, 4, 3, 2, 1}, all against -1).  Written by the kernel itself, or once per net by
 // prep_first_tma_kernel (then bulk-copied per CTA).
-template <int K, bool FP4>
+// REAL (mode NONE, u8 pixels as the unsigned A operand, zero padding R5): strip bytes SB and SB+1 are
+// A = 1 and A = 255, and B carries -(thr'+1) = r + 255 q there (|r| <= 127, |q| <= 75) in strip row 0.
+template <int K, bool FP4, bool REAL = false>
 BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, int step) {
   using C = FirstTmaCfg<K, FP4>;
   constexpr int N = C::N, NT = C::NT, CIN = C::CIN;
@@ -151,7 +153,7 @@ BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, i
     const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
     const bool ok = o < A.c_out;
     const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
-    const int bias = first_tma_bias<K>(A, o);
+    const int bias = first_tma_bias<K, REAL>(A, o);
     uint32_t w4[4] = {0u, 0u, 0u, 0u};
     if (FP4) {
       const int srow = 2 * mi + kc, ky = srow - dy;
@@ -181,7 +183,13 @@ BNN_DEV void stage_b_first_tma(const ConvArgs& A, int g, uint8_t* dst, int i0, i
           v = ((wv >> (31 - c)) & 1u) ? 1 : -1;
           if (f) v = -v;
         }
-        if (srow == 0 && el == C::SB) v = bias;
+        if (REAL) {
+          const int nb = -bias, q = (nb >= 0 ? nb + 127 : nb - 127) / 255, r = nb - 255 * q;
+          if (srow == 0 && el == C::SB) v = r;
+          if (srow == 0 && el == C::SB + 1) v = q;
+        } else if (srow == 0 && el == C::SB) {
+          v = bias;
+        }
         w4[e >> 2] |= ((uint32_t)v & 0xFFu) << (8 * (e & 3));
       }
     }
@@ -203,7 +211,7 @@ __global__ void prep_first_tma_kernel(const ConvArgs A, uint8_t* out) {
 // acc_empty[b]  epilogue (4)                 -> MMA issuer (one or two TMEM accumulator sets)
 constexpr int kFirstTmaThreads = 320;
 
-template <int K, bool FP4, bool DB = false>
+template <int K, bool FP4, bool DB = false, bool REAL = false>
 __global__ void __launch_bounds__(kFirstTmaThreads, (FP4 || DB) ? 2 : 3)
 conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
@@ -248,11 +256,12 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     ox0 = tx * TW;
   };
 
-  if (tid < NT) s_bias[tid] = first_tma_bias<K>(A, g * NT + tid);
+  static_assert(!(REAL && FP4), "real u8 pixels need the int8 operand");
+  if (tid < NT) s_bias[tid] = first_tma_bias<K, REAL>(A, g * NT + tid);
   if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
-    stage_b_first_tma<K, FP4>(A, g, sB, tid, kFirstTmaThreads);
+    stage_b_first_tma<K, FP4, REAL>(A, g, sB, tid, kFirstTmaThreads);
   }
   griddep_wait();  // the image buffer and the output buffer belong to the predecessors' stream order
   tc::fence_async_smem();
@@ -264,7 +273,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
   if (warp == 0) {
     // ------------------------------------------------------------ producer + MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = FP4 ? tc::idesc_mxf4(128, N) : tc::idesc_i8(128, N, true);
+      constexpr uint32_t idesc = FP4 ? tc::idesc_mxf4(128, N) : tc::idesc_i8(128, N, !REAL);  // REAL: u8 A
       const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // FP4 block scales (all 1.0)
       auto issue_raw = [&](int tile, int slot) {
         int img, oy0, ox0;
@@ -349,8 +358,8 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         // M[w]: 0xFF where the byte is +1 (x > t_c, R14), 0x00 where -1
         uint32_t M[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) M[w] = thresh_mask4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
-        if (!zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
+        for (int w = 0; w < 8; ++w) M[w] = REAL ? src[w] : thresh_mask4(src[w], E[(C::C0 + w) % 3], O[(C::C0 + w) % 3]);
+        if (!REAL && !zero_ok) {  // out-of-image bytes must be -1 whatever the threshold (uniform branch)
           int img, oy0, ox0;
           tile_origin(tile, img, oy0, ox0);
           const int gy = oy0 - R + r;
@@ -397,7 +406,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         } else {
           uint32_t T[8];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) T[w] = ~M[w] | 0x01010101u;  // int8 +1 / -1
+          for (int w = 0; w < 8; ++w) T[w] = REAL ? M[w] : (~M[w] | 0x01010101u);  // raw u8 / int8 +1 / -1
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
             constexpr int e0 = C::E;
@@ -408,10 +417,17 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
               const int w = qw + k;
               const uint32_t lo = w < 8 ? T[w] : 0xFFFFFFFFu, hi = w + 1 < 8 ? T[w + 1] : 0xFFFFFFFFu;
               v[k] = sh ? __funnelshift_r(lo, hi, sh) : lo;
-              // bytes >= SB of the strip: -1 (bias slots / unused K)
+              // bytes >= SB of the strip: -1 (bias slots / unused K); REAL: 1, 255, then 0
               const int b0 = 4 * k;
-              if (b0 >= C::SB) v[k] = 0xFFFFFFFFu;
-              else if (b0 + 4 > C::SB) v[k] |= 0xFFFFFFFFu << (8 * (C::SB - b0));
+              const uint32_t keep = b0 >= C::SB ? 0u : (b0 + 4 > C::SB ? 0xFFFFFFFFu >> (8 * (b0 + 4 - C::SB)) : 0xFFFFFFFFu);
+              uint32_t pat = 0xFFFFFFFFu;
+              if (REAL) {
+                pat = 0u;
+#pragma unroll
+                for (int jb = 0; jb < 4; ++jb)
+                  pat |= (b0 + jb == C::SB ? 0x01u : (b0 + jb == C::SB + 1 ? 0xFFu : 0u)) << (8 * jb);
+              }
+              v[k] = (v[k] & keep) | (pat & ~keep);
             }
             const int px = 2 * j + s;
             *reinterpret_cast<uint4*>(a + r * C::ROWP + px * 16) = make_uint4(v[0], v[1], v[2], v[3]);

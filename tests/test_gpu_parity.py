@@ -670,3 +670,33 @@ def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, tma):
         cuda.set_option("first_tma", 1)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+
+
+# ------------------------------------------------------------------------------------ real u8 first layer (TMA)
+@pytest.mark.parametrize("tma", [1, 0])
+@pytest.mark.parametrize("h,w,k,cout,fill", [(32, 48, 5, 32, None), (18, 16, 3, 40, None), (34, 64, 5, 64, None),
+                                             (16, 16, 5, 32, 255)])
+def test_first_layer_real_u8_tma(cuda, orc, h, w, k, cout, fill, tma):
+    """Mode NONE (R5): real u8 pixels x +/-1 weights with zero padding on the TMA kernel (unsigned int8 A
+    operand, bias r + 255 q in two slots) or the register-staged kernel: exact int32 accumulators,
+    thresholds spanning the +/-K^2*3*255 range, flips, fused 2x2 pool; fill = 255: the extreme sums."""
+    seed = 2100 + h + k + cout
+    x = synth.images(3, h, w, 3, seed)
+    if fill is not None:
+        x[:] = fill
+    wt = synth.pm1((cout, k, k, 3), seed + 1)
+    thr = synth.int_thresholds(cout, seed + 2, -4000, 4001)
+    thr[0], thr[1] = 19200, -19200  # beyond |acc| <= 19125: constant bits
+    flip = synth.flips(cout, seed + 3)
+    try:
+        cuda.set_option("first_real_tma", tma)
+        y, acc = cuda.conv2d(dev(x), cuda.U8, 3, cuda.pack_weights(dev(wt)), cout, k, dev(thr), dev(flip), pool=2,
+                             want_acc=True)
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("first_real_tma", 1)
+    for i in range(3):
+        ra = orc.conv_real(x[i].numpy().astype(np.float64), wt.numpy())
+        assert np.array_equal(acc[i].cpu().numpy(), ra.astype(np.int32))
+        b = orc.maxpool2(orc.binarize(ra, thr.numpy(), flip.numpy()))
+        assert np.array_equal(u32(y[i]), orc.pack_channels(b))
