@@ -1,11 +1,14 @@
-"""Per-layer live times of the vehicle forward (library events, one stream), batch 32768."""
+"""Per-layer live times of the vehicle forward (library events, one stream) and the two-stream step,
+batch 32768.  usage: python tools/time_layers.py [chunk]"""
 import torch
 import paper_1808_00209_b200 as bnn
 from paper_1808_00209_b200 import synth
+import sys
 B = 32768
+CHUNK = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 layers = synth.make_weights(synth.VEHICLE, 1, 5)
 dl = [dict(L, wt=bnn.pack_weights(L["wt"].cuda())) for L in layers]
-net = bnn.Net(96, 96, 3, bnn.U8, 1, synth.thresholds(3, 5).cuda(), dl, max_batch=8192)
+net = bnn.Net(96, 96, 3, bnn.U8, 1, synth.thresholds(3, 5).cuda(), dl, max_batch=CHUNK)
 x = synth.images(B, 96, 96, 3, 6).cuda()
 lg = torch.empty((B, 4), dtype=torch.int32, device="cuda"); cls = torch.empty((B,), dtype=torch.int32, device="cuda")
 for rep in range(2):
