@@ -202,20 +202,39 @@ conv_tc4_big_kernel(const ConvArgs A) {
     tc::fence_before();
   };
 
-  uint32_t stage_uses = 0;
-  int it = 0;
-  int64_t prev = -1;
-  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
+  // A words of the next stage are loaded into registers one stage ahead (their global-load latency
+  // overlaps the current stage's MMAs instead of stalling the expansion)
+  uint32_t pref[PF];
+  auto load_a = [&](int64_t tile, int st) {
     int img, oy0, ox0;
     tile_origin(tile, img, oy0, ox0);
     const uint32_t* xin = A.x + (int64_t)img * A.H * A.W * A.cw;
+    const int j0 = st * CG;
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int i = tid + q * 256;
+      uint32_t w = 0u;  // outside the map / beyond c_in: -1 bits (weights there are 0 for words >= cw)
+      if (i < CG * NPIX) {
+        const int p = i % NPIX, jl = i / NPIX, j = j0 + jl;
+        const int r = p / IC, cc = p - r * IC, ih = cc / ICI, c = cc - ih * ICI;
+        const int gy = oy0 - R + r, gx = ox0 - R + c;
+        if (j < A.cw && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W && img + ih < A.n)
+          w = __ldg(xin + ((int64_t)ih * A.H * A.W + (int64_t)gy * A.W + gx) * A.cw + j);
+      }
+      pref[q] = w;
+    }
+  };
+  uint32_t stage_uses = 0;
+  int it = 0;
+  int64_t prev = -1;
+  if ((int64_t)blockIdx.x < A.total_tiles) load_a(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
     for (int st = 0; st < nstage; ++st, ++stage_uses) {
       const int s = stage_uses & 1;
       if (stage_uses >= 2) tc::mbar_wait(&bar_stage[s], ((stage_uses - 2) >> 1) & 1);
       uint8_t* a = dsm + s * C::STAGE_BYTES;
       uint8_t* b = a + C::A_BYTES;
-      const int j0 = st * CG;
       if (A.bimg != nullptr && tid == 0)
         tc::stage_image(b, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES, &w_bar[s]);
       // A: halo words j0 .. j0+CG-1 -> planes [jl][p] (16 B = 32 channels as e2m1)
@@ -223,17 +242,13 @@ conv_tc4_big_kernel(const ConvArgs A) {
       for (int q = 0; q < PF; ++q) {
         const int i = tid + q * 256;
         if (i < CG * NPIX) {
-          const int p = i % NPIX, jl = i / NPIX, j = j0 + jl;
-          const int r = p / IC, cc = p - r * IC, ih = cc / ICI, c = cc - ih * ICI;
-          const int gy = oy0 - R + r, gx = ox0 - R + c;
-          uint32_t w = 0u;  // outside the map / beyond c_in: -1 bits (weights there are 0 for words >= cw)
-          if (j < A.cw && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W && img + ih < A.n)
-            w = __ldg(xin + ((int64_t)ih * A.H * A.W + (int64_t)gy * A.W + gx) * A.cw + j);
           uint32_t o4[4];
-          expand_word_fp4(w, s_lut, o4);
+          expand_word_fp4(pref[q], s_lut, o4);
           *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
         }
       }
+      if (st + 1 < nstage) load_a(tile, st + 1);
+      else if (tile + (int64_t)gridDim.x < A.total_tiles) load_a(tile + gridDim.x, 0);
       if (A.bimg != nullptr) {
         // B: this stage's pre-expanded weight image, one bulk copy (issued before the A expansion)
       } else {
