@@ -1,0 +1,28 @@
+"""CIFAR BinaryNet per-layer live times (library events, one stream) under a list of options.
+usage: python tools/time_cifar.py key=value[,key=value] ..."""
+import sys
+import torch
+import paper_1808_00209_b200 as bnn
+from paper_1808_00209_b200 import synth
+B = 16384
+layers = synth.make_weights(synth.CIFAR, 1, 5)
+dl = [dict(L, wt=bnn.pack_weights(L["wt"].cuda())) for L in layers]
+net = bnn.Net(32, 32, 3, bnn.U8, 1, synth.thresholds(3, 5).cuda(), dl, max_batch=8192)
+bnn.set_option("streams", 1)  # per-layer events are only meaningful on one stream
+x = synth.images(B, 32, 32, 3, 6).cuda()
+ref = None
+for arg in sys.argv[1:] or [""]:
+    opts = dict(kv.split("=") for kv in arg.split(",") if kv)
+    for k, v in opts.items():
+        bnn.set_option(k, int(v))
+    lg, cls = net.forward(x)
+    torch.cuda.synchronize()
+    if ref is None:
+        ref = lg.clone()
+    assert torch.equal(ref, lg), "results changed"
+    net.profile(True)
+    for _ in range(5):
+        net.forward(x)
+    ms, cnt = net.profile_read()
+    net.profile(False)
+    print("%-30s" % arg, " ".join("%.3f" % (m / 5) for m in ms[1:10]), " total %.3f ms" % (sum(ms) / 5), flush=True)
