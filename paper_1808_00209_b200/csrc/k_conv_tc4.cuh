@@ -44,7 +44,11 @@ conv_tc4_kernel(const ConvArgs A) {
   uint8_t* sA = dsm + C::B_BYTES;                              // 2 x [j][NPIX][16] (+ slack)
   float* s_thr = reinterpret_cast<float*>(sA + 2 * C::A_BYTES);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);  // 256 entries
-  __shared__ uint64_t bar[2];
+  // warp roles: warps 4-7 expand the A halo (4 words / pixel -> e2m1) of tile it into A[it % 2], warp 4
+  // lane 0 also issues the MMAs; warps 0-3 drain the accumulators of tile it from TMEM buffer it % 2.
+  // a_full[b]: loaders (4) -> issuer; a_free[b]: commit -> loaders; acc_full[b]: commit -> epilogue;
+  // acc_empty[b]: epilogue (4) -> issuer.  No block-wide barrier in the tile loop.
+  __shared__ uint64_t a_full[2], a_free[2], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ uint32_t s_flip[NT / 32];
 
@@ -70,8 +74,13 @@ conv_tc4_kernel(const ConvArgs A) {
   for (int i = tid; i < 2 * (int)C::A_BYTES / 16; i += 256) reinterpret_cast<uint4*>(sA)[i] = make_uint4(0, 0, 0, 0);
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&a_full[b], 4);
+      tc::mbar_init(&a_free[b], 1);
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 4);
+    }
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -116,7 +125,7 @@ conv_tc4_kernel(const ConvArgs A) {
   auto epilogue = [&](int64_t tile, int buf, uint32_t phase) {
     int img, oy0, ox0;
     tile_origin(tile, img, oy0, ox0);
-    tc::mbar_wait(&bar[buf], phase);
+    tc::mbar_wait_sleep(&acc_full[buf], phase);
     tc::fence_after();
     const int m = warp * 32 + lane;
     const int oy = oy0 + m / TW, ox = ox0 + m % TW;
@@ -154,7 +163,8 @@ conv_tc4_kernel(const ConvArgs A) {
     tc::fence_before();
   };
 
-  constexpr int PF = (CW * NPIX + 255) / 256;
+  constexpr int PF = (CW * NPIX + 127) / 128;  // words per loader thread (warps 4-7)
+  const int lt = tid - 128;
   uint32_t pref[PF];
   auto load_tile = [&](int64_t tile) {
     int img, oy0, ox0;
@@ -162,7 +172,7 @@ conv_tc4_kernel(const ConvArgs A) {
     const uint32_t* xin = A.x + (int64_t)img * A.H * A.W * A.cw;
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      const int i = tid + q * 256;
+      const int i = lt + q * 128;
       uint32_t w = 0u;  // outside the map: all -1 (R4)
       if (i < CW * NPIX) {
         const int p = i % NPIX, j = i / NPIX;
@@ -173,48 +183,60 @@ conv_tc4_kernel(const ConvArgs A) {
       pref[q] = w;
     }
   };
-  if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
 
-  int it = 0;
-  int64_t prev = -1;
-  for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    if (it >= 2) tc::mbar_wait(&bar[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] free again
-    uint8_t* a = sA + buf * C::A_BYTES;
+  if (warp >= 4) {
+    // ------------------------------------------------------------ loaders (+ MMA issuer: tid 128)
+    if (blockIdx.x < A.total_tiles) load_tile(blockIdx.x);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      if (it >= 2) tc::mbar_wait_sleep(&a_free[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      uint8_t* a = sA + buf * C::A_BYTES;
 #pragma unroll
-    for (int q = 0; q < PF; ++q) {
-      const int i = tid + q * 256;
-      if (i < CW * NPIX) {
-        uint32_t o4[4];
-        expand_word_fp4(pref[q], s_lut, o4);
-        *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);  // [j][p]
+      for (int q = 0; q < PF; ++q) {
+        const int i = lt + q * 128;
+        if (i < CW * NPIX) {
+          uint32_t o4[4];
+          expand_word_fp4(pref[q], s_lut, o4);
+          *reinterpret_cast<uint4*>(a + (size_t)i * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);  // [j][p]
+        }
       }
-    }
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    if (tid == 128) {  // warp 4 issues; warps 0-3 drain the previous tile
-      const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
-      const uint32_t d_tmem = tmem + (uint32_t)(buf * NT);
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&a_full[buf]);
+      if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
+      if (tid == 128) {
+        tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
+        if (it >= 2) tc::mbar_wait(&acc_empty[buf], (uint32_t)(((it - 2) >> 1) & 1));  // tile it-2 drained
+        tc::fence_after();
+        const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(sB);
+        const uint32_t d_tmem = tmem + (uint32_t)(buf * NT);
 #pragma unroll
-      for (int i = 0; i < C::NMMA; ++i) {
-        // chunk u -> byte offset of its pixel for output pixel 0: plane j, halo (t / K, t % K)
-        const int u0 = 2 * i, u1 = (2 * i + 1 < U) ? 2 * i + 1 : 2 * i;  // odd U: dummy (weights 0)
-        const int off0 = ((u0 / KK) * NPIX + ((u0 % KK) / K) * IC + (u0 % KK) % K) * 16;
-        const int off1 = ((u1 / KK) * NPIX + ((u1 % KK) / K) * IC + (u1 % KK) % K) * 16;
-        const uint32_t lbo = (off1 > off0) ? (uint32_t)(off1 - off0) : 16u;
-        const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)off0, lbo, IC * 16);
-        const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(i * 2 * NT * 16), NT * 16, 128);
-        tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, i > 0 ? 1u : 0u);
+        for (int i = 0; i < C::NMMA; ++i) {
+          // chunk u -> byte offset of its pixel for output pixel 0: plane j, halo (t / K, t % K)
+          const int u0 = 2 * i, u1 = (2 * i + 1 < U) ? 2 * i + 1 : 2 * i;  // odd U: dummy (weights 0)
+          const int off0 = ((u0 / KK) * NPIX + ((u0 % KK) / K) * IC + (u0 % KK) % K) * 16;
+          const int off1 = ((u1 / KK) * NPIX + ((u1 % KK) / K) * IC + (u1 % KK) % K) * 16;
+          const uint32_t lbo = (off1 > off0) ? (uint32_t)(off1 - off0) : 16u;
+          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)off0, lbo, IC * 16);
+          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(i * 2 * NT * 16), NT * 16, 128);
+          tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, i > 0 ? 1u : 0u);
+        }
+        tc::commit(&a_free[buf]);
+        tc::commit(&acc_full[buf]);
       }
-      tc::commit(&bar[buf]);
+      __syncwarp();
     }
-    if (tile + gridDim.x < A.total_tiles) load_tile(tile + gridDim.x);
-    if (prev >= 0 && warp < 4) epilogue(prev, buf ^ 1, (uint32_t)(((it - 1) >> 1) & 1));
-    prev = tile;
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 0-3)
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < A.total_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      epilogue(tile, buf, (uint32_t)((it >> 1) & 1));
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
+    }
   }
-  if (prev >= 0 && warp < 4) epilogue(prev, (it - 1) & 1, (uint32_t)(((it - 1) >> 1) & 1));
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
 }
