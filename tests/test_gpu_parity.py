@@ -700,3 +700,34 @@ def test_first_layer_real_u8_tma(cuda, orc, h, w, k, cout, fill, tma):
         assert np.array_equal(acc[i].cpu().numpy(), ra.astype(np.int32))
         b = orc.maxpool2(orc.binarize(ra, thr.numpy(), flip.numpy()))
         assert np.array_equal(u32(y[i]), orc.pack_channels(b))
+
+
+@pytest.mark.parametrize("mode", [2, 3, -1])
+def test_forward_chunked_two_streams_modes(cuda, orc, mode):
+    """GRAY / LBP / NONE nets over several chunks alternating between the two internal streams
+    (max_batch 16, 37 images: 3 chunks, ragged last) equal the oracle; launch accounting matches."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, mode, 2300 + mode, max_batch=16)
+    imgs = synth.images(37, 96, 96, 3, 2310 + mode)
+    lg, cls = net.forward(dev(imgs))
+    torch.cuda.synchronize()
+    ref_l, ref_c = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=8)
+    assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+    assert net.layer_kernel(0, 16) == "conv_first_tma_pool_kernel"
+    # per chunk: (pack / luma kernel unless fused) + 5 layers
+    per_chunk = 6 if mode in (2, 3) else 5
+    assert cuda.forward_launches(net, 37) == 3 * per_chunk
+
+
+def test_forward_scores_chunked(cuda, orc):
+    """bnn_forward_scores over 3 chunks on two streams: scores / classes of every image."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 2400, max_batch=16)
+    imgs = synth.images(40, 96, 96, 3, 2401)
+    scale = torch.tensor([0.5, -1.25, 2.0, 1.0])
+    bias = torch.tensor([3.0, 0.0, -2.5, 0.125])
+    logits, scores, cls = net.forward_scores(dev(imgs), dev(scale), dev(bias))
+    torch.cuda.synchronize()
+    ref_l, _ = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=8)
+    _, s32, rcls = orc.affine(ref_l, scale.numpy(), bias.numpy())
+    assert np.array_equal(logits.cpu().numpy(), ref_l)
+    assert np.array_equal(scores.cpu().numpy().view(np.uint32), s32.view(np.uint32))
+    assert np.array_equal(cls.cpu().numpy(), rcls)
