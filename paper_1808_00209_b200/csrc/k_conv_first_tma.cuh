@@ -492,7 +492,36 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           }
       }
       uint32_t neg = 0, negp[4] = {0u, 0u, 0u, 0u};
-      if (!(A.exp & 2))
+      bool packed = false;
+      if constexpr (!FP4 && !REAL) {
+        // 16-bit packed drain: acc' = acc - thr' - 1 is in [-151, 151], so the low halves of the int32
+        // accumulators are exact s16 values; .pack::16b loads two channels per register, VIMNMX3 /
+        // VIMNMX .S16x2 take the 4-way pool max of two channels per instruction, and the sign bits
+        // of 4 channels are gathered by one PRMT (bytes 1 / 3 hold them as bit 7) and one multiply
+        // (bits 7, 15, 23, 31 -> 31..28, MSB-first) instead of one funnel shift per channel
+        if (!(A.exp & 3)) {
+          packed = true;
+#pragma unroll
+          for (int cb = 0; cb < NT; cb += 16) {
+            uint32_t a[8], b[8], c[8], d[8];
+            tc::tmem_ld8_p16(acc_base + (uint32_t)(0 * NT + cb), a);
+            tc::tmem_ld8_p16(acc_base + (uint32_t)(1 * NT + cb), b);
+            tc::tmem_ld8_p16(acc_base + (uint32_t)(2 * NT + cb), c);
+            tc::tmem_ld8_p16(acc_base + (uint32_t)(3 * NT + cb), d);
+            tc::tmem_ld_wait();
+            uint32_t m[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) m[jj] = __vmaxs2(__vimax3_s16x2(a[jj], b[jj], c[jj]), d[jj]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t w = __byte_perm(m[2 * i], m[2 * i + 1], 0x1357);  // ch 4i+3, 4i+2, 4i+1, 4i
+              const uint32_t y = (w & 0x80808080u) * 0x00204081u;              // signs -> bits 28..31
+              neg |= (y >> 28) << (28 - cb - 4 * i);
+            }
+          }
+        }
+      }
+      if (!packed && !(A.exp & 2))
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
         int a[16], b[16], c[16];
@@ -518,7 +547,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           nk = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), nk, 1);
         }
       }
-      neg = (negp[0] << 24) | (negp[1] << 16) | (negp[2] << 8) | negp[3];
+      if (!packed) neg = (negp[0] << 24) | (negp[1] << 16) | (negp[2] << 8) | negp[3];
       tc::fence_before();
       __syncwarp();
       if (tid == 6 * 32) trace_ev(A, it, 13);

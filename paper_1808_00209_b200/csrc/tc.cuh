@@ -135,6 +135,14 @@ BNN_DEV void tmem_ld16(uint32_t taddr, int (&v)[16]) {
       : "r"(taddr));
 }
 
+// 16 consecutive columns of this thread's TMEM lane, low 16 bits of each, packed in pairs: register j
+// holds column 2j in bits 0-15 and column 2j+1 in bits 16-31 (.pack::16b).
+BNN_DEV void tmem_ld8_p16(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
 BNN_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 }  // namespace tc
