@@ -731,3 +731,20 @@ def test_forward_scores_chunked(cuda, orc):
     assert np.array_equal(logits.cpu().numpy(), ref_l)
     assert np.array_equal(scores.cpu().numpy().view(np.uint32), s32.view(np.uint32))
     assert np.array_equal(cls.cpu().numpy(), rcls)
+
+
+@pytest.mark.parametrize("mode", [2, 3, -1, 0])
+def test_forward_staged_graph_modes(cuda, orc, mode):
+    """The CUDA-graph latency path for GRAY / LBP (luma kernel + TMA first layer), NONE (real-u8 TMA
+    first layer) and SIGN nets: replays with newly staged images equal the oracle."""
+    net, layers, T = build_net(cuda, synth.VEHICLE, mode, 2500 + mode, max_batch=64)
+    onet = oracle_net(orc, synth.VEHICLE, mode, layers, T)
+    st_in, st_lg, st_cls = net.staging(4)
+    for n, seed in [(1, 2501), (3, 2502), (1, 2503)]:
+        imgs = synth.images(n, 96, 96, 3, seed + mode)
+        st_in[:n].copy_(imgs.cuda())
+        net.forward_staged(n)
+        torch.cuda.synchronize()
+        ref_l, ref_c = onet.forward(imgs.numpy(), threads=n)
+        assert np.array_equal(st_lg[:n].cpu().numpy(), ref_l)
+        assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
