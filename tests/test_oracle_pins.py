@@ -355,16 +355,37 @@ def test_lbp_orientation_and_border(orc):
 # ----------------------------------------------------------------------------- whole network
 def _torch_forward(images, mode, T, layers):
     """Library composition of the Section 2 pipeline in float64 (independent of the oracle's
-    code): input binarization written with torch ops, conv2d with -1 padding, sign with
-    acc <= 0 -> -1, max_pool2d, HWC flatten, matmul."""
-    def sgn(a):  # Eq. (1): a <= 0 -> -1
-        return (a > 0).double() * 2 - 1
+    code): input binarization written with torch ops (integer luma R15 as int64 tensor arithmetic,
+    LBP R16 as comparisons against a replicate-padded luma plane, mode NONE as a zero-padded
+    conv2d of the raw pixels, R5), conv2d with -1 padding, the threshold (acc > thr) XOR flip
+    with acc <= thr -> -1 (Eq. 1, R23), max_pool2d, HWC flatten, matmul."""
+    def binar(a, L, ax):
+        t = torch.zeros(a.shape[ax], dtype=torch.float64) if L.get("thr") is None else \
+            torch.as_tensor(np.asarray(L["thr"]), dtype=torch.float64)
+        f = torch.zeros(a.shape[ax], dtype=torch.bool) if L.get("flip") is None else \
+            torch.as_tensor(np.asarray(L["flip"]) != 0)
+        shape = [1] * a.dim()
+        shape[ax] = -1
+        pos = (a > t.view(shape)) ^ f.view(shape)
+        return pos.double() * 2 - 1
 
     x = torch.from_numpy(images.astype(np.float64))  # [n,h,w,c]
+    xi = torch.from_numpy(images.astype(np.int64))
     if mode == 1:
-        x = sgn(x + torch.from_numpy(np.asarray(T, np.float32).astype(np.float64)))
+        x = (x + torch.from_numpy(np.asarray(T, np.float32).astype(np.float64)) > 0).double() * 2 - 1
     elif mode == 0:
-        x = sgn(x)
+        x = (x > 0).double() * 2 - 1
+    elif mode in (2, 3):
+        Y = torch.div(299 * xi[..., 0] + 587 * xi[..., 1] + 114 * xi[..., 2] + 500, 1000, rounding_mode="floor")
+        if mode == 2:
+            x = ((Y.double() + float(np.float32(T[0]))) > 0).double()[..., None] * 2 - 1
+        else:
+            Yp = F.pad(Y.double()[:, None], (1, 1, 1, 1), mode="replicate")[:, 0]  # [n, h+2, w+2]
+            h, w = Y.shape[1], Y.shape[2]
+            tl = Yp[:, 0:h, 0:w]            # n0: top-left
+            r = Yp[:, 1:h + 1, 2:w + 2]     # n3: right
+            bl = Yp[:, 2:h + 2, 0:w]        # n6: bottom-left
+            x = torch.stack([(nb > Y.double()).double() * 2 - 1 for nb in (tl, r, bl)], dim=-1)
     x = x.permute(0, 3, 1, 2)
     flat = None
     for i, L in enumerate(layers):
@@ -372,8 +393,9 @@ def _torch_forward(images, mode, T, layers):
         last = i == len(layers) - 1
         if L["kind"] == "conv":
             R = (L["k"] - 1) // 2
-            a = F.conv2d(F.pad(x, (R, R, R, R), value=-1.0), wt.permute(0, 3, 1, 2))
-            x = sgn(a)
+            pad = 0.0 if (i == 0 and mode == -1) else -1.0
+            a = F.conv2d(F.pad(x, (R, R, R, R), value=pad), wt.permute(0, 3, 1, 2))
+            x = binar(a, L, 1)
             if L.get("pool", 1) == 2:
                 x = F.max_pool2d(x, 2)
         else:
@@ -382,23 +404,62 @@ def _torch_forward(images, mode, T, layers):
             a = flat @ wt.T
             if last:
                 return a.numpy().astype(np.int64)
-            flat = sgn(a)
+            flat = binar(a, L, 1)
     raise AssertionError
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_forward_vs_torch_composition(orc, mode):
-    spec = dict(h=8, w=8, c=3, layers=[dict(kind="conv", k=3, c_out=4, pool=2), dict(kind="conv", k=5, c_out=6, pool=2),
-                                       dict(kind="dense", l=7), dict(kind="dense", l=5)])
-    layers = synth.make_weights(spec, mode, 100 + mode, small_layers=spec["layers"])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, -1])
+@pytest.mark.parametrize("bn", [False, True])
+def test_forward_vs_torch_composition(orc, mode, bn):
+    """orc_forward for every input mode (SIGN, THRESH_RGB, THRESH_GRAY, LBP, NONE), with and without
+    BN-folded thresholds / flips, against the torch composition above.  Odd map sizes (10x6 after
+    the first pool: 5x3) and a c_out that is not a multiple of 32 exercise the HWC flatten."""
+    spec = dict(h=10, w=6, c=3, layers=[dict(kind="conv", k=3, c_out=4, pool=2), dict(kind="conv", k=5, c_out=6, pool=1),
+                                        dict(kind="dense", l=7), dict(kind="dense", l=5)])
+    seed = 100 + 10 * mode + bn
+    layers = synth.make_weights(spec, mode, seed, small_layers=spec["layers"])
     layers = [dict(L, wt=synth.numpy(L["wt"])) for L in layers]
-    imgs = synth.numpy(synth.images(4, 8, 8, 3, 30 + mode))
-    T = [-128.0, -100.0, -140.0]
-    net = orc.Net(8, 8, 3, mode, T if mode == 1 else None, layers)
+    if bn:
+        for j, L in enumerate(layers[:-1]):
+            c = L["wt"].shape[0]
+            lo, hi = (-300, 300) if (j == 0 and mode == -1) else (-6, 7)
+            L["thr"] = synth.numpy(synth.int_thresholds(c, seed + j, lo, hi))
+            L["flip"] = synth.numpy(synth.flips(c, seed + 50 + j))
+    imgs = synth.numpy(synth.images(4, 10, 6, 3, 30 + mode))
+    imgs[0] = 128  # flat image: every LBP comparison is a tie (-> -1), luma 128, X + T = 0 at T = -128
+    T = {1: [-128.0, -100.0, -140.0], 2: [-128.0]}.get(mode)
+    net = orc.Net(10, 6, 3, mode, T, layers)
     logits, cls = net.forward(imgs)
     ref = _torch_forward(imgs, mode, T, layers)
     assert np.array_equal(logits, ref)
     assert list(cls) == [int(np.argmax(r)) for r in ref]
+
+
+@pytest.mark.parametrize("case", GOLD["binarize_real"])
+def test_binarize_real_golden(orc, case):
+    """orc_binarize_f64 (the real first layer's threshold, R5/R23) on hand-derived values: ties at
+    acc == thr -> -1, signed zeros -> -1, thr / flip."""
+    acc = np.array(case["acc"], np.float64).reshape(1, -1)
+    out = orc.binarize(acc, thr=case["thr"], flip=case["flip"])[0]
+    assert list(out) == case["out"]
+
+
+def test_binarize_real_closed_form_none_layer(orc):
+    """Mode NONE closed form: a constant image v with all-(+1) weights gives acc = v * C * n_in(y,x)
+    (zero padding, R5).  With thr = v * C * 9 (the interior value, k = 3) every interior pixel is a
+    tie -> -1, every border pixel is below -> -1; with thr = v * C * 6 - 1 the edge (non-corner)
+    pixels and the interior are +1 and the corners (4 taps) are -1."""
+    h, w, c, v = 5, 6, 3, 7.0
+    wt = np.ones((1, 3, 3, c), np.int8)
+    acc = orc.conv_real(np.full((h, w, c), v), wt)
+    b = orc.binarize(acc, thr=[int(v * c * 9)])[..., 0]
+    assert np.all(b == -1)
+    b = orc.binarize(acc, thr=[int(v * c * 6) - 1])[..., 0]
+    corner = np.zeros((h, w), bool)
+    corner[[0, 0, -1, -1], [0, -1, 0, -1]] = True
+    assert np.all(b[corner] == -1) and np.all(b[~corner] == 1)
+    b = orc.binarize(acc, thr=[int(v * c * 6) - 1], flip=[1])[..., 0]
+    assert np.all(b[corner] == 1) and np.all(b[~corner] == -1)
 
 
 def test_forward_equals_layer_composition(orc):
