@@ -1,21 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 binarized-CNN forward pass (arXiv 1808.00209) -- the driver contract.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bnn|reference] [--batch B] [--mode rgb]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bnn|reference] [--total-batch B] [--mode rgb]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-A "step" is one pass of the whole hot path (bnn_forward: pack -> conv1+pool -> conv2+pool -> FC1 ->
-FC2 -> FC3 + argmax) over one batch of B synthetic images per GPU (default B = 32768: the
-per-GPU shard of BASELINE config 5, 262144 images over 8 GPUs; weak scaling, B fixed per GPU),
-followed at N > 1 by the NCCL all-gather of the predictions.  Inputs are resident in HBM before
-the timed region; the 906 MB input per GPU is larger than the 126 MB L2, so no L2 flush is needed.
+A "step" is one pass of the whole hot path (bnn_forward: conv1 (+ fused input binarization, threshold,
+pool) -> conv2 + pool -> FC1 -> FC2 -> FC3 + argmax) over BASELINE config 5's batch: 262,144 synthetic
+images per step, split into contiguous shards over the N GPUs (strong scaling; --batch B instead fixes
+B images per GPU = weak scaling), followed at N > 1 by the NCCL all-gather of the predictions.  Inputs are
+resident in HBM before the timed region; the 7.25 GB input (906 MB per GPU at N = 8) is larger than the
+126 MB L2, so no L2 flush is needed.
 
-Prints ONE JSON line (rank 0).  `value` = images/s of the whole job (all ranks), timed with CUDA
-events on the forward stream, max over ranks.  `e2e` = the same metric through bnn_forward_host
-(pinned host images -> host logits/classes, copies inside the timed region).  `roofline` = the
-dominant conv kernel (largest live CUDA-event time): tcgen05 kernels as int8 TOPS (2 x algorithmic
-binary MACs / time) vs 2 x the measured bf16 sustained peak; POPC kernels as algorithmic popcounts /
-time vs the POPC pipe (16 / clk / SM, tools/probes/pipe_probe.cu) x SMs x max SM clock.
+Prints ONE JSON line (rank 0).  `value` = images/s of the whole job, timed with CUDA events on the
+forward stream, max over ranks.  `e2e` = the same metric through bnn_forward_host (pinned host images
+-> host logits/classes, copies inside the timed region).  `roofline` = the dominant conv kernel
+(largest live CUDA-event time): tcgen05 kernels as TOPS (2 x algorithmic binary MACs / time) vs the
+measured bf16 peak x the nominal ratio of the kernel's operand type (burst when the SM clock held its
+maximum during the timed region, else sustained), plus the repo's probed MMA rate; POPC kernels as
+algorithmic popcounts / time vs the POPC pipe (16 / clk / SM, tools/probes/pipe_probe.cu).
+`parity` = sampled images of the whole job vs the CPU oracle; `multi_gpu_check` (N > 1) = the gathered
+predictions vs a 1-GPU pass over the same global batch on rank 0.
 `cpu_baseline` = the CPU oracle (oracle/) on a bounded sample on the host cores (rank 0, N = 1).
 --impl reference times that oracle alone as the reference arm.
 """
@@ -45,7 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="bnn", choices=["bnn", "reference"])
-    ap.add_argument("--batch", type=int, default=32768, help="images per GPU per step")
+    ap.add_argument("--total-batch", type=int, default=262144,
+                    help="images per step over all GPUs (BASELINE config 5; strong scaling, contiguous shards)")
+    ap.add_argument("--batch", type=int, default=0, help="if set: fixed images per GPU per step (weak scaling)")
     ap.add_argument("--chunk", type=int, default=16384, help="bnn_net max_batch (images per internal chunk; 16384 measured best: 2 chunks per step on two streams)")
     ap.add_argument("--mode", default="rgb", choices=sorted(MODES))
     ap.add_argument("--seed", type=int, default=2018)
@@ -170,11 +176,73 @@ def read_peaks():
     return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+# tcgen05 MMA rates measured by the repo's probes (M = 128, N >= 128, 148 CTAs): MAC / clk / SM
+PROBE_MAC_PER_CLK_SM = {"i8": 8187, "fp4": 16375}  # profiles/umma_probe_r01.txt, profiles/mxf4_probe_r01.txt
+
+
+def kernel_dtype(kernel: str):
+    """Operand type of a kernel family: 'fp4' (tcgen05 kind::mxf4), 'i8' (kind::i8) or None (integer pipe)."""
+    if "tc4" in kernel or kernel.endswith("_fp4"):
+        return "fp4"
+    if "_tc" in kernel or "_tma_" in kernel:
+        return "i8"
+    return None
+
+
+def clocks_held(clocks) -> bool:
+    """True when the SM clock stayed at its maximum with no throttle reason during the timed region:
+    the kernel then runs at the burst (not the sustained, power-limited) tensor rate."""
+    sm, mx = clocks.get("sm_mhz"), clocks.get("sm_max_mhz")
+    return bool(sm and mx and sm >= 0.97 * mx and not clocks.get("reasons"))
+
+
+def tensor_peak(dt: str, clocks, sms: int):
+    """Peak dense TOPS (2 ops per MAC) for operand type dt: the measured bf16 peak of MEASURED_PEAKS.json x the
+    nominal ratio (i8 2x, fp4 4x; B200_PROFILING.md), burst when the clocks held (clocks_held) else sustained;
+    plus the MMA rate the repo's own probes measured x SMs x the median SM clock under load."""
+    peaks = read_peaks()
+    ratio = 4.0 if dt == "fp4" else 2.0
+    burst, sustained = ratio * peaks["bf16"], ratio * peaks["bf16_sustained"]
+    held = clocks_held(clocks)
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    probe = 2.0 * PROBE_MAC_PER_CLK_SM[dt] * sms * mhz * 1e6 / 1e12
+    return {"peak": burst if held else sustained, "peak_burst": burst, "peak_sustained": sustained,
+            "peak_probe": probe,
+            "peak_basis": "%s dense = %g x bf16 %s %.1f TFLOP/s, %s; %s" % (
+                dt, ratio, "burst" if held else "sustained", peaks["bf16"] if held else peaks["bf16_sustained"],
+                peaks["source"], "SM clock held at max with no throttle reason during the timed region -> burst"
+                if held else "SM clock below max or throttled during the timed region -> sustained"),
+            "peak_probe_basis": "tcgen05 %s probe %d MAC/clk/SM x %d SMs x %.0f MHz (median under load) x 2" % (
+                dt, PROBE_MAC_PER_CLK_SM[dt], sms, mhz)}
+
+
+def roofline_for(kernel: str, macs: float, popc: float, ms: float, clocks, sms: int):
+    """Roofline of one kernel: `macs` algorithmic binary MACs (and `popc` popcounts) per launch in `ms`."""
+    dt = kernel_dtype(kernel)
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    popc_peak = POPC_PER_CLK_SM * sms * sm_max * 1e6
+    if dt is not None:
+        achieved = 2.0 * macs / (ms * 1e-3) / 1e12
+        p = tensor_peak(dt, clocks, sms)
+        r = {"bound": "tensor", "pipe": "tcgen05 kind::%s" % ("mxf4" if dt == "fp4" else "i8"),
+             "unit": "TOPS (%s, 2 x binary MAC)" % ("fp4" if dt == "fp4" else "int8"), "achieved": achieved}
+        r.update(p)
+        r["frac"] = achieved / p["peak"]
+        r["frac_burst"] = achieved / p["peak_burst"]
+        r["frac_sustained"] = achieved / p["peak_sustained"]
+        r["frac_probe"] = achieved / p["peak_probe"]
+        r["popc_equivalent_frac"] = popc / (ms * 1e-3) / popc_peak
+    else:
+        achieved = popc / (ms * 1e-3) / 1e12
+        r = {"bound": "alu", "pipe": "POPC (16/clk/SM, measured: profiles/pipe_probe_r01.txt)", "unit": "Tpopc/s",
+             "achieved": achieved, "peak": popc_peak / 1e12,
+             "peak_basis": "16 POPC/clk/SM x %d SMs x %.0f MHz (sm max clock)" % (sms, sm_max)}
+        r["frac"] = achieved / r["peak"]
+    return r
+
+
 def dominant_roofline(net, spec, mode, stage_ms, stage_launch, images_total, clocks, dev):
-    """Roofline object for the conv layer with the largest live CUDA-event time.
-    POPC-path kernels: algorithmic popcounts / time vs the POPC pipe (16/clk/SM measured, x SMs x max clock).
-    tcgen05 kernels: algorithmic int8 ops (2 x binary MACs) / time vs the int8 dense tensor peak =
-    measured bf16 (sustained: the kernel runs inside a long step) x 2 (nominal i8 : bf16 ratio)."""
+    """Roofline object for the conv layer with the largest live CUDA-event time (roofline_for)."""
     import torch
     popc_img, mac_img = conv_popc_per_image(spec, mode)
     conv_stages = [i for i, Ly in enumerate(spec["layers"]) if Ly["kind"] == "conv"]
@@ -184,24 +252,7 @@ def dominant_roofline(net, spec, mode, stage_ms, stage_launch, images_total, clo
     imgs_per_launch = images_total / launches
     kernel = net.layer_kernel(dom, int(imgs_per_launch))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peaks = read_peaks()
-    if "_tc" in kernel or "_tma_" in kernel:
-        fp4 = "tc4" in kernel  # kind::mxf4 kernels: fp4 dense peak = 4 x bf16 (nominal ratio), else int8 = 2 x bf16
-        ratio = 4.0 if fp4 else 2.0
-        achieved = 2.0 * mac_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3)
-        peak = ratio * peaks["bf16_sustained"] * 1e12
-        r = {"bound": "tensor", "pipe": "tcgen05 kind::mxf4" if fp4 else "tcgen05 kind::i8",
-             "unit": "TOPS (%s, 2 x binary MAC)" % ("fp4" if fp4 else "int8"),
-             "peak_basis": "%s dense = %g x bf16 sustained %.1f TFLOP/s, %s" % (
-                 "fp4" if fp4 else "int8", ratio, peaks["bf16_sustained"], peaks["source"]),
-             "popc_equivalent_frac": popc_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3) /
-                                     (POPC_PER_CLK_SM * sms * sm_max * 1e6)}
-    else:
-        achieved = popc_img[dom] * imgs_per_launch / (ms_per_launch * 1e-3)
-        peak = POPC_PER_CLK_SM * sms * sm_max * 1e6
-        r = {"bound": "alu", "pipe": "POPC (16/clk/SM, measured: profiles/pipe_probe_r01.txt)", "unit": "Tpopc/s",
-             "peak_basis": "16 POPC/clk/SM x %d SMs x %.0f MHz (sm max clock)" % (sms, sm_max)}
+    r = roofline_for(kernel, mac_img[dom] * imgs_per_launch, popc_img[dom] * imgs_per_launch, ms_per_launch, clocks, sms)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -212,9 +263,9 @@ def dominant_roofline(net, spec, mode, stage_ms, stage_launch, images_total, clo
         except (ValueError, KeyError):
             traffic = None
     step_ms = sum(stage_ms)
-    r.update({"kernel": "layer%d %s" % (dom, kernel), "achieved": achieved / 1e12, "peak": peak / 1e12,
-              "frac": achieved / peak, "traffic": traffic, "ms_per_launch": ms_per_launch,
+    r.update({"kernel": "layer%d %s" % (dom, kernel), "traffic": traffic, "ms_per_launch": ms_per_launch,
               "images_per_launch": imgs_per_launch,
+              "algorithmic": "%d binary MAC x 2 ops per image x %d images per launch" % (mac_img[dom], imgs_per_launch),
               "kernel_share_of_step": stage_ms[dom + 1] / step_ms if step_ms else None})
     return r
 
@@ -238,17 +289,54 @@ def run_reference(a, rank, world):
     el = time.perf_counter() - t0
     v = n / el
     line = {"metric": METRIC, "value": v, "unit": "images/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": el * 1e3 / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": el * 1e3 / a.steps, "higher_is_better": True,
+            "scaling": "weak" if a.batch else "strong", "vs_baseline": None,
             "dtype": "i64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "vehicle classifier (PAPER.md Table 2), %s input binarization; oracle sample of %d "
-                                   "images per step (one per host core)" % (a.mode, cores), "batch_per_step": cores},
-            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle",
+            "config": {"workload": "vehicle classifier (PAPER.md Table 2: conv32x5x5+pool, conv32x5x5+pool, FC100, "
+                                   "FC100, FC4), %s input binarization, %d images per step (BASELINE config 5); each "
+                                   "timed step is a bounded sample of %d of them (one per host core)" % (
+                                       a.mode, a.batch * world if a.batch else a.total_batch, cores),
+                       "batch_per_step": cores},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                              "sample": "%d steps x %d images (vehicle net, %s)" % (a.steps, cores, a.mode)},
             "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------------- bnn arm
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def workload(a, world):
+    """(start, n, n_max, total, scaling) of this rank: strong scaling over --total-batch (BASELINE config 5,
+    contiguous shards, dist.shard_total) unless --batch sets a fixed per-GPU batch (weak scaling)."""
+    from paper_1808_00209_b200 import dist as bdist
+    rank = int(os.environ.get("RANK", "0"))
+    if a.batch:
+        start, n = bdist.shard(a.batch, rank)
+        return start, n, a.batch, a.batch * world, "weak"
+    start, n = bdist.shard_total(a.total_batch, rank, world)
+    return start, n, -(-a.total_batch // world), a.total_batch, "strong"
+
+
+def assemble_predictions(logits_all, cls_all, total, world, n_max, scaling):
+    """Global-order predictions from the padded all-gather buffers ([world * n_max, ...], rank r's shard
+    in rows [r * n_max, r * n_max + size_r))."""
+    import torch
+    from paper_1808_00209_b200 import dist as bdist
+    sizes = [bdist.shard_total(total, r, world)[1] if scaling == "strong" else n_max for r in range(world)]
+    return (torch.cat([logits_all[r * n_max:r * n_max + sizes[r]] for r in range(world)]),
+            torch.cat([cls_all[r * n_max:r * n_max + sizes[r]] for r in range(world)]))
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -273,7 +361,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     spec = synth.VEHICLE
     mode = MODES[a.mode]
-    B = a.batch
+    start, B, n_max, total, scaling = workload(a, world)
 
     # weights: identical on every rank (same seed), packed on the device by bnn_pack(SIGN)
     layers = synth.make_weights(spec, mode, a.seed)
@@ -284,19 +372,22 @@ def main():
     elif mode == 2:
         T = torch.tensor([-127.0], device=dev)
     net = bnn.Net(spec["h"], spec["w"], spec["c"], bnn.U8, mode, T, dl, max_batch=min(a.chunk, B))
-    images = synth.images_chunked(rank * B, B, spec["h"], spec["w"], spec["c"], a.seed + 1, device=dev)
+    # this rank's contiguous shard of the seeded stream (4096-image chunks: identical data for any N)
+    images = synth.images_chunked(start, B, spec["h"], spec["w"], spec["c"], a.seed + 1, device=dev)
     L = spec["layers"][-1]["l"]
-    logits = torch.empty((B, L), dtype=torch.int32, device=dev)
-    cls = torch.empty((B,), dtype=torch.int32, device=dev)
+    # prediction buffers padded to the largest shard so the all-gather has equal sizes
+    logits_pad = torch.zeros((n_max, L), dtype=torch.int32, device=dev)
+    cls_pad = torch.full((n_max,), -1, dtype=torch.int32, device=dev)
+    logits, cls = logits_pad[:B], cls_pad[:B]
     if world > 1:
-        logits_all = torch.empty((world * B, L), dtype=torch.int32, device=dev)
-        cls_all = torch.empty((world * B,), dtype=torch.int32, device=dev)
+        logits_all = torch.empty((world * n_max, L), dtype=torch.int32, device=dev)
+        cls_all = torch.empty((world * n_max,), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
     def step():
         net.forward(images, logits, cls)
         if world > 1:
-            bdist.gather_predictions(logits, cls, logits_all, cls_all)
+            bdist.gather_predictions(logits_pad, cls_pad, logits_all, cls_all)
 
     for _ in range(a.warmup):
         step()
@@ -318,26 +409,27 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / a.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * B / (ms * 1e-3)
+    clocks["timed_region_s"] = round(ms * a.steps / 1e3, 3)
+    ms = bdist.max_over_ranks(ms, dev)
+    value = total / (ms * 1e-3)
     # per-stage live kernel times: the same steps again with the library's CUDA events around every
     # launch (kept out of the timed region: events between kernels serialise programmatic launches)
     bnn.set_option("streams", 1)  # one stream here, so a kernel's event time is its own duration
+    net.forward(images, logits, cls)  # warm (first-launch costs stay out of the per-stage times)
+    torch.cuda.synchronize()
+    prof_steps = max(1, min(a.steps, 5))
     net.profile(True)
-    for _ in range(a.steps):
-        step()
+    for _ in range(prof_steps):
+        net.forward(images, logits, cls)
     torch.cuda.synchronize()
     stage_ms, stage_launch = net.profile_read()
     net.profile(False)
     bnn.set_option("streams", 2)
 
     # ---- roofline of the dominant conv kernel (live CUDA-event times of its launches)
-    roofline = dominant_roofline(net, spec, mode, stage_ms, stage_launch, B * a.steps, clocks, dev)
+    roofline = dominant_roofline(net, spec, mode, stage_ms, stage_launch, B * prof_steps, clocks, dev)
     stages = {("pack" if i == 0 else ("layer%d" % (i - 1) if i <= len(spec["layers"]) else "argmax")):
-              round(stage_ms[i] / a.steps, 4) for i in range(len(stage_ms)) if stage_launch[i]}
+              round(stage_ms[i] / prof_steps, 4) for i in range(len(stage_ms)) if stage_launch[i]}
 
     # ---- end to end through bnn_forward_host (pinned host in, host out)
     e2e = None
@@ -346,59 +438,77 @@ def main():
         h_images.copy_(images)
         h_logits = torch.empty((B, L), dtype=torch.int32, pin_memory=True)
         h_cls = torch.empty((B,), dtype=torch.int32, pin_memory=True)
-        ke = max(3, min(a.steps, 10))
+        ke = max(3, min(a.steps, 5))
         net.forward_host(h_images, h_logits, h_cls)  # warm the staging buffers
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(ke):
             net.forward_host(h_images, h_logits, h_cls)
-        el = (time.perf_counter() - t0) / ke
-        if world > 1:
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = bdist.max_over_ranks((time.perf_counter() - t0) / ke, dev)
         assert torch.equal(h_cls, cls.cpu()), "forward_host disagrees with forward"
-        e2e = {"value": world * B / el, "unit": "images/s", "h2d_bytes_per_step": int(h_images.numel()),
-               "d2h_bytes_per_step": int(h_logits.numel() * 4 + h_cls.numel() * 4), "steps": ke,
-               "timing": "wall clock around the synchronous C-ABI call, max over ranks"}
+        e2e = {"value": total / el, "unit": "images/s", "h2d_bytes_per_step": int(h_images.numel()) * world,
+               "d2h_bytes_per_step": int(h_logits.numel() * 4 + h_cls.numel() * 4) * world, "steps": ke,
+               "timing": "wall clock around the synchronous C-ABI call (pinned host images in, host logits/classes "
+                         "out), max over ranks"}
+        del h_images
 
-    # ---- sampled parity against the oracle at this size (not timed)
-    parity = None
+    # ---- predictions of the whole job, in global image order (rank 0)
+    parity, multi = None, None
+    if world > 1:
+        g_logits, g_cls = assemble_predictions(logits_all, cls_all, total, world, n_max, scaling)
+    else:
+        g_logits, g_cls = logits, cls
+    if rank == 0 and world > 1:
+        # the gathered N-GPU predictions must be bit-identical to a 1-GPU pass over the same global batch
+        # (the images are independent, SURVEY row e); rank 0 regenerates the whole batch and runs it alone
+        del images
+        torch.cuda.empty_cache()
+        full = synth.images_chunked(0, total, spec["h"], spec["w"], spec["c"], a.seed + 1, device=dev)
+        ref_l, ref_c = net.forward(full)
+        ok = bool(torch.equal(ref_l, g_logits) and torch.equal(ref_c, g_cls))
+        multi = {"images": total, "gathered_equals_1gpu_pass": ok}
+        del full
+        assert ok, "gathered %d-GPU predictions differ from the 1-GPU pass" % world
     if a.check > 0 and rank == 0:
+        # sampled images spread over the WHOLE job (every shard, incl. the last image) against the oracle
         import numpy as np
         from oracle import oracle as orc
-        idx = np.linspace(0, B - 1, a.check).astype(int)
+        idx = np.unique(np.linspace(0, total - 1, a.check).astype(int))
         om = {0: orc.SIGN, 1: orc.THRESH_RGB, 2: orc.THRESH_GRAY, 3: orc.LBP, -1: orc.NONE}[mode]
         onet = orc.Net(spec["h"], spec["w"], spec["c"], om, None if T is None else T.cpu().numpy(),
                        [dict(Ly, wt=Ly["wt"].numpy()) for Ly in layers])
-        ref_l, ref_c = onet.forward(images[idx].cpu().numpy(), threads=min(len(idx), host_cores()))
-        ok = bool(np.array_equal(logits[idx].cpu().numpy(), ref_l) and np.array_equal(cls[idx].cpu().numpy(), ref_c))
-        parity = {"images_checked": int(len(idx)), "bit_exact": ok}
+        # regenerated from the seeded stream on the device (the CUDA generator's stream, as the timed inputs)
+        sample = torch.cat([synth.images_chunked(int(i), 1, spec["h"], spec["w"], spec["c"], a.seed + 1, device=dev)
+                            for i in idx]).cpu().numpy()
+        ref_l, ref_c = onet.forward(sample, threads=min(len(idx), host_cores()))
+        ok = bool(np.array_equal(g_logits[idx].cpu().numpy(), ref_l) and np.array_equal(g_cls[idx].cpu().numpy(), ref_c))
+        parity = {"images_checked": int(len(idx)), "global_indices": [int(i) for i in idx], "bit_exact": ok}
         assert ok, "sampled parity against the oracle FAILED"
 
     cpu = None
     if not a.no_cpu and rank == 0 and world == 1:
         cores = host_cores()
         v, done, el = oracle_sample(spec, mode, 12.0, cores, a.seed)
-        cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "oracle",
+        cpu = {"value": v, "unit": "images/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": "%d vehicle images (%s), %.1f s on %d threads, one image per thread" % (done, a.mode, el, cores)}
 
     launches = bnn.forward_launches(net, B) * a.steps
     _, mac_img = conv_popc_per_image(spec, mode)
-    tot_mac = sum(mac_img) * B * world
+    tot_mac = sum(mac_img) * total
     line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
             "dtype": "u32", "data": "synthetic",
             "config": {"workload": "vehicle classifier (PAPER.md Table 2: conv32x5x5+pool, conv32x5x5+pool, FC100, "
-                                   "FC100, FC4), %s input binarization, %d images per GPU per step (config 5 shard: "
-                                   "262144 over 8 GPUs)" % (a.mode, B), "batch_per_gpu": B, "global_batch": B * world,
-                       "chunk": min(a.chunk, B), "input": "u8 96x96x3 uniform, resident in HBM",
+                                   "FC100, FC4), %s input binarization, %d images per step over %d GPU(s)%s" % (
+                                       a.mode, total, world, " (BASELINE config 5)" if total == 262144 else ""),
+                       "global_batch": total, "batch_per_gpu": B, "chunk": min(a.chunk, B),
+                       "input": "u8 96x96x3 uniform, resident in HBM",
                        "l2": "inputs (%d MB/GPU) larger than L2; no flush" % (B * 27648 // 2 ** 20),
-                       "parallelism": "dp%d (NCCL all-gather of predictions)" % world},
+                       "parallelism": "dp%d (contiguous shards; NCCL all-gather of predictions)" % world},
             "binary_mac_per_s": tot_mac / (ms * 1e-3), "stage_ms_per_step": stages,
             "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
-            "parity": parity}
+            "parity": parity, "multi_gpu_check": multi}
     if rank == 0:
         print(json.dumps(line), flush=True)
     net.close()
@@ -418,18 +528,36 @@ def _net_for(spec, mode, seed, dev, max_batch):
     return bnn.Net(spec["h"], spec["w"], spec["c"], bnn.U8, mode, T, dl, max_batch=max_batch), layers, T
 
 
-def _timed(fn, steps, warmup):
+def _timed(fn, steps, warmup, min_s: float = 0.0):
+    """ms per call of fn over `steps` calls (more if needed to fill min_s seconds), after `warmup` calls."""
     import torch
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if min_s > 0:
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        steps = max(steps, int(min_s * 1e3 / max(e0.elapsed_time(e1), 1e-3)) + 1)
     e0.record()
     for _ in range(steps):
         fn()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / steps
+
+
+def _timed_clocks(fn, steps, warmup, min_s: float = 0.5):
+    """_timed with the nvidia-smi clock sampler running over the timed region: (ms, clocks)."""
+    import torch
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    time.sleep(0.25)
+    ms = _timed(fn, steps, warmup, min_s)
+    clocks = sampler.stop()
+    return ms, clocks
 
 
 def _emit(d):
@@ -441,6 +569,7 @@ def run_latency(a):
     time; the timer starts after the image is on the device and stops after the last kernel.  Here
     one image = one CUDA-graph replay (bnn_forward_staged), timed with an event pair per image."""
     import torch
+    import paper_1808_00209_b200 as bnn
     from paper_1808_00209_b200 import synth
     dev = torch.device("cuda", 0)
     net, _, _ = _net_for(synth.VEHICLE, 1, a.seed, dev, 64)
@@ -450,6 +579,9 @@ def run_latency(a):
         st_in.copy_(imgs[i:i + 1])
         net.forward_staged(1)
     torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    sampler.start()
+    time.sleep(0.25)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(1000)]
     for i in range(1000):
         st_in.copy_(imgs[i:i + 1])  # the "memory copy" of the paper's protocol, outside the timer
@@ -458,14 +590,50 @@ def run_latency(a):
         ev[i][1].record()
     torch.cuda.synchronize()
     per = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ev)
-    b2b = _timed(lambda: net.forward_staged(1), 1000, 20) * 1e3
+    b2b = _timed(lambda: net.forward_staged(1), 1000, 20, 0.3) * 1e3
+    clocks = sampler.stop()
     _emit({"metric": "latency per image, batch 1 (kernel time)", "value": sum(per) / len(per), "unit": "us",
            "higher_is_better": False, "median_us": per[len(per) // 2], "p99_us": per[int(0.99 * len(per))],
            "back_to_back_us": b2b, "images_per_s_back_to_back": 1e6 / b2b,
            "config": {"workload": "config 1: vehicle classifier, THRESH_RGB, 1000 random images one at a time, "
-                                  "one CUDA graph replay per image"},
+                                  "one CUDA graph replay per image", "kernel": net.layer_kernel(0, 1)},
            "context": "paper: 55.63 us per image on a GTX 1080 (Table 1, PAPER.md:292)",
-           "gpu_launches_per_image": 1})
+           "gpu_launches_per_image": bnn.forward_launches(net, 1), "clocks": clocks})
+
+
+def _stage_profile(net, fn, reps=3):
+    """Per-stage live times (ms per call) of fn on one stream, AFTER a warm call (first-launch costs excluded)."""
+    import torch
+    import paper_1808_00209_b200 as bnn
+    bnn.set_option("streams", 1)
+    fn()
+    torch.cuda.synchronize()
+    net.profile(True)
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    sms, cnt = net.profile_read()
+    net.profile(False)
+    bnn.set_option("streams", 2)
+    return [x / reps for x in sms], [c // reps for c in cnt]
+
+
+def _layer_rooflines(net, spec, mode, stage_ms, stage_cnt, B, clocks):
+    """roofline_for of every conv / dense layer of a net run over B images (live per-stage times)."""
+    import torch
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    popc, macs = conv_popc_per_image(spec, mode)
+    out = []
+    for i in range(len(spec["layers"])):
+        t, c = stage_ms[i + 1], max(1, stage_cnt[i + 1])
+        if t <= 0:
+            continue
+        kernel = net.layer_kernel(i, B // c if c > 1 else B)
+        r = roofline_for(kernel, macs[i] * B / c, popc[i] * B / c, t / c, clocks, sms)
+        out.append({"layer": i, "kernel": kernel, "ms": round(t, 4), "bound": r["bound"], "unit": r["unit"],
+                    "achieved": round(r["achieved"], 1), "peak": round(r["peak"], 1), "frac": round(r["frac"], 4),
+                    **({"frac_probe": round(r["frac_probe"], 4)} if "frac_probe" in r else {})})
+    return out
 
 
 def run_modes(a):
@@ -480,16 +648,16 @@ def run_modes(a):
         net, _, _ = _net_for(synth.VEHICLE, mode, a.seed, dev, B)
         lg = torch.empty((B, 4), dtype=torch.int32, device=dev)
         cls = torch.empty((B,), dtype=torch.int32, device=dev)
-        net.profile(True)
-        ms = _timed(lambda: net.forward(imgs, lg, cls), a.steps, a.warmup)
-        sms, cnt = net.profile_read()
-        net.profile(False)
-        n_calls = a.steps + a.warmup
+        fn = lambda: net.forward(imgs, lg, cls)  # noqa: E731
+        ms, clocks = _timed_clocks(fn, a.steps, a.warmup)
+        st, cnt = _stage_profile(net, fn)
         _, macs = conv_popc_per_image(synth.VEHICLE, mode)
         _emit({"metric": "images/s", "value": B / (ms * 1e-3), "unit": "images/s", "config": {
             "workload": "config 2: vehicle classifier, batch 4096, input binarization %s" % name},
             "ms_per_step": ms, "binary_or_int_mac_per_s": sum(macs) * B / (ms * 1e-3),
-            "stage_ms": [round(x / n_calls, 4) for x, c in zip(sms, cnt) if c]})
+            "stage_ms": {("pack" if i == 0 else "layer%d" % (i - 1) if i <= 5 else "argmax"): round(x, 4)
+                         for i, (x, c) in enumerate(zip(st, cnt)) if c},
+            "layers": _layer_rooflines(net, synth.VEHICLE, mode, st, cnt, B, clocks), "clocks": clocks})
         net.close()
 
 
@@ -509,15 +677,13 @@ def run_alg1(a):
     res = {}
     for name, flag in [("paper_alg1", 1), ("framework", 0)]:
         bnn.set_option("alg1", flag)
-        net.profile(True)
-        ms = _timed(lambda: net.forward(imgs, lg, cls), a.steps, a.warmup)
-        sms, cnt = net.profile_read()
-        net.profile(False)
-        n_calls = a.steps + a.warmup
+        fn = lambda: net.forward(imgs, lg, cls)  # noqa: E731
+        ms, clocks = _timed_clocks(fn, a.steps, a.warmup)
+        st, cnt = _stage_profile(net, fn)
         one = imgs[:1]
         lat = _timed(lambda: net.forward(one, lg[:1], cls[:1]), 200, 20) * 1e3
         res[name] = {"images_per_s": B / (ms * 1e-3), "ms_per_4096": ms, "batch1_us_stream": lat,
-                     "stage_ms": [round(x / n_calls, 4) for x, c in zip(sms, cnt) if c]}
+                     "stage_ms": [round(x, 4) for x, c in zip(st, cnt) if c], "clocks": clocks}
     bnn.set_option("alg1", 0)
     net.close()
     _emit({"metric": "images/s", "value": res["paper_alg1"]["images_per_s"], "unit": "images/s",
@@ -525,6 +691,7 @@ def run_alg1(a):
                                   "net, THRESH_RGB, batch 4096, same B200"},
            "paper_design": res["paper_alg1"], "framework": res["framework"],
            "speedup_framework_over_paper_design": res["framework"]["images_per_s"] / res["paper_alg1"]["images_per_s"],
+           "clocks": res["framework"]["clocks"],
            "context": "paper Table 2 (GTX 1080, batch 1): 42.58 us binarized layers total (PAPER.md:325-331)"})
 
 
@@ -541,47 +708,69 @@ def run_cifar(a):
     imgs = synth.images(B, 32, 32, 3, a.seed + 1, device=dev)
     lg = torch.empty((B, 10), dtype=torch.int32, device=dev)
     cls = torch.empty((B,), dtype=torch.int32, device=dev)
+    fn = lambda: net.forward(imgs, lg, cls)  # noqa: E731
     # the step is timed without per-kernel events (they serialise programmatic launches); per-layer
     # times come from a separate one-stream pass with the library's events
-    ms = _timed(lambda: net.forward(imgs, lg, cls), a.steps, a.warmup)
-    import paper_1808_00209_b200 as bnn
-    bnn.set_option("streams", 1)
-    net.profile(True)
-    for _ in range(3):
-        net.forward(imgs, lg, cls)
-    sms, cnt = net.profile_read()
-    net.profile(False)
-    bnn.set_option("streams", 2)
-    popc, macs = conv_popc_per_image(synth.CIFAR, 1)
-    layer_ms = [x / 3 for x in sms[1:1 + len(popc)]]
-    peak = POPC_PER_CLK_SM * 148 * 1965e6
+    ms, clocks = _timed_clocks(fn, a.steps, a.warmup)
+    st, cnt = _stage_profile(net, fn)
+    _, macs = conv_popc_per_image(synth.CIFAR, 1)
     _emit({"metric": "images/s", "value": B / (ms * 1e-3), "unit": "images/s", "config": {
         "workload": "config 4: CIFAR-10 BinaryNet VGG (2x128C3-MP2-2x256C3-MP2-2x512C3-MP2-1024FC-1024FC-10FC), "
-                    "batch 16384, THRESH_RGB"}, "ms_per_step": ms, "binary_mac_per_s": sum(macs) * B / (ms * 1e-3),
-        "layers": [{"layer": i, "ms": round(t, 4), "popc_frac_of_peak": round(p * B / (t * 1e-3) / peak, 4)}
-                   for i, (t, p) in enumerate(zip(layer_ms, popc))]})
+                    "batch 16384, THRESH_RGB", "chunk": CIFAR_CHUNK}, "ms_per_step": ms,
+        "binary_mac_per_s": sum(macs) * B / (ms * 1e-3),
+        "layers": _layer_rooflines(net, synth.CIFAR, 1, st, cnt, B, clocks), "clocks": clocks})
+    net.close()
 
 
 def run_sweep(a):
     """BASELINE config 3: single binary conv layers, k in {3,5} x C in {64..1024} x H=W in {32..96},
-    batch 256, C_out = C_in, sign threshold, no pool; inputs uniform random words."""
+    batch 256, C_out = C_in, sign threshold, no pool; inputs uniform random words.  Each point: the
+    tensor roofline of its kernel (all run on tcgen05 kind::mxf4), the clocks over its timed region, and
+    the packed output bits of 2 sampled pixels (every channel) against orc_conv_binary_point (Eq. 3 + Eq. 1)."""
+    import numpy as np
     import torch
     import paper_1808_00209_b200 as bnn
+    from oracle import oracle as orc
     from paper_1808_00209_b200 import synth
     dev = torch.device("cuda", 0)
-    peak = POPC_PER_CLK_SM * 148 * 1965e6
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     N = 256
+    rng = np.random.default_rng(a.seed)
     for k in (3, 5):
         for C in (64, 128, 256, 512, 1024):
-            wt = bnn.pack_weights(synth.pm1((C, k, k, C), a.seed + k + C, device=dev))
+            ws = synth.pm1((C, k, k, C), a.seed + k + C)
+            wt = bnn.pack_weights(ws.to(dev))
+            ws_np = ws.numpy()
             for H in (32, 48, 64, 96):
                 x = synth.words((N, H, H, C // 32), a.seed + H + C, device=dev)
                 y = torch.empty((N, H, H, C // 32), dtype=torch.int32, device=dev)
-                ms = _timed(lambda: bnn.conv2d(x, bnn.BITS, C, wt, C, k), 3, 1)
-                popc = N * H * H * C * k * k * (C // 32)
-                _emit({"metric": "binary conv popc/s", "value": popc / (ms * 1e-3), "unit": "popc/s",
-                       "config": {"workload": "config 3 sweep point", "k": k, "c": C, "hw": H, "batch": N},
-                       "ms": ms, "binary_mac_per_s": popc * 32 / (ms * 1e-3), "popc_frac_of_peak": popc / (ms * 1e-3) / peak})
+                fn = lambda: bnn.conv2d(x, bnn.BITS, C, wt, C, k)  # noqa: E731
+                ms, clocks = _timed_clocks(fn, 3, 1, 0.25)
+                y, _ = fn()
+                torch.cuda.synchronize()
+                kernel = "conv_tc4_kernel" if (k == 5 and C <= 64) or (k == 3 and C in (64, 128)) else "conv_tc4_big_kernel"
+                macs = N * H * H * C * k * k * C
+                r = roofline_for(kernel, macs, macs / 32, ms, clocks, sms)
+                # sampled parity: the last pixel of the last image and one random pixel, all C channels
+                checks, ok = 0, True
+                for (i, yy, xx) in [(N - 1, H - 1, H - 1), (int(rng.integers(N)), int(rng.integers(H)), int(rng.integers(H)))]:
+                    # the k x k window (cropped at the map edge, so the -1 padding is the oracle's own)
+                    R = k // 2
+                    y0, x0 = max(0, yy - R), max(0, xx - R)
+                    win = x[i, y0:min(H, yy + R + 1), x0:min(H, xx + R + 1)].cpu().numpy().view(np.uint32)
+                    xi = orc.unpack_channels(win, C)
+                    bits = np.array([orc.sign(orc.conv_binary_point(xi, ws_np[o], yy - y0, xx - x0))
+                                     for o in range(C)], np.int8)
+                    ok = ok and np.array_equal(y[i, yy, xx].cpu().numpy().view(np.uint32), orc.pack(bits))
+                    checks += C
+                _emit({"metric": "binary conv MAC/s", "value": macs / (ms * 1e-3), "unit": "binary MAC/s",
+                       "config": {"workload": "config 3 sweep point", "k": k, "c": C, "hw": H, "batch": N,
+                                  "kernel": kernel}, "ms": ms,
+                       "roofline": {kk: r[kk] for kk in ("bound", "pipe", "unit", "achieved", "peak", "frac",
+                                                         "peak_probe", "frac_probe", "peak_basis")},
+                       "popc_equivalent_frac": r.get("popc_equivalent_frac"),
+                       "parity": {"outputs_checked": checks, "bit_exact": bool(ok)}, "clocks": clocks})
+                assert ok, "sweep point k=%d C=%d H=%d differs from the oracle" % (k, C, H)
                 del x, y
 
 

@@ -102,8 +102,9 @@ BNN_API int bnn_version(void);
  *                   kernel with the pixels as the unsigned int8 operand; 0: the register-staged kernel.
  *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);
  *                   0: one accumulator set (3 CTAs/SM).
- *   "first_exp"     0 (default).  Timing experiments on that kernel (tools/time_first_exp.py); any
- *                   nonzero value skips work and gives WRONG results.  Never set in production.
+ *   "first_exp"     diagnostics build only (libbnn_trace.so, tools/time_first_exp.py): timing experiments
+ *                   that skip work.  libbnn.so does not know the key (BNN_E_ARG) and its kernels contain
+ *                   none of the experiment branches.
  *   "csa"           1 (default): the XOR-popcount conv compresses each kernel row's K XOR words
  *                   with carry-save adders (LOP3) before POPC; 0: one POPC per word (Eq. 4 as printed).
  *   "big_img"       1 (default): the streamed wide-channel conv expands its weights once per call
@@ -120,7 +121,8 @@ BNN_API int bnn_version(void);
  *                   im2col + packing (B = k*k), tiled XOR-popcount GEMM, int32 max-pool, 64-segment
  *                   FC -- as a comparison baseline (u8 SIGN / THRESH_RGB nets,
  *                   k <= 5, no thresholds / flips; else BNN_E_UNSUPPORTED).
- * Results are bit-identical for every setting except "first_exp" (tiling invariance is a parity test).
+ * Results are bit-identical for every setting (tiling / kernel-choice invariance is a parity test):
+ * no option of libbnn.so can make a call return a non-exact result.
  * Returns BNN_OK or BNN_E_ARG for an unknown key. */
 BNN_API int bnn_set_option(const char* key, int value);
 
@@ -193,6 +195,8 @@ BNN_API bnn_status bnn_maxpool(const uint32_t* x, int n, int h, int w, int c, ui
  *   acc : int32 [n, l] or NULL (the logits of a last layer).
  *   cls : int32 [n] argmax over l (first maximum wins, R19), or NULL; needs acc semantics
  *         only, l <= 1024.
+ * Exact for every d: the tensor-core kernel (fp32 accumulators) is used only while d <= 2^24,
+ * wider layers run on the XOR-popcount kernel (int32 accumulators).
  * Errors: BNN_E_ARG, BNN_E_ALIGN, BNN_E_CUDA.
  * ------------------------------------------------------------------------------- */
 BNN_API bnn_status bnn_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,

@@ -111,6 +111,21 @@ def _dev(t: torch.Tensor, name: str):
         raise ValueError("%s must be contiguous" % name)
 
 
+def _dev_typed(t: torch.Tensor | None, name: str, dtypes, numel: int | None = None):
+    """t is None, or a contiguous CUDA tensor of one of `dtypes` (and `numel` elements if given)."""
+    if t is None:
+        return
+    _dev(t, name)
+    if t.dtype not in dtypes:
+        raise TypeError("%s must be %s, got %s" % (name, " / ".join(str(d) for d in dtypes), t.dtype))
+    if numel is not None and t.numel() != numel:
+        raise ValueError("%s must have %d elements, got %d" % (name, numel, t.numel()))
+
+
+_WORDS = (torch.int32, torch.uint32) if hasattr(torch, "uint32") else (torch.int32,)
+_IN_TORCH = {U8: torch.uint8, F32: torch.float32}
+
+
 def _stream(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -230,8 +245,17 @@ class Net:
                  max_batch: int = 8192):
         arr = (_Layer * len(layers))()
         self._keep = [T]
+        if in_dtype not in _IN_TORCH:
+            raise ValueError("in_dtype must be U8 or F32")
+        if mode == THRESH_RGB:
+            _dev_typed(T, "T", (torch.float32,), c)
+        elif mode == THRESH_GRAY:
+            _dev_typed(T, "T", (torch.float32,), 1)
         for i, L in enumerate(layers):
-            _dev(L["wt"], "wt")
+            _dev_typed(L["wt"], "layers[%d].wt" % i, _WORDS)
+            n_out = L["c_out"] if L["kind"] == "conv" else L["l"]
+            _dev_typed(L.get("thr"), "layers[%d].thr" % i, (torch.int32,), n_out)
+            _dev_typed(L.get("flip"), "layers[%d].flip" % i, (torch.uint8,), n_out)
             self._keep += [L["wt"], L.get("thr"), L.get("flip")]
             if L["kind"] == "conv":
                 arr[i] = _Layer(1, L["k"], L["c_out"], L.get("pool", 1), 0, _ptr(L["wt"]), _ptr(L.get("thr")),
@@ -247,11 +271,36 @@ class Net:
         self.n_classes = layers[-1]["l"]
         self.device = layers[0]["wt"].device
 
+    def _check_images(self, images: torch.Tensor, host: bool = False):
+        """The C ABI receives only a pointer and n: the shape and dtype are checked here."""
+        if host:
+            if images.is_cuda or not images.is_contiguous():
+                raise ValueError("forward_host takes a contiguous CPU tensor (pinned for full speed)")
+        else:
+            _dev(images, "images")
+        if images.dim() != 4 or tuple(images.shape[1:]) != (self.h, self.w, self.c):
+            raise ValueError("images must be [n, %d, %d, %d], got %s" % (self.h, self.w, self.c, tuple(images.shape)))
+        if images.dtype != _IN_TORCH[self.in_dtype]:
+            raise TypeError("images must be %s for this net, got %s" % (_IN_TORCH[self.in_dtype], images.dtype))
+
+    def _check_out(self, n: int, logits, cls, host: bool = False):
+        for t, nm, shape in ((logits, "logits", (n, self.n_classes)), (cls, "cls", (n,))):
+            if t is None:
+                continue
+            if host:
+                if t.is_cuda or not t.is_contiguous():
+                    raise ValueError("%s must be a contiguous CPU tensor" % nm)
+            else:
+                _dev(t, nm)
+            if t.dtype != torch.int32 or tuple(t.shape) != shape:
+                raise ValueError("%s must be int32 %s, got %s %s" % (nm, shape, t.dtype, tuple(t.shape)))
+
     def forward(self, images: torch.Tensor, logits: torch.Tensor | None = None, cls: torch.Tensor | None = None,
                 stream=None):
         """bnn_forward: images [n,h,w,c] (CUDA) -> (int32 logits [n, L], int32 cls [n])."""
-        _dev(images, "images")
+        self._check_images(images)
         n = images.shape[0]
+        self._check_out(n, logits, cls)
         if logits is None:
             logits = torch.empty((n, self.n_classes), dtype=torch.int32, device=images.device)
         if cls is None:
@@ -262,7 +311,9 @@ class Net:
 
     def forward_scores(self, images: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, stream=None):
         """bnn_forward_scores: images -> (int32 logits [n, L], fp32 scores [n, L], int32 cls [n])."""
-        _dev(images, "images")
+        self._check_images(images)
+        _dev_typed(scale, "scale", (torch.float32,), self.n_classes)
+        _dev_typed(bias, "bias", (torch.float32,), self.n_classes)
         n = images.shape[0]
         logits = torch.empty((n, self.n_classes), dtype=torch.int32, device=images.device)
         scores = torch.empty((n, self.n_classes), dtype=torch.float32, device=images.device)
@@ -274,9 +325,9 @@ class Net:
     def forward_host(self, images: torch.Tensor, logits: torch.Tensor | None = None, cls: torch.Tensor | None = None,
                      stream=None):
         """bnn_forward_host: HOST images (pinned CPU tensor) -> HOST (logits, cls); synchronous."""
-        if images.is_cuda or not images.is_contiguous():
-            raise ValueError("forward_host takes a contiguous CPU tensor (pinned for full speed)")
+        self._check_images(images, host=True)
         n = images.shape[0]
+        self._check_out(n, logits, cls, host=True)
         if logits is None:
             logits = torch.empty((n, self.n_classes), dtype=torch.int32, pin_memory=True)
         if cls is None:

@@ -6,6 +6,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -55,15 +57,52 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 #define BNN_REQUIRE_ALIGNED(p, name) \
   do { if ((p) != nullptr && !aligned16(p)) return fail(BNN_E_ALIGN, "%s: pointer not 16-byte aligned", name); } while (0)
 
-int g_num_sms = 0;
-int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+// Per-device launch setup.  The dynamic shared-memory opt-in (cudaFuncSetAttribute) and the SM count
+// belong to the CURRENT device, so they are cached per (kernel, device), behind a mutex (the entry
+// points are reentrant and may be called from several threads / for several devices).
+std::mutex g_dev_mu;
+std::map<std::pair<const void*, int>, int> g_dev_cache;  // (kernel or tag, device) -> value
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// value of `key` on the current device, computing it once with f() (outside the lock: f may call CUDA)
+template <typename F>
+int dev_cached(const void* key, F&& f) {
+  const std::pair<const void*, int> k(key, current_device());
+  {
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    auto it = g_dev_cache.find(k);
+    if (it != g_dev_cache.end()) return it->second;
   }
-  return g_num_sms;
+  const int v = f();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  g_dev_cache[k] = v;
+  return v;
+}
+
+int g_num_sms_tag = 0;
+int num_sms() {
+  return dev_cached(&g_num_sms_tag, [] {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, current_device());
+    (void)cudaGetLastError();
+    return n > 0 ? n : 148;
+  });
+}
+
+// dynamic shared-memory opt-in of kfn on the current device (once per device)
+template <typename F>
+void ensure_smem(F kfn, uint32_t dyn_smem) {
+  if (dyn_smem <= 48 * 1024) return;
+  dev_cached(reinterpret_cast<const void*>(kfn), [&] {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+    (void)cudaGetLastError();
+    return 1;
+  });
 }
 
 // tuning / test knobs (bnn_set_option)
@@ -71,17 +110,16 @@ int num_sms() {
 // consumer) from the device's default pool, which keeps freed blocks (release threshold = max) so a
 // steady-state allocation is a pool hit, not a new mapping.
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
-  static int init_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (init_dev != dev) {
+  static int tag = 0;
+  dev_cached(&tag, [] {
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, current_device()) == cudaSuccess) {
       uint64_t keep = ~0ull;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    init_dev = dev;
-  }
+    (void)cudaGetLastError();
+    return 1;
+  });
   return cudaMallocAsync(p, bytes, s);
 }
 
@@ -94,20 +132,20 @@ int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (ki
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
-int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (wrong results unless 0)
-int g_opt_first_tma = 1;
+int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (diagnostics build only; see exp_bits)
+int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
 int g_opt_first_real_tma = 1;  // 1: real u8 first layers (mode NONE) use the TMA kernel (u8 x +/-1 kind::i8)
-unsigned long long* g_trace = nullptr;  // bnn_set_trace
-int g_trace_cap = 0;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
+unsigned long long* g_trace = nullptr;  // bnn_set_trace (diagnostics build)
+int g_trace_cap = 0;
 int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
-int g_opt_pdl = 1;
-int g_opt_alg1 = 0;
+int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
+int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison
 int g_opt_csa = 1;      // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
 int g_opt_big_img = 1;  // 1: the streamed wide-channel conv stages a per-call pre-expanded weight image
-int g_opt_streams = 2;  // bnn_forward over several chunks alternates chunks over 1 or 2 streams  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison  // 1: forward-path kernels are launched with programmatic dependent launch
+int g_opt_streams = 2;  // bnn_forward over several chunks alternates chunks over 1 or 2 streams
 
 // Launch with the programmatic-stream-serialization attribute: the kernel may be scheduled while its
 // stream predecessor is still running; it runs its prologue (barriers, TMEM, weight images) and then
@@ -263,8 +301,7 @@ bnn_status dispatch_conv_first_lp(int k, int nw, const ConvArgs& A, const uint8_
 // Resident CTAs per SM of a 256-thread tcgen05 kernel: registers, shared memory (227 KB usable,
 // ~1 KB reserved per CTA) and TMEM columns (512 per SM).
 template <typename F>
-int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols, int threads = 256) {
-  if (dyn_smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem);
+int tc_occupancy_calc(F kfn, uint32_t dyn_smem, uint32_t tmem_cols, int threads) {
   cudaFuncAttributes fa;
   int regs = 128, static_smem = 2048;
   if (cudaFuncGetAttributes(&fa, kfn) == cudaSuccess) { regs = fa.numRegs; static_smem = (int)fa.sharedSizeBytes; }
@@ -275,12 +312,20 @@ int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols, int threads = 256
   return std::max(1, std::min(std::min(by_regs, by_smem), std::min(by_tmem, 8)));
 }
 
+// ... per (kernel, current device), with the kernel's shared-memory opt-in done on that device
+template <typename F>
+int tc_occupancy(F kfn, uint32_t dyn_smem, uint32_t tmem_cols, int threads = 256) {
+  ensure_smem(kfn, dyn_smem);
+  // key: kernel pointer + 1 byte (distinct from ensure_smem's key for the same kernel)
+  return dev_cached(reinterpret_cast<const char*>(kfn) + 1,
+                    [&] { return tc_occupancy_calc(kfn, dyn_smem, tmem_cols, threads); });
+}
+
 template <int K, int NT, int CIN, int SRC>
 bnn_status launch_conv_first_tc_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   auto kfn = conv_first_tc_kernel<K, NT, CIN, SRC>;
-  static int occ = -1;
   using C = FirstTcCfg<K, NT, CIN, SRC>;
-  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  const int occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -306,9 +351,8 @@ bool use_first_tc(int c_in, int k, int src) {
 template <int K, int NT, int CIN, int SRC>
 bnn_status launch_conv_first_tc_pool_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   auto kfn = conv_first_tc_pool_kernel<K, NT, CIN, SRC>;
-  static int occ = -1;
   using C = FirstTcPoolCfg<K, NT, CIN, SRC>;
-  if (occ < 0) occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
+  const int occ = tc_occupancy(kfn, 0, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -325,16 +369,15 @@ bnn_status launch_conv_first_tc_pool_t(ConvArgs A, const uint8_t* xu8, const flo
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     (void)cudaGetLastError();
-  }
+  });
   return fn;
 }
 
@@ -350,8 +393,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   using C = FirstTmaCfg<K, FP4, DB>;
   auto kfn = conv_first_tma_pool_kernel<K, FP4, DB, REAL>;
   constexpr uint32_t smem = C::NRAW * C::RAW_STRIDE + 2 * C::A_BYTES + C::B_BYTES + 1024;
-  static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
+  const int occ = tc_occupancy(kfn, smem, C::TMEM_COLS, kFirstTmaThreads);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -434,8 +476,7 @@ template <int K, int CW, int NT>
 bnn_status launch_conv_tc_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTcCfg<K, CW, NT>;
   auto kfn = conv_tc_kernel<K, CW, NT>;
-  static int occ = -1;  // CTAs per SM for this instantiation (smem / TMEM bound)
-  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -460,8 +501,7 @@ template <int K, int CG, int NT, int P = 1>
 bnn_status launch_conv_tc4_big_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTc4BigCfg<K, CG, NT, P>;
   auto kfn = conv_tc4_big_kernel<K, CG, NT, P>;
-  static int set = 0;
-  if (!set) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM); set = 1; }
+  ensure_smem(kfn, C::SMEM);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)((A.n + P - 1) / P) * A.tiles_x * A.tiles_y;  // P images per tile
@@ -497,8 +537,7 @@ template <int K, int CW, int NT>
 bnn_status launch_conv_tc4_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTc4Cfg<K, CW, NT>;
   auto kfn = conv_tc4_kernel<K, CW, NT>;
-  static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
+  const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -516,8 +555,7 @@ template <int K>
 bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTc4PoolCfg<K>;
   auto kfn = conv_tc4_pool_kernel<K>;
-  static int occ = -1;
-  if (occ < 0) occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, kTc4PoolThreads);
+  const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, kTc4PoolThreads);
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -704,7 +742,12 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k, int pool) {
 
 // ---------------------------------------------------------------------------- dense
 // Dense layers with a real batch and a long reduction run on the tensor cores (kind::mxf4).
-bool use_dense_tc(int n, int64_t dw) { return g_opt_dense_tc && n >= 256 && dw >= 32 && (dw % 4) == 0; }
+// fp32 accumulation (TMEM, K-split partial sums) is exact only for |acc| <= d <= 2^24: wider layers stay
+// on the integer pipe (dense_kernel), whatever the option says
+constexpr int64_t kDenseTcMaxWords = (int64_t{1} << 24) / 32;
+bool use_dense_tc(int n, int64_t dw) {
+  return g_opt_dense_tc && n >= 256 && dw >= 32 && (dw % 4) == 0 && dw <= kDenseTcMaxWords;
+}
 
 // K-split factor of dense_tc4_kernel (grid.z): split when the tile grid leaves SMs idle (FC1 at 8192
 // images: 64 tiles -> 2); each split then needs at least 4 stages of 16 words
@@ -744,9 +787,7 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     }
     if (A.ks > 1) A.cls = cls;  // the reduction kernel takes the argmax over all l
     auto launch = [&](auto kfn, uint32_t smem) {
-      static int set_nt128 = 0, set_nt256 = 0;
-      int& flag = (nt == 128) ? set_nt128 : set_nt256;
-      if (!flag) { cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); flag = 1; }
+      ensure_smem(kfn, smem);
       dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)groups, (unsigned)A.ks);
       launch_pdl(kfn, grid, dim3(256), smem, s, A);
     };
@@ -811,7 +852,9 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
-  if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }
+#ifdef BNN_TRACE
+  if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }  // diagnostics build only
+#endif
   if (strcmp(key, "dense_ksplit") == 0) { g_opt_dense_ksplit = value; return BNN_OK; }
   if (strcmp(key, "first_real_tma") == 0) { g_opt_first_real_tma = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }

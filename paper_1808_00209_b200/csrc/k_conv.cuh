@@ -40,6 +40,18 @@ struct ConvArgs {
   int trace_cap;
 };
 
+// Timing-experiment bits of the TMA first layer (bnn_set_option "first_exp"): compiled only into the
+// diagnostics build (-DBNN_TRACE, libbnn_trace.so).  In libbnn.so this is the constant 0, so none of the
+// experiment branches exist in the production kernel and no option can make it skip work.
+template <typename Args>
+BNN_DEV constexpr int exp_bits(const Args& A) {
+#ifdef BNN_TRACE
+  return A.exp;
+#else
+  return ((void)A, 0);
+#endif
+}
+
 // Role timestamp of tile iteration `it`, event `ev` (< 16) of CTA (0, 0), SM clock (bnn_set_trace)
 template <typename Args>
 BNN_DEV void trace_ev(const Args& A, int it, int ev) {

@@ -317,7 +317,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           // MMA s: strip row s + 2 * (pooled row), both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
-            if ((A.exp & 8) && s > 0) break;
+            if ((exp_bits(A) & 8) && s > 0) break;
             const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * C::ROWP), C::PLANE, 2 * C::ROWP);
             const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
             tc::mma_i8(d_tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
@@ -348,10 +348,10 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1, slot = it % C::NRAW;
-      wait_x(A.exp, &raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
-      if (it >= 2) wait_x(A.exp, &mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      wait_x(exp_bits(A), &raw_full[slot], (uint32_t)((it / C::NRAW) & 1));
+      if (it >= 2) wait_x(exp_bits(A), &mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
       if (tid == 32) trace_ev(A, it, 12);
-      if (bt < C::GROUPS && !(A.exp & 4)) {
+      if (bt < C::GROUPS && !(exp_bits(A) & 4)) {
         // 2 strips (pooled columns 2j, 2j+1) of strip row r: box bytes [DELTA + 12 j, + 6 + SB)
         constexpr int WB = C::DELTA - C::E;  // 4-byte aligned word base of item 0
         const uint32_t* src = reinterpret_cast<const uint32_t*>(sRaw + slot * C::RAW_STRIDE + r * RAW_W + WB + 12 * j);
@@ -465,7 +465,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
       const int buf = it & 1;
       int img, oy0, ox0;
       tile_origin(tile, img, oy0, ox0);
-      wait_x(A.exp, &mma_done[buf], (uint32_t)((it >> 1) & 1));
+      wait_x(exp_bits(A), &mma_done[buf], (uint32_t)((it >> 1) & 1));
       if (lane == 0) trace_ev(A, it, 2 + warp);  // epilogue warps 6-9 -> events 8-11
       __syncwarp();
       tc::fence_after();
@@ -499,7 +499,7 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         // VIMNMX .S16x2 take the 4-way pool max of two channels per instruction, and the sign bits
         // of 4 channels are gathered by one PRMT (bytes 1 / 3 hold them as bit 7) and one multiply
         // (bits 7, 15, 23, 31 -> 31..28, MSB-first) instead of one funnel shift per channel
-        if (!(A.exp & 3)) {
+        if (!(exp_bits(A) & 3)) {
           packed = true;
 #pragma unroll
           for (int cb = 0; cb < NT; cb += 16) {
@@ -521,11 +521,11 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
           }
         }
       }
-      if (!packed && !(A.exp & 2))
+      if (!packed && !(exp_bits(A) & 2))
 #pragma unroll
       for (int cb = 0; cb < NT; cb += 16) {
         int a[16], b[16], c[16];
-        if (A.exp & 1) {
+        if (exp_bits(A) & 1) {
           tc::tmem_ld16(acc_base + (uint32_t)(0 * NT + cb), a);
           tc::tmem_ld16(acc_base + (uint32_t)(1 * NT + cb), b);
           tc::tmem_ld_wait();

@@ -95,9 +95,17 @@ def test_validation_errors(L):
     doc = hdr[hdr.index("Process-wide tuning"):hdr.index("BNN_API int bnn_set_option")]
     keys = re.findall(r'\*\s+"(\w+)"', doc)
     assert {"conv_algo", "conv_tc", "conv_tc_fp4", "conv_pool_tc", "first_tma", "pdl"} <= set(keys)
-    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 16, "fused_max_n": 0, "alg1": 0, "first_fp4": 0, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1, "dense_ksplit": 1, "first_exp": 0}
+    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 16, "fused_max_n": 0, "alg1": 0, "first_fp4": 0, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1, "dense_ksplit": 1}
     for k in keys:
+        if k == "first_exp":
+            continue
         assert L.bnn_set_option(k.encode(), defaults.get(k, 1)) == 0, k
+    # the production library has no knob that skips work: the timing-experiment key exists only in
+    # the diagnostics build (libbnn_trace.so), and a trace buffer is refused
+    assert "first_exp" in keys
+    for v in (0, 1, 15):
+        assert L.bnn_set_option(b"first_exp", v) == 1
+    assert L.bnn_set_trace(ctypes.c_void_p(16), 16) == 3
     assert L.bnn_forward_launches(None, 5) == 0
 
 
@@ -115,3 +123,24 @@ def test_no_oracle_in_product_path():
             assert "import paper_1808_00209_b200" not in src and "bnn.h" not in src.replace("include/bnn.h", "")
     libs = os.popen("ldd %s" % os.path.join(pkg, "libbnn.so")).read()
     assert "oracle" not in libs
+
+
+def test_binding_validates_before_the_c_call():
+    """The C ABI takes only pointers and n, so the binding checks shapes / dtypes / devices first
+    (a wrong image size would otherwise be read out of bounds)."""
+    import torch
+    import paper_1808_00209_b200 as b
+    net = object.__new__(b.Net)
+    net.h, net.w, net.c, net.in_dtype, net.n_classes = 96, 96, 3, b.U8, 4
+    with pytest.raises(ValueError):  # not a CUDA tensor
+        net._check_images(torch.zeros((2, 96, 96, 3), dtype=torch.uint8))
+    net._check_images(torch.zeros((2, 96, 96, 3), dtype=torch.uint8), host=True)
+    with pytest.raises(ValueError):  # lower resolution
+        net._check_images(torch.zeros((2, 48, 48, 3), dtype=torch.uint8), host=True)
+    with pytest.raises(TypeError):  # f32 pixels for a u8 net
+        net._check_images(torch.zeros((2, 96, 96, 3), dtype=torch.float32), host=True)
+    with pytest.raises(ValueError):  # logits of the wrong width
+        net._check_out(2, torch.zeros((2, 5), dtype=torch.int32), None, host=True)
+    with pytest.raises(ValueError):  # weights must be device tensors: nothing reaches bnn_net_create
+        b.Net(8, 8, 3, b.U8, b.SIGN, None, [dict(kind="conv", k=3, c_out=32, pool=2, wt=torch.zeros((32, 3, 3, 1),
+                                                                                                   dtype=torch.int32))])

@@ -82,3 +82,46 @@ def test_shard_total_covers_everything():
             assert parts[0][0] == 0 and sum(c for _, c in parts) == n
             for (s0, c0), (s1, _) in zip(parts, parts[1:]):
                 assert s0 + c0 == s1
+
+
+def _bench_worker(rank, world, port, total, out_q):
+    """The sharding / padded-gather / reassembly code of bench.py itself (strong scaling over `total`)."""
+    import argparse
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import bench
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = argparse.Namespace(batch=0, total_batch=total)
+    start, n, n_max, tot, scaling = bench.workload(a, world)
+    assert tot == total and scaling == "strong"
+    imgs = synth.images_chunked(start, n, 8, 8, 3, seed=5)
+    lg, cls = _oracle_predict(imgs.numpy())
+    lg_pad = torch.zeros((n_max, lg.shape[1]), dtype=torch.int32)
+    cls_pad = torch.full((n_max,), -1, dtype=torch.int32)
+    lg_pad[:n] = torch.from_numpy(lg.astype(np.int32))
+    cls_pad[:n] = torch.from_numpy(cls.astype(np.int32))
+    g_lg, g_cls = bdist.gather_predictions(lg_pad, cls_pad)
+    if rank == 0:
+        a_lg, a_cls = bench.assemble_predictions(g_lg, g_cls, total, world, n_max, scaling)
+        out_q.put((a_lg.numpy(), a_cls.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 7), (3, 11)])
+def test_gloo_bench_strong_scaling_matches_single_process(world, total):
+    """bench.py's strong-scaling shards (uneven when world does not divide the batch), padded all-gather
+    and reassembly give exactly the single-process predictions in global image order (SURVEY row e)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    g_lg, g_cls = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = synth.images_chunked(0, total, 8, 8, 3, seed=5)
+    lg, cls = _oracle_predict(full.numpy())
+    assert g_lg.shape[0] == total
+    assert np.array_equal(g_lg, lg.astype(np.int32)) and np.array_equal(g_cls, cls.astype(np.int32))
