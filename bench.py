@@ -182,7 +182,7 @@ PROBE_MAC_PER_CLK_SM = {"i8": 8187, "fp4": 16375}  # profiles/umma_probe_r01.txt
 
 def kernel_dtype(kernel: str):
     """Operand type of a kernel family: 'fp4' (tcgen05 kind::mxf4), 'i8' (kind::i8) or None (integer pipe)."""
-    if "tc4" in kernel or kernel.endswith("_fp4"):
+    if "tc4" in kernel or "fp4" in kernel:
         return "fp4"
     if "_tc" in kernel or "_tma_" in kernel:
         return "i8"

@@ -97,7 +97,8 @@ BNN_API int bnn_version(void);
  *   "conv_pool_tc"  1 (default): pooled 32-channel convs fold the 2x2 window into the MMA N.
  *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
- *   "first_fp4"     0 (default): that kernel's operands are int8 (kind::i8); 1: e2m1 (kind::mxf4).
+ *   "first_fp4"     1 (default): binarized pooled u8 first layers run conv1_fp4_pool_kernel (kind::mxf4,
+ *                   {0,1} activations, one CTA per SM); 0: the int8 TMA kernel (kind::i8).
  *   "first_real_tma" 1 (default): pooled real-u8 first layers (mode NONE, c_in = 3) use the same TMA
  *                   kernel with the pixels as the unsigned int8 operand; 0: the register-staged kernel.
  *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);

@@ -21,6 +21,7 @@
 #include "k_conv_tc.cuh"
 #include "k_conv_first_tc.cuh"
 #include "k_conv_first_tma.cuh"
+#include "k_conv1_fp4.cuh"
 #include "k_conv_tc4.cuh"
 #include "k_conv_tc4_pool.cuh"
 #include "k_dense_tc4.cuh"
@@ -130,7 +131,7 @@ int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
-int g_opt_first_fp4 = 0;     // 1: the TMA first layer uses e2m1 operands (kind::mxf4, 3 MMAs per tile, TMEM 256 -> 2 CTAs/SM: measured slower); 0: int8 (6 MMAs)
+int g_opt_first_fp4 = 1;     // 1: the binarized TMA first layer is conv1_fp4_pool_kernel (kind::mxf4, {0,1} operands, 1 CTA/SM); 0: the int8 kernel
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
 int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (diagnostics build only; see exp_bits)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
@@ -419,11 +420,42 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   return check_launch("conv_first_tma_pool_kernel");
 }
 
-// The TMA-fed pooled first layer on a u8 [n, H, W, 3] image (k in {3, 5}), operand type / TMEM
-// buffering per the first_fp4 / first_db options.  A.c_in may be 1 (THRESH_GRAY via luma_u8img4_kernel:
-// channels 1-2 get zero weights).
+// The mxf4 pooled first layer (k_conv1_fp4.cuh): one CTA per SM, {0, 1} activations, TMA-fed.
+template <int K, bool SPIN = false>
+bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
+  using C = Conv1Fp4Cfg<K>;
+  auto kfn = conv1_fp4_pool_kernel<K, SPIN>;
+  const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, C::THREADS);
+  A.trace = g_trace;
+  A.trace_cap = g_trace_cap;
+  A.tiles_y = (A.H + C::TH - 1) / C::TH;
+  A.tiles_x = (A.W + C::TW - 1) / C::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31)) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
+  const cuuint64_t strides[2] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H * A.W * 3};
+  const cuuint32_t box[3] = {(cuuint32_t)C::RAW_W, (cuuint32_t)C::IR, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tma_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xu8), dims, strides, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv1_fp4: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+  dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
+  launch_pdl(kfn, grid, dim3(C::THREADS), C::SMEM, s, A, map, T);
+  return check_launch("conv1_fp4_pool_kernel");
+}
+
+// The TMA-fed pooled first layer on a u8 [n, H, W, 3] image (k in {3, 5}): the mxf4 kernel (first_fp4 = 1,
+// default) or the int8 one (first_fp4 = 0; TMEM double buffering per first_db).  A.c_in may be 1
+// (THRESH_GRAY via luma_u8img4_kernel: channels 1-2 get zero weights).
 bnn_status dispatch_first_tma(int k, const ConvArgs& A, const uint8_t* xu8, const float* T, cudaStream_t s) {
-  if (g_opt_first_fp4) return k == 5 ? launch_conv_first_tma_t<5, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, true>(A, xu8, T, s);
+  if (g_opt_first_fp4 == 2) return k == 5 ? launch_conv1_fp4_t<5, true>(A, xu8, T, s) : launch_conv1_fp4_t<3, true>(A, xu8, T, s);
+  if (g_opt_first_fp4) return k == 5 ? launch_conv1_fp4_t<5>(A, xu8, T, s) : launch_conv1_fp4_t<3>(A, xu8, T, s);
   if (g_opt_first_db) return k == 5 ? launch_conv_first_tma_t<5, false, true>(A, xu8, T, s) : launch_conv_first_tma_t<3, false, true>(A, xu8, T, s);
   return k == 5 ? launch_conv_first_tma_t<5, false>(A, xu8, T, s) : launch_conv_first_tma_t<3, false>(A, xu8, T, s);
 }
@@ -1349,15 +1381,15 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
                           (net->mode == BNN_SIGN || net->mode == BNN_THRESH_RGB || use_luma_tma(net));
     if (first_u8) {
       const bool fp4 = g_opt_first_fp4 != 0;
-      const size_t bb = P.k == 5 ? (fp4 ? FirstTmaCfg<5, true>::B_BYTES : FirstTmaCfg<5, false>::B_BYTES)
-                                 : (fp4 ? FirstTmaCfg<3, true>::B_BYTES : FirstTmaCfg<3, false>::B_BYTES);
+      const size_t bb = P.k == 5 ? (fp4 ? Conv1Fp4Cfg<5>::B_BYTES : FirstTmaCfg<5, false>::B_BYTES)
+                                 : (fp4 ? Conv1Fp4Cfg<3>::B_BYTES : FirstTmaCfg<3, false>::B_BYTES);
       if ((e = cudaMalloc(&P.bimg, (size_t)groups * bb)) != cudaSuccess) break;
       P.bimg_fp4 = fp4 ? 1 : 0;
       if (P.k == 5) {
-        if (fp4) prep_first_tma_kernel<5, true><<<groups, 256>>>(A, P.bimg);
+        if (fp4) prep_conv1_fp4_kernel<5><<<groups, 256>>>(A, P.bimg);
         else prep_first_tma_kernel<5, false><<<groups, 256>>>(A, P.bimg);
       } else {
-        if (fp4) prep_first_tma_kernel<3, true><<<groups, 256>>>(A, P.bimg);
+        if (fp4) prep_conv1_fp4_kernel<3><<<groups, 256>>>(A, P.bimg);
         else prep_first_tma_kernel<3, false><<<groups, 256>>>(A, P.bimg);
       }
     } else if (P.x_dt == BNN_BITS && P.c_in == 32) {
@@ -1649,12 +1681,13 @@ const char* bnn_net_layer_kernel(const bnn_net* net, int layer, int n) {
     if (use_dense_tc(nn, (P.d + 31) / 32)) return "dense_tc4_kernel";
     return nn <= g_opt_gemv_max_n ? "dense_gemv_kernel" : "dense_kernel";
   }
-  if (layer == 0 && use_luma_tma(net)) return "conv_first_tma_pool_kernel";
+  const char* tma_name = g_opt_first_fp4 ? "conv1_fp4_pool_kernel" : "conv_first_tma_pool_kernel";
+  if (layer == 0 && use_luma_tma(net)) return tma_name;
   if (layer == 0 && fused_input(net)) {
     if (use_first_tc(P.c_in, P.k, kSrcThresh)) {
       if (P.pool != 2 || !g_opt_first_pool_tc) return "conv_first_tc_kernel";
       const bool tma = g_opt_first_tma && P.c_in == 3 && (P.k == 3 || P.k == 5) && (P.W * 3) % 16 == 0 && tma_encoder();
-      return tma ? "conv_first_tma_pool_kernel" : "conv_first_tc_pool_kernel";
+      return tma ? tma_name : "conv_first_tc_pool_kernel";
     }
     return use_first_lp(P.c_in, P.k) ? "conv_first_lp_kernel" : "conv_strip_kernel";
   }

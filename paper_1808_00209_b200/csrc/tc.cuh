@@ -145,5 +145,54 @@ BNN_DEV void tmem_ld8_p16(uint32_t taddr, uint32_t (&v)[8]) {
 
 BNN_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 32 consecutive columns of this thread's TMEM lane, low 16 bits of each, packed in pairs (.pack::16b):
+// register j holds column 2j in bits 0-15 and column 2j+1 in bits 16-31.
+BNN_DEV void tmem_ld16_p16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+// Writes v into 32 consecutive TMEM columns of this warp's 32 lanes.
+BNN_DEV void tmem_st32_same(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v));
+}
+
+// ---- variants on precomputed shared-memory addresses, for single-thread-latency-bound loops
+BNN_DEV void mbar_wait_at(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tBNN_WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra BNN_DONEA_%=;\n\tbra BNN_WAITA_%=;\n\tBNN_DONEA_%=:\n\t}\n" ::"r"(bar), "r"(phase) : "memory");
+}
+BNN_DEV void mbar_wait_sleep_at(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tBNN_WAITB_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra BNN_DONEB_%=;\n\tbra BNN_WAITB_%=;\n\tBNN_DONEB_%=:\n\t}\n" ::"r"(bar), "r"(phase), "r"(1000000u)
+      : "memory");
+}
+BNN_DEV void mbar_arrive_at(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// tcgen05.mma (kind::mxf4, cta_group::1) and tcgen05.commit issued by ONE elected lane of a converged
+// warp: every lane runs the loop, so no per-lane issue loop is needed around the instruction
+BNN_DEV void mma_mxf4_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t sfa,
+                            uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %6, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%4], [%5], p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(accumulate));
+}
+BNN_DEV void commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar));
+}
+
 }  // namespace tc
 }  // namespace bnn

@@ -40,10 +40,19 @@ def op_images():
     return synth.images_chunked(0, N_OP, 96, 96, 3, 7001, device="cuda")
 
 
-@pytest.mark.parametrize("mode,thr", [(1, False), (1, True), (2, False), (3, False), (-1, True), (0, False)])
-def test_forward_operating_point(cuda, orc, op_images, mode, thr):
+@pytest.mark.parametrize("mode,thr,fp4", [(1, False, 1), (1, True, 1), (1, True, 0), (2, False, 1), (3, False, 1),
+                                          (-1, True, 1), (0, False, 1)])
+def test_forward_operating_point(cuda, orc, op_images, mode, thr, fp4):
+    cuda.set_option("first_fp4", fp4)  # 1: conv1_fp4_pool_kernel (default), 0: the int8 TMA kernel
+    try:
+        _operating_point(cuda, orc, op_images, mode, thr, fp4)
+    finally:
+        cuda.set_option("first_fp4", 1)
+
+
+def _operating_point(cuda, orc, op_images, mode, thr, fp4):
     net, layers, T = build_net(cuda, synth.VEHICLE, mode, 7100 + mode, max_batch=CHUNK, thr=thr)
-    assert net.layer_kernel(0, CHUNK) == "conv_first_tma_pool_kernel"
+    assert net.layer_kernel(0, CHUNK) == ("conv1_fp4_pool_kernel" if fp4 and mode != -1 else "conv_first_tma_pool_kernel")
     assert net.layer_kernel(1, CHUNK) == "conv_tc4_pool_kernel"
     logits, cls = net.forward(op_images)
     torch.cuda.synchronize()

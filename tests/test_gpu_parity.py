@@ -442,7 +442,7 @@ def test_forward_input_threshold_edges(cuda, orc, algo, T):
         cuda.set_option("conv_algo", 0)
 
 
-@pytest.mark.parametrize("tma", [3, 2, 1, 0])
+@pytest.mark.parametrize("tma", [3, 2, 1, 0])  # 3: mxf4 conv1_fp4 (default); 2 / 1: int8 TMA double / single buffered; 0: no TMA
 @pytest.mark.parametrize("h,w,k,cout,T,mode", [
     (96, 96, 5, 32, None, 1),
     (34, 48, 5, 32, [-128.0, 3.0, -0.5], 1),   # t = (127, -1, 0): out-of-image bytes patched to -1
@@ -467,16 +467,16 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     imgs = synth.images(5, h, w, 3, seed + 2)
     try:
         cuda.set_option("first_tma", 1 if tma else 0)
-        cuda.set_option("first_fp4", 1 if tma == 2 else 0)  # 2: e2m1 operands (kind::mxf4), 1: int8
-        cuda.set_option("first_db", 0 if tma == 1 else 1)   # 1: int8, one accumulator set; 3: int8 double-buffered (default)
+        cuda.set_option("first_fp4", 1 if tma == 3 else 0)
+        cuda.set_option("first_db", 0 if tma == 1 else 1)
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if Tt is None else dev(Tt), dl, max_batch=8)
         if tma:
-            assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
+            assert net.layer_kernel(0, 5) == ("conv1_fp4_pool_kernel" if tma == 3 else "conv_first_tma_pool_kernel")
         lg, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
         cuda.set_option("first_tma", 1)
-        cuda.set_option("first_fp4", 0)
+        cuda.set_option("first_fp4", 1)
         cuda.set_option("first_db", 1)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, Tt).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
@@ -489,7 +489,7 @@ def test_forward_pooled_layers_weight_images(cuda, orc):
     spec = dict(h=32, w=32, c=3, layers=[dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="conv", k=3, c_out=64, pool=2),
                                          dict(kind="dense", l=8)])
     net, layers, T = build_net(cuda, spec, 1, 3100, max_batch=4, thr=True)
-    assert net.layer_kernel(0, 4) == "conv_first_tma_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool_kernel"
+    assert net.layer_kernel(0, 4) == "conv1_fp4_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool_kernel"
     imgs = synth.images(7, 32, 32, 3, 3101)  # two chunks
     lg, cls = net.forward(dev(imgs))
     torch.cuda.synchronize()
@@ -663,7 +663,7 @@ def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, tma):
         cuda.set_option("first_tma", tma)
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if T is None else dev(T), dl, max_batch=8)
         if tma:
-            assert net.layer_kernel(0, 5) == "conv_first_tma_pool_kernel"
+            assert net.layer_kernel(0, 5) == "conv1_fp4_pool_kernel"
         lg, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
@@ -712,7 +712,7 @@ def test_forward_chunked_two_streams_modes(cuda, orc, mode):
     torch.cuda.synchronize()
     ref_l, ref_c = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=8)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
-    assert net.layer_kernel(0, 16) == "conv_first_tma_pool_kernel"
+    assert net.layer_kernel(0, 16) == ("conv_first_tma_pool_kernel" if mode == -1 else "conv1_fp4_pool_kernel")
     # per chunk: (pack / luma kernel unless fused) + 5 layers
     per_chunk = 6 if mode in (2, 3) else 5
     assert cuda.forward_launches(net, 37) == 3 * per_chunk
