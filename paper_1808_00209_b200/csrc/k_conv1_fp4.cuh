@@ -14,8 +14,10 @@
 // rides in B "bias slots" that A fills with 1.0.  TMEM then holds V_q = acc~_q - thr' - 1 for the
 // four pool offsets q = (dy, dx) in N (B holds W shifted by q), and the pooled bit is
 // max_q V_q >= 0 (thr' / flip folding as k_conv_first_tma.cuh, R23).  Every value is an integer with
-// |V| <= 2 * 75 + 151, so the fp32 accumulation is exact however the tensor core orders it (measured
-// exact up to 1.5 * 2^23 by tools/probes/acc_probe.cu).
+// |V| <= 2 * 75 + 151.  Every tile's first MMA (constant operands, block scale 2^20) writes C0 = 1.5 * 2^23
+// into the accumulators; fp32 holds every integer there and the tensor core's accumulation is exact
+// (tools/probes/acc_probe.cu), so the low 16 bits of a result are V as an s16 and the epilogue drains two
+// channels per register.
 //
 // Building A from the u8 bytes: the 16-bit-lane threshold gives per-byte masks (0xFF where x > t_c,
 // R14); a strip of 18 bytes (6 taps x 3 channels) becomes 4 e2m1 words with two LOP per 8 bytes:
@@ -66,13 +68,17 @@ struct Conv1Fp4Cfg {
   static constexpr int NACC = 3;   // TMEM accumulator sets (3 x 128 columns + block scales)
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
   static constexpr uint32_t TMEM_COLS = 512;
-  static constexpr uint32_t SF_COL = NACC * N;  // block scales (all 1.0): SFA at SF_COL, SFB at SF_COL + 8
+  // block scales: SFA at SF_COL and SFB at SF_COL + 8 (all 1.0); SFB of the offset MMA at SF_COL + 16 (2^20)
+  static constexpr uint32_t SF_COL = NACC * N;
+  // the offset MMA's constant operands: A = 1.0 everywhere (128 rows x 2 chunks), B = 6.0 at element 0 of
+  // each 32-element block, scaled by 2^20: D = 2 * 6 * 2^20 = C0 = 1.5 * 2^23 in every accumulator
+  static constexpr uint32_t CONST_BYTES = 2 * 2 * 128 * 16;
   static constexpr int GROUPS = IR * (PW / SPI);  // items per tile
   static constexpr int NB = (GROUPS + 31) / 32;    // builder warps per group (2 groups: tile parity)
   static constexpr int NE = NACC;                  // epilogue groups of 4 warps (group = accumulator set)
   static constexpr int THREADS = 32 * (2 + 2 * NB + 4 * NE);
   static constexpr bool LDS64 = WB % 8 == 0 && (6 * SPI) % 8 == 0;  // item words 8-byte aligned: LDS.64
-  static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + 1024;
+  static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + CONST_BYTES + 1024;
   static_assert(KS % 2 == 0 && GROUPS <= NB * 32, "config");
   static_assert(WB + 4 * NWI + 6 * SPI * (PW / SPI - 1) <= RAW_W && E + 6 * (SPI - 1) + SB <= 4 * NWI,
                 "item words inside the box row");
@@ -183,6 +189,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
   uint8_t* sRaw = dsm;                           // NRAW x RAW_STRIDE
   uint8_t* sA = sRaw + NRAW * C::RAW_STRIDE;     // NA x A_BYTES: [strip row][px][16 B]
   uint8_t* sB = sA + NA * C::A_BYTES;            // B_BYTES
+  uint8_t* sC = sB + C::B_BYTES;                 // CONST_BYTES: offset MMA's A, then its B
   __shared__ int32_t s_bias[NT];  // thr' + 1 (debug acc output)
   __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_free[NA], acc_full[NACC], acc_empty[NACC];
   __shared__ uint64_t w_bar, scale_bar;
@@ -228,6 +235,11 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
   } else {
     stage_b_conv1_fp4<K>(A, g, sB, tid, C::THREADS);
   }
+  for (int i = tid; i < (int)(C::CONST_BYTES / 16); i += C::THREADS) {
+    const bool a_part = i < (int)(C::CONST_BYTES / 32);  // A: e2m1 1.0 everywhere; B: 6.0 at element 0 of a row chunk
+    *reinterpret_cast<uint4*>(sC + 16 * i) = a_part ? make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u)
+                                                    : make_uint4(0x7u, 0u, 0u, 0u);
+  }
   griddep_wait();  // the image and output buffers belong to the predecessors' stream order
   tc::fence_async_smem();
   tc::fence_before();
@@ -239,7 +251,9 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
   if (warp == 0) {
     // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
     constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
-    const uint32_t sfa = tmem + C::SF_COL, sfb = tmem + C::SF_COL + 8;
+    const uint32_t sfa = tmem + C::SF_COL, sfb = tmem + C::SF_COL + 8, sfb_c = tmem + C::SF_COL + 16;
+    const uint64_t adesc_c = tc::desc_kmajor(tc::smem_addr(sC), 128 * 16, 128);
+    const uint64_t bdesc_c = tc::desc_kmajor(tc::smem_addr(sC) + C::CONST_BYTES / 2, 128 * 16, 128);
     const uint32_t a_full0 = tc::smem_addr(&a_full[0]), a_free0 = tc::smem_addr(&a_free[0]);
     const uint32_t acc_full0 = tc::smem_addr(&acc_full[0]), acc_empty0 = tc::smem_addr(&acc_empty[0]);
     // strip rows 2p, 2p + 1 (+ 2 per pooled row): LBO = one strip row, SBO = two; buffer ab at + ab A_BYTES
@@ -264,9 +278,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       tc::fence_after();
       const uint32_t d_tmem = tmem + cb * N;
       const uint64_t ad = adesc0 + (uint64_t)(ab * (C::A_BYTES >> 4));
+      tc::mma_mxf4_elect(d_tmem, adesc_c, bdesc_c, idesc, sfa, sfb_c, 0u);  // D = C0
 #pragma unroll
       for (int p = 0; p < C::NMMA; ++p)
-        tc::mma_mxf4_elect(d_tmem, ad + (uint64_t)(p * ((2 * C::ROWP) >> 4)), bdesc[p], idesc, sfa, sfb, p > 0 ? 1u : 0u);
+        tc::mma_mxf4_elect(d_tmem, ad + (uint64_t)(p * ((2 * C::ROWP) >> 4)), bdesc[p], idesc, sfa, sfb, 1u);
       tc::commit_elect(a_free0 + 8 * ab);
       tc::commit_elect(acc_full0 + 8 * cb);
       trace_ev(A, it, 3);
@@ -395,22 +410,17 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     if (grp == 0) {  // block scales of A (lanes = rows) and B: 1.0 (E8M0 127)
       tc::tmem_st8_same(lane_base + C::SF_COL, 0x7F7F7F7Fu);
       tc::tmem_st8_same(lane_base + C::SF_COL + 8, 0x7F7F7F7Fu);
+      tc::tmem_st8_same(lane_base + C::SF_COL + 16, 0x93939393u);  // 2^20
       tc::tmem_st_wait();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&scale_bar);
     }
-    // pooled bit of channel o = max_q V_q >= 0: the fp32 bit patterns order like int32 about the sign,
-    // so VIMNMX3 + VIMNMX and one funnel shift of the sign bit per channel
-    auto half_bits = [&](const int (&a)[16], const int (&b)[16], const int (&c)[16], const int (&d)[16]) {
-      uint32_t n0 = 0u, n1 = 0u;  // two independent 8-channel chains
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        n0 = __funnelshift_l((uint32_t)max(__vimax3_s32(a[k], b[k], c[k]), d[k]), n0, 1);
-        n1 = __funnelshift_l((uint32_t)max(__vimax3_s32(a[k + 8], b[k + 8], c[k + 8]), d[k + 8]), n1, 1);
-      }
-      return (n0 << 8) | n1;  // 16 sign bits, channel 0 of the half at bit 15
-    };
+    // every tile's first MMA writes C0 = 1.5 * 2^23 (the offset MMA): fp32 still holds every integer there and
+    // the tensor core's accumulation is exact (tools/probes/acc_probe.cu), so the bit pattern of a result is
+    // 0x4B400000 + V and its low 16 bits ARE V as an s16 (|V| <= 301): .pack::16b loads give 2 channels
+    // per register and the pool max runs on s16 pairs
+    constexpr uint32_t C0_BITS = 0x4B400000u;
     uint32_t ph = 0;
 #pragma unroll 1
     for (int tile = blockIdx.x + grp * stride, it = grp; tile < ntiles; tile += NE * stride, it += NE, ph ^= 1u) {
@@ -435,34 +445,31 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
               int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + c0;
               for (int c = 0; c < 16 && g * NT + c0 + c < A.c_out; ++c) {
                 const int o = g * NT + c0 + c;
-                const int a = (int)__int_as_float(vv[c]) + s_bias[c0 + c];
+                const int a = (vv[c] - (int)C0_BITS) + s_bias[c0 + c];
                 dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
               }
             }
           }
       }
-      uint32_t neg;
-      {
-        int a[16], b[16], c[16], d[16];
-        tc::tmem_ld16(acc_base + (uint32_t)(0 * NT), a);
-        tc::tmem_ld16(acc_base + (uint32_t)(1 * NT), b);
-        tc::tmem_ld16(acc_base + (uint32_t)(2 * NT), c);
-        tc::tmem_ld16(acc_base + (uint32_t)(3 * NT), d);
-        tc::tmem_ld_wait();
-        neg = half_bits(a, b, c, d) << 16;
-      }
-      {
-        int a[16], b[16], c[16], d[16];
-        tc::tmem_ld16(acc_base + (uint32_t)(0 * NT + 16), a);
-        tc::tmem_ld16(acc_base + (uint32_t)(1 * NT + 16), b);
-        tc::tmem_ld16(acc_base + (uint32_t)(2 * NT + 16), c);
-        tc::tmem_ld16(acc_base + (uint32_t)(3 * NT + 16), d);
-        tc::tmem_ld_wait();
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0 && quarter == 0) trace_ev(A, it, 8);
-        if (lane == 0) tc::mbar_arrive_at(empty_bar);  // all values are in registers: the MMA may overwrite
-        neg |= half_bits(a, b, c, d);
+      uint32_t a[16], b[16], c[16], d[16];
+      tc::tmem_ld16_p16(acc_base + (uint32_t)(0 * NT), a);
+      tc::tmem_ld16_p16(acc_base + (uint32_t)(1 * NT), b);
+      tc::tmem_ld16_p16(acc_base + (uint32_t)(2 * NT), c);
+      tc::tmem_ld16_p16(acc_base + (uint32_t)(3 * NT), d);
+      tc::tmem_ld_wait();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0 && quarter == 0) trace_ev(A, it, 8);
+      if (lane == 0) tc::mbar_arrive_at(empty_bar);  // all values are in registers: the MMA may overwrite
+      // pooled bit = max_q V_q >= 0: VIMNMX3 + VIMNMX on s16 pairs, then one PRMT + one multiply gather the
+      // sign bits of 4 channels (bytes 1 / 3 hold them as bit 7; bits 7, 15, 23, 31 -> 31..28, MSB-first)
+      uint32_t neg = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t m0 = __vmaxs2(__vimax3_s16x2(a[2 * i], b[2 * i], c[2 * i]), d[2 * i]);
+        const uint32_t m1 = __vmaxs2(__vimax3_s16x2(a[2 * i + 1], b[2 * i + 1], c[2 * i + 1]), d[2 * i + 1]);
+        const uint32_t w = __byte_perm(m0, m1, 0x1357);  // ch 4i+3, 4i+2, 4i+1, 4i
+        neg |= (((w & 0x80808080u) * 0x00204081u) >> 28) << (28 - 4 * i);
       }
       if (ybase != nullptr && in) ybase[(((int64_t)img * Ho + py) * Wo + px) * A.cwo + g] = ~neg & vmask;
     }

@@ -1,7 +1,7 @@
 """Role timeline of conv1_fp4_pool_kernel (bnn_set_trace; diagnostics build): CTA (0,0), SM clock per tile.
 usage: BNN_TRACE_LIB=1 python tools/trace_conv1.py [first_fp4 = 1 (sleep waits) | 2 (spin waits)]
 (after `python -m paper_1808_00209_b200._build --trace`).  Events per tile it: 0 MMA thread before the
-A-ready wait, 1 after it, 2 after the accumulator-free wait, 3 after the commits; 4 builder (group leader)
+ready wait (A built + accumulator set drained), 2 after it, 3 after the commit; 4 builder (group leader)
 after its waits, 5 / 6 builder warps 1 / 5 of the group at A ready; 7 epilogue (quarter 0) at accumulator
 ready, 8 at release."""
 import sys
@@ -39,6 +39,6 @@ for i in list(range(min(n, 12))) + list(range(max(12, n - 6), n)):
 s = slice(8, n)
 d = lambda a, b: float((t[s, b] - t[s, a]).median())  # noqa: E731
 print("median period (commit to commit) %.0f clk" % float((t[9:n, 3] - t[8:n - 1, 3]).median()))
-print("median MMA waits: A %.0f, acc %.0f, issue+commit %.0f clk" % (d(0, 1), d(1, 2), d(2, 3)))
+print("median MMA wait (A ready + accumulator free) %.0f, issue+commit %.0f clk" % (d(0, 2), d(2, 3)))
 print("median builder: go -> warp1 ready %.0f, go -> warp5 ready %.0f clk" % (d(4, 5), d(4, 6)))
 print("median epilogue: ready -> release %.0f clk; commit -> epi ready %.0f clk" % (d(7, 8), d(3, 7)))
