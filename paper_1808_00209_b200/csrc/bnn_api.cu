@@ -426,6 +426,7 @@ bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cu
   using C = Conv1Fp4Cfg<K>;
   auto kfn = conv1_fp4_pool_kernel<K, SPIN>;
   const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, C::THREADS);
+  A.exp = g_opt_first_exp;
   A.trace = g_trace;
   A.trace_cap = g_trace_cap;
   A.tiles_y = (A.H + C::TH - 1) / C::TH;

@@ -64,7 +64,14 @@ struct Conv1Fp4Cfg {
   // r and r+1 fall in different banks (LBO = ROWP, SBO = 2 ROWP; core matrices stay contiguous)
   static constexpr uint32_t ROWP = PW * 16 + 16;
   static constexpr uint32_t A_BYTES = IR * ROWP;
-  static constexpr int NA = 4;     // A buffers
+#ifndef BNN_C1_NA
+#define BNN_C1_NA 4
+#endif
+#ifndef BNN_C1_NBG
+#define BNN_C1_NBG 2
+#endif
+  static constexpr int NA = BNN_C1_NA;     // A buffers (power of 2)
+  static constexpr int NBG = BNN_C1_NBG;   // builder groups (group = tile % NBG)
   static constexpr int NACC = 3;   // TMEM accumulator sets (3 x 128 columns + block scales)
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
   static constexpr uint32_t TMEM_COLS = 512;
@@ -76,7 +83,7 @@ struct Conv1Fp4Cfg {
   static constexpr int GROUPS = IR * (PW / SPI);  // items per tile
   static constexpr int NB = (GROUPS + 31) / 32;    // builder warps per group (2 groups: tile parity)
   static constexpr int NE = NACC;                  // epilogue groups of 4 warps (group = accumulator set)
-  static constexpr int THREADS = 32 * (2 + 2 * NB + 4 * NE);
+  static constexpr int THREADS = 32 * (2 + NBG * NB + 4 * NE);
   static constexpr bool LDS64 = WB % 8 == 0 && (6 * SPI) % 8 == 0;  // item words 8-byte aligned: LDS.64
   static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + CONST_BYTES + 1024;
   static_assert(KS % 2 == 0 && GROUPS <= NB * 32, "config");
@@ -111,6 +118,11 @@ __host__ __device__ constexpr int conv1_bias_slots() {
   return c;
 }
 
+// Output channel held by TMEM column c (0..31) of each pool-offset block: the epilogue ANDs the four offsets'
+// sign bits of the s16 pair (c = 2j, 2j + 1) in register j and shifts them into one word with IMAD.HI, which
+// leaves column 2j at bit j and column 2j + 1 at bit 16 + j; channel o must land on bit 31 - o (Eq. 2).
+__host__ __device__ constexpr int conv1_col_channel(int c) { return (c & 1) ? 15 - (c >> 1) : 31 - (c >> 1); }
+
 // thr' + 1 + S~_o (the bias the MMA subtracts) of output channel o; invalid channels: 1 (V = -1)
 template <int K>
 BNN_DEV int conv1_fp4_bias(const ConvArgs& A, int o) {
@@ -135,7 +147,7 @@ BNN_DEV void stage_b_conv1_fp4(const ConvArgs& A, int g, uint8_t* dst, int i0, i
   static_assert(NSLOT * C::KS * 6 >= 2 * K * K * CIN + 1, "bias slots must hold |thr' + 1 + S| <= 2 K^2 C + 1");
   for (int i = i0; i < C::NMMA * 2 * N; i += step) {
     const int n = i % N, kc = (i / N) & 1, p = i / (2 * N), s = 2 * p + kc;
-    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1, ky = s - dy;
+    const int q = n / NT, o = g * NT + conv1_col_channel(n % NT), dy = q >> 1, dx = q & 1, ky = s - dy;
     const bool ok = o < A.c_out;
     const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
     const int bias = -conv1_fp4_bias<K>(A, o);
@@ -313,7 +325,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       }
     }
     __syncwarp();
-  } else if (warp <= 1 + 2 * NB) {
+  } else if (warp <= 1 + C::NBG * NB) {
     // ------------------------------------------------------------ builders (group = tile parity)
     const int grp = (warp - 2) / NB, bt = tid - 64 - grp * NB * 32;
     int t[CIN];
@@ -335,12 +347,12 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     uint8_t* const a_item = sA + r * C::ROWP + C::SPI * j * 16;
     int it = grp;
 #pragma unroll 1
-    for (int tile = blockIdx.x + grp * stride; tile < ntiles; tile += 2 * stride, it += 2) {
+    for (int tile = blockIdx.x + grp * stride; tile < ntiles; tile += C::NBG * stride, it += C::NBG) {
       const int slot = it % NRAW, ab = it % NA;
       wait_x(SPIN ? 16 : 0, &raw_full[slot], (uint32_t)((it / NRAW) & 1));
       if (it >= NA) wait_x(SPIN ? 16 : 0, &a_free[ab], (uint32_t)(((it / NA) - 1) & 1));
       if (bt == 0) trace_ev(A, it, 4);
-      if (bt < C::GROUPS) {
+      if (bt < C::GROUPS && !(exp_bits(A) & 2)) {  // (diagnostics build: exp bit 2 skips the build)
         const uint8_t* src = sRaw + slot * C::RAW_STRIDE + item_off;
         uint32_t X[C::NWI];
         if constexpr (C::LDS64) {
@@ -397,7 +409,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     }
   } else {
     // ------------------------------------------------------------ epilogue (group = accumulator set)
-    const int ew = warp - 2 - 2 * NB, grp = ew >> 2, quarter = warp & 3;
+    const int ew = warp - 2 - C::NBG * NB, grp = ew >> 2, quarter = warp & 3;
     const int m_row = quarter * 32 + lane, m_py = m_row / PW, m_pxl = m_row % PW;  // pooled pixel of the tile
     const int Ho = A.H >> 1, Wo = A.W >> 1;
     const int nvalid = min(32, A.c_out - g * NT);
@@ -442,14 +454,21 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
             tc::tmem_ld_wait();
             const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
             if (in && oy < A.H && ox < A.W) {
-              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + c0;
-              for (int c = 0; c < 16 && g * NT + c0 + c < A.c_out; ++c) {
-                const int o = g * NT + c0 + c;
-                const int a = (vv[c] - (int)C0_BITS) + s_bias[c0 + c];
-                dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + c0;  // dst[oc - c0]
+              for (int c = 0; c < 16; ++c) {  // TMEM column c0 + c holds channel conv1_col_channel(c0 + c)
+                const int oc = conv1_col_channel(c0 + c), o = g * NT + oc;
+                if (o >= A.c_out) continue;
+                const int a = (vv[c] - (int)C0_BITS) + s_bias[oc];
+                dst[oc - c0] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
               }
             }
           }
+      }
+      if (exp_bits(A) & 1) {  // diagnostics build: exp bit 1 releases the set without draining it
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_at(empty_bar);
+        continue;
       }
       uint32_t a[16], b[16], c[16], d[16];
       tc::tmem_ld16_p16(acc_base + (uint32_t)(0 * NT), a);
@@ -461,15 +480,16 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       __syncwarp();
       if (lane == 0 && quarter == 0) trace_ev(A, it, 8);
       if (lane == 0) tc::mbar_arrive_at(empty_bar);  // all values are in registers: the MMA may overwrite
-      // pooled bit = max_q V_q >= 0: VIMNMX3 + VIMNMX on s16 pairs, then one PRMT + one multiply gather the
-      // sign bits of 4 channels (bytes 1 / 3 hold them as bit 7; bits 7, 15, 23, 31 -> 31..28, MSB-first)
+      // pooled bit = max_q V_q >= 0, i.e. NOT(all four V_q < 0): two LOP3 AND the sign bits (15, 31) of an s16
+      // pair over the offsets and one LEA.HI, (neg >> 1) + x, shifts them into the word (3 ops per 2 channels);
+      // the B column order (conv1_col_channel) makes the result MSB-first
       uint32_t neg = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t m0 = __vmaxs2(__vimax3_s16x2(a[2 * i], b[2 * i], c[2 * i]), d[2 * i]);
-        const uint32_t m1 = __vmaxs2(__vimax3_s16x2(a[2 * i + 1], b[2 * i + 1], c[2 * i + 1]), d[2 * i + 1]);
-        const uint32_t w = __byte_perm(m0, m1, 0x1357);  // ch 4i+3, 4i+2, 4i+1, 4i
-        neg |= (((w & 0x80808080u) * 0x00204081u) >> 28) << (28 - 4 * i);
+      for (int j = 0; j < 16; ++j) {
+        uint32_t x;
+        asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(x) : "r"(a[j]), "r"(b[j]), "r"(c[j]));  // a & b & c
+        x = x & d[j] & 0x80008000u;
+        neg = __umulhi(neg, 0x80000000u) + x;  // (neg >> 1) + x: ptxas emits LEA.HI
       }
       if (ybase != nullptr && in) ybase[(((int64_t)img * Ho + py) * Wo + px) * A.cwo + g] = ~neg & vmask;
     }

@@ -169,6 +169,16 @@ BNN_DEV void mbar_wait_at(uint32_t bar, uint32_t phase) {
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra BNN_DONEA_%=;\n\tbra BNN_WAITA_%=;\n\tBNN_DONEA_%=:\n\t}\n" ::"r"(bar), "r"(phase) : "memory");
 }
+// Waits for two barriers at once: both try_waits are in flight together, so the latency is the larger of
+// the two, not their sum (the loop re-checks both until both phases have completed)
+BNN_DEV void mbar_wait2_at(uint32_t bar1, uint32_t phase1, uint32_t bar2, uint32_t phase2) {
+  asm volatile(
+      "{\n\t.reg .pred P1, P2;\n\tBNN_WAIT2_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P2, [%2], %3;\n\t"
+      "@!P1 bra BNN_WAIT2_%=;\n\t@!P2 bra BNN_WAIT2_%=;\n\t}\n" ::"r"(bar1), "r"(phase1), "r"(bar2), "r"(phase2)
+      : "memory");
+}
 BNN_DEV void mbar_wait_sleep_at(uint32_t bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tBNN_WAITB_%=:\n\t"
