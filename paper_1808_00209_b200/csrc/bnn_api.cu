@@ -793,10 +793,11 @@ int dense_ks(int n, int l, int64_t dw) {
 }
 
 bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt, int l, const int32_t* thr,
-                        const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, cudaStream_t s) {
+                        const uint8_t* flip, uint32_t* y, int32_t* acc, int32_t* cls, cudaStream_t s,
+                        const uint8_t* bimg = nullptr) {
   if (n == 0) return BNN_OK;
   DenseArgs A{};
-  A.x = x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = acc;
+  A.x = x; A.wt = wt; A.thr = thr; A.flip = flip; A.y = y; A.acc = acc; A.bimg = bimg;
   A.cls = (l <= 32) ? cls : nullptr;
   A.n = n; A.l = l; A.lw = (l + 31) / 32; A.d = d; A.dw = (d + 31) / 32;
   constexpr int PI = 8, NWARP = 8, DC = 64;
@@ -1257,12 +1258,12 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
       cur_dt = BNN_BITS;
     } else if (!last) {
       uint32_t* out = net->buf[i & 1];
-      st = launch_dense((const uint32_t*)cur, nb, P.d, P.wt, P.l, P.thr, P.flip, out, nullptr, nullptr, s);
+      st = launch_dense((const uint32_t*)cur, nb, P.d, P.wt, P.l, P.thr, P.flip, out, nullptr, nullptr, s, P.bimg);
       cur = out;
     } else {
       int32_t* lg = logits ? logits : net->logits_tmp;
       st = launch_dense((const uint32_t*)cur, nb, P.d, P.wt, P.l, nullptr, nullptr, nullptr, lg,
-                        P.l <= 32 ? cls : nullptr, s);
+                        P.l <= 32 ? cls : nullptr, s, P.bimg);
       if (st == BNN_OK && cls != nullptr && P.l > 32) {
         ProfScope pa(net, nl + 1, s);
         argmax_kernel<<<grid_for((int64_t)nb * 32, 256), 256, 0, s>>>(lg, nb, P.l, cls);
@@ -1370,10 +1371,27 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
     net_free(net);
     return fail(BNN_E_CUDA, "bnn_net_create: workspace allocation: %s", cudaGetErrorString(e));
   }
-  // Weight operands of the pool-in-N tensor-core kernels, expanded once here (the kernels then stage
-  // them with one bulk copy per CTA instead of re-expanding the packed weights in every CTA).
+  // Weight operands of the pool-in-N tensor-core kernels and of the tensor-core dense layers, expanded
+  // once here (the kernels then stage them with bulk copies instead of re-expanding the packed weights
+  // in every CTA).
   for (size_t i = 0; i < net->L.size() && e == cudaSuccess; ++i) {
     LayerPlan& P = net->L[i];
+    if (P.kind == 2) {
+      // dense layers on the tensor cores at the chunk size: the e2m1 weight image, one bulk copy per stage
+      const int64_t dw = (P.d + 31) / 32;
+      if (!use_dense_tc(std::min(net->chunk, 256), dw)) continue;
+      DenseArgs D{};
+      D.wt = P.wt; D.l = P.l; D.d = P.d; D.dw = dw;
+      const bool wide = P.l > 128;
+      const int nt = wide ? 256 : 128, groups = (P.l + nt - 1) / nt;
+      const int nstage = (int)((dw + DenseTc4Cfg<128>::KC - 1) / DenseTc4Cfg<128>::KC);
+      const size_t bb = wide ? DenseTc4Cfg<256>::B_BYTES : DenseTc4Cfg<128>::B_BYTES;
+      if ((e = cudaMalloc(&P.bimg, (size_t)groups * nstage * bb)) != cudaSuccess) break;
+      if (wide) prep_dense_tc4_kernel<256><<<dim3((unsigned)nstage, (unsigned)groups), 256>>>(D, P.bimg);
+      else prep_dense_tc4_kernel<128><<<dim3((unsigned)nstage, (unsigned)groups), 256>>>(D, P.bimg);
+      e = cudaGetLastError();
+      continue;
+    }
     if (P.kind != 1 || P.pool != 2 || (P.k != 3 && P.k != 5)) continue;
     ConvArgs A{};
     A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.c_in = P.c_in; A.c_out = P.c_out;

@@ -25,6 +25,7 @@ struct DenseArgs {
   int64_t d, dw;
   int ks;        // dense_tc4: K split over gridDim.z (1 = none)
   float* part;   // ks > 1: partial sums [ks][ntiles * 128][gridDim.y * NT] (stream-ordered scratch)
+  const uint8_t* bimg;  // dense_tc4: pre-expanded e2m1 weight image [group][stage][word][NT][16 B] or null
 };
 
 template <int PI, int NWARP, int DC>

@@ -20,8 +20,45 @@ struct DenseTc4Cfg {
   static constexpr uint32_t A_BYTES = KC * 128 * 16;    // 32 KB
   static constexpr uint32_t B_BYTES = KC * NT * 16;
   static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
-  static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 + 16;
+  static constexpr int LUTC = 8;                        // LUT copies (lane & 7): fewer bank conflicts
+  static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 * LUTC + 16;
 };
+
+// The shared-memory image of B for output group g, stage st: [word kw][NT][16 B] (e2m1 +/-1 of the
+// outputs' packed weights, pad bits / rows zero) -- what dense_tc4_kernel expands per stage when no
+// image is given.  Written once per net (prep_dense_tc4_kernel), then bulk-copied per stage.
+template <int NT>
+__global__ void __launch_bounds__(256) prep_dense_tc4_kernel(const DenseArgs A, uint8_t* out) {
+  using C = DenseTc4Cfg<NT>;
+  __shared__ uint32_t lut[256];
+  {
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= (((threadIdx.x >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+    lut[threadIdx.x] = v;
+  }
+  __syncthreads();
+  const int g = blockIdx.y, st = blockIdx.x;
+  const int dw = (int)A.dw, dvalid_last = (int)(A.d - (int64_t)(dw - 1) * 32);
+  uint8_t* dst = out + ((size_t)g * gridDim.x + st) * C::B_BYTES;
+  for (int i = threadIdx.x; i < C::KC * NT; i += blockDim.x) {
+    const int n = i % NT, kw = i / NT, w = st * C::KC + kw, o = g * NT + n;
+    uint32_t o4[4] = {0u, 0u, 0u, 0u};
+    if (o < A.l && w < dw) {
+      expand_word_fp4(__ldg(A.wt + (int64_t)o * A.dw + w), lut, o4);
+      if (w == dw - 1 && dvalid_last < 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t m = 0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m |= (8 * q + k < dvalid_last ? 0xFu : 0u) << (4 * k);
+          o4[q] &= m;
+        }
+      }
+    }
+    *reinterpret_cast<uint4*>(dst + ((size_t)kw * NT + n) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+  }
+}
 
 template <int NT>
 __global__ void __launch_bounds__(256, 1)
@@ -33,8 +70,8 @@ dense_tc4_kernel(const DenseArgs A) {
   uint8_t* sA = dsm;                                  // 2 x [kw][128][16]
   uint8_t* sB = dsm + 2 * C::A_BYTES;                 // 2 x [kw][NT][16]
   float* s_thr = reinterpret_cast<float*>(sB + 2 * C::B_BYTES);
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);
-  __shared__ uint64_t bar_stage[2], bar_acc;
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);  // LUTC interleaved copies: entry i, copy c at LUTC i + c
+  __shared__ uint64_t bar_stage[2], bar_acc, bar_b[2];
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -43,8 +80,11 @@ dense_tc4_kernel(const DenseArgs A) {
     uint32_t v = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) v |= (((tid >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
-    s_lut[tid] = v;
+#pragma unroll
+    for (int c = 0; c < C::LUTC; ++c) s_lut[C::LUTC * tid + c] = v;
   }
+  const uint32_t* my_lut = s_lut + (lane & (C::LUTC - 1));  // this lane's copy (stride LUTC)
+  const bool b_img = A.bimg != nullptr;
   if (tid < NT) {
     const int o = g * NT + tid;
     const int t = (o < A.l && A.thr != nullptr) ? max(-(1 << 24), min(1 << 24, A.thr[o])) : 0;
@@ -55,6 +95,8 @@ dense_tc4_kernel(const DenseArgs A) {
     tc::mbar_init(&bar_stage[0], 1);
     tc::mbar_init(&bar_stage[1], 1);
     tc::mbar_init(&bar_acc, 1);
+    tc::mbar_init(&bar_b[0], 1);
+    tc::mbar_init(&bar_b[1], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -92,6 +134,7 @@ dense_tc4_kernel(const DenseArgs A) {
       ra[q] = (w < dw && img < A.n) ? __ldg(reinterpret_cast<const uint4*>(A.x + (int64_t)img * A.dw + w))
                                     : make_uint4(0, 0, 0, 0);
     }
+    if (b_img) return;
 #pragma unroll
     for (int q = 0; q < PB; ++q) {
       const int i = tid + q * 256;
@@ -108,7 +151,8 @@ dense_tc4_kernel(const DenseArgs A) {
       const int w = w0k + e;
       uint32_t o4[4] = {0u, 0u, 0u, 0u};
       if (valid_row && w < dw) {
-        expand_word_fp4(wv[e], s_lut, o4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o4[q] = my_lut[C::LUTC * ((wv[e] >> (24 - 8 * q)) & 0xFFu)];
         if (w == dw - 1 && dvalid_last < 32) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -136,23 +180,28 @@ dense_tc4_kernel(const DenseArgs A) {
       uint8_t* a = sA + s * C::A_BYTES;
       uint8_t* b = sB + s * C::B_BYTES;
       const int w0 = st * KC;
+      if (b_img && tid == 0)  // the stage's weight operand: one bulk copy of the pre-expanded image (L2-resident)
+        tc::stage_image(b, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES, &bar_b[s]);
 #pragma unroll
       for (int q = 0; q < PA; ++q) {
         const int i = tid + q * 256;
         const int r = i & 127, k4 = i >> 7;
         put4(a, 128, r, w0 + 4 * k4, ra[q], img0 + r < A.n);
       }
+      if (!b_img) {
 #pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        const int i = tid + q * 256;
-        const int n = i % NT, k4 = i / NT;
-        put4(b, NT, n, w0 + 4 * k4, rb[q], g * NT + n < A.l);
+        for (int q = 0; q < PB; ++q) {
+          const int i = tid + q * 256;
+          const int n = i % NT, k4 = i / NT;
+          put4(b, NT, n, w0 + 4 * k4, rb[q], g * NT + n < A.l);
+        }
       }
       tc::fence_async_smem();
       tc::fence_before();
       __syncthreads();
       tc::fence_after();
       if (tid == 0) {
+        if (b_img) tc::mbar_wait(&bar_b[s], (stage_uses >> 1) & 1);  // weight stage landed
         const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(a), 128 * 16, 128);
         const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(b), NT * 16, 128);
 #pragma unroll
