@@ -113,6 +113,8 @@ BNN_API int bnn_version(void);
  *   "streams"       2 (default): bnn_forward alternates chunks over the caller's stream and an
  *                   internal second stream (own workspace; joined back before returning); 1: one.
  *   "dense_tc"      1 (default): dense layers over n >= 256 images run on tensor cores.
+ *   "dense_tma"     1 (default): such a layer's activation stages arrive by TMA (4-deep ring); 0: register
+ *                   prefetch one stage ahead.
  *   "dense_ksplit"  1 (default): such a layer splits K over up to 4 CTA groups (+ a reduction kernel)
  *                   when its 128-image tile grid would leave SMs idle; 0: no split.
  *   "pdl"           1 (default): forward-path kernels use programmatic dependent launch.

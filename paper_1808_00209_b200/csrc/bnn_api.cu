@@ -140,6 +140,7 @@ unsigned long long* g_trace = nullptr;  // bnn_set_trace (diagnostics build)
 int g_trace_cap = 0;
 int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
+int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
 
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
@@ -820,13 +821,31 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
       A.part = part;
     }
     if (A.ks > 1) A.cls = cls;  // the reduction kernel takes the argmax over all l
+    // activation stages by TMA (2-D map over the packed [n, dw] words; dw % 4 == 0 keeps rows 16-byte aligned)
+    CUtensorMap xmap;
+    std::memset(&xmap, 0, sizeof(xmap));
+    bool tmax = g_opt_dense_tma && aligned16(x) && tma_encoder() != nullptr;
+    if (tmax) {
+      const cuuint64_t dims[2] = {(cuuint64_t)A.dw, (cuuint64_t)n};
+      const cuuint64_t strides[1] = {(cuuint64_t)A.dw * 4};
+      const cuuint32_t box[2] = {(cuuint32_t)DenseTc4Cfg<128>::KC, 128};
+      const cuuint32_t estr[2] = {1, 1};
+      tmax = tma_encoder()(&xmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(x), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     auto launch = [&](auto kfn, uint32_t smem) {
       ensure_smem(kfn, smem);
       dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)groups, (unsigned)A.ks);
-      launch_pdl(kfn, grid, dim3(256), smem, s, A);
+      launch_pdl(kfn, grid, dim3(256), smem, s, A, xmap);
     };
-    if (wide) launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM);
-    else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM);
+    if (wide) {
+      if (tmax) launch(dense_tc4_kernel<256, true>, DenseTc4Cfg<256>::SMEM_TMAX);
+      else launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM);
+    } else {
+      if (tmax) launch(dense_tc4_kernel<128, true>, DenseTc4Cfg<128>::SMEM_TMAX);
+      else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM);
+    }
     st = check_launch("dense_tc4_kernel");
     if (st == BNN_OK && A.ks > 1) {
       launch_pdl(dense_tc4_reduce_kernel, dim3((unsigned)((n + 7) / 8)), dim3(256), 0, s, A, groups * nt, ntiles * 128);
@@ -900,6 +919,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_pool_tc") == 0) { g_opt_conv_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
+  if (strcmp(key, "dense_tma") == 0) { g_opt_dense_tma = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 

@@ -21,7 +21,11 @@ struct DenseTc4Cfg {
   static constexpr uint32_t B_BYTES = KC * NT * 16;
   static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
   static constexpr int LUTC = 8;                        // LUT copies (lane & 7): fewer bank conflicts
+  static constexpr int RING = NT > 128 ? 2 : 4;         // TMA ring of raw activation stages (TMAX variant)
+  static constexpr uint32_t RAWB = 128 * KC * 4;        // one raw stage: 128 images x KC words
+  static constexpr uint32_t RAW_OFF = (2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 * LUTC + 127) / 128 * 128;
   static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 * LUTC + 16;
+  static constexpr uint32_t SMEM_TMAX = RAW_OFF + RING * RAWB + 16;
 };
 
 // The shared-memory image of B for output group g, stage st: [word kw][NT][16 B] (e2m1 +/-1 of the
@@ -60,9 +64,12 @@ __global__ void __launch_bounds__(256) prep_dense_tc4_kernel(const DenseArgs A, 
   }
 }
 
-template <int NT>
+// TMAX: the activation stages arrive by TMA (2-D box of KC words x 128 images) in a RING-deep shared
+// ring, issued RING stages ahead, instead of one-stage-ahead register prefetches (whose L2 latency
+// every stage waited for).
+template <int NT, bool TMAX = false>
 __global__ void __launch_bounds__(256, 1)
-dense_tc4_kernel(const DenseArgs A) {
+dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
   griddep_launch();
   using C = DenseTc4Cfg<NT>;
   constexpr int KC = C::KC;
@@ -71,7 +78,8 @@ dense_tc4_kernel(const DenseArgs A) {
   uint8_t* sB = dsm + 2 * C::A_BYTES;                 // 2 x [kw][NT][16]
   float* s_thr = reinterpret_cast<float*>(sB + 2 * C::B_BYTES);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);  // LUTC interleaved copies: entry i, copy c at LUTC i + c
-  __shared__ uint64_t bar_stage[2], bar_acc, bar_b[2];
+  __shared__ uint64_t bar_stage[2], bar_acc, bar_b[2], bar_raw[C::RING];
+  uint8_t* sRaw = dsm + C::RAW_OFF;  // TMAX: RING x [128 images][KC words]
   __shared__ uint32_t tmem_base_s;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -97,6 +105,8 @@ dense_tc4_kernel(const DenseArgs A) {
     tc::mbar_init(&bar_acc, 1);
     tc::mbar_init(&bar_b[0], 1);
     tc::mbar_init(&bar_b[1], 1);
+#pragma unroll
+    for (int i = 0; i < C::RING; ++i) tc::mbar_init(&bar_raw[i], 1);
     tc::fence_mbar_init();
   }
   __syncthreads();
@@ -128,7 +138,7 @@ dense_tc4_kernel(const DenseArgs A) {
   auto load_stage = [&](int img0, int st) {
     const int w0 = st * KC;
 #pragma unroll
-    for (int q = 0; q < PA; ++q) {
+    for (int q = 0; q < (TMAX ? 0 : PA); ++q) {  // TMAX: the activations arrive by TMA
       const int i = tid + q * 256;
       const int r = i & 127, k4 = i >> 7, w = w0 + 4 * k4, img = img0 + r;
       ra[q] = (w < dw && img < A.n) ? __ldg(reinterpret_cast<const uint4*>(A.x + (int64_t)img * A.dw + w))
@@ -170,7 +180,24 @@ dense_tc4_kernel(const DenseArgs A) {
 
   uint32_t stage_uses = 0;  // global stage counter (for mbarrier parity)
   uint32_t acc_uses = 0;
+  const int nst = st1 - st0;
+  // TMAX: stage use u of this CTA -> (tile, stage): raw box into ring slot u % RING
+  auto issue_raw = [&](uint32_t u) {
+    const int t = (int)blockIdx.x + (int)(u / nst) * (int)gridDim.x, st = st0 + (int)(u % nst);
+    if (t >= ntiles) return;
+    uint64_t* bar = &bar_raw[u % C::RING];
+    tc::mbar_arrive_expect_tx(bar, C::RAWB);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            tc::smem_addr(sRaw + (u % C::RING) * C::RAWB)),
+        "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(st * KC), "r"(t * 128), "r"(tc::smem_addr(bar))
+        : "memory");
+  };
   griddep_wait();  // activations of the predecessor layer
+  if constexpr (TMAX) {
+    if (tid == 0)
+      for (uint32_t u = 0; u < (uint32_t)C::RING; ++u) issue_raw(u);
+  }
   if ((int)blockIdx.x < ntiles) load_stage((int)blockIdx.x * 128, st0);
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int img0 = tile * 128;
@@ -182,6 +209,17 @@ dense_tc4_kernel(const DenseArgs A) {
       const int w0 = st * KC;
       if (b_img && tid == 0)  // the stage's weight operand: one bulk copy of the pre-expanded image (L2-resident)
         tc::stage_image(b, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES, &bar_b[s]);
+      if constexpr (TMAX) {
+        const uint32_t slot = stage_uses % C::RING;
+        tc::mbar_wait(&bar_raw[slot], (stage_uses / C::RING) & 1);
+        const uint8_t* raw = sRaw + slot * C::RAWB;
+#pragma unroll
+        for (int q = 0; q < PA; ++q) {
+          const int i = tid + q * 256;
+          const int r = i & 127, k4 = i >> 7;
+          ra[q] = *reinterpret_cast<const uint4*>(raw + (r * KC + 4 * k4) * 4);  // OOB rows / words: zero fill
+        }
+      }
 #pragma unroll
       for (int q = 0; q < PA; ++q) {
         const int i = tid + q * 256;
@@ -201,6 +239,7 @@ dense_tc4_kernel(const DenseArgs A) {
       __syncthreads();
       tc::fence_after();
       if (tid == 0) {
+        if constexpr (TMAX) issue_raw(stage_uses + C::RING);  // the slot was read by every thread (barrier above)
         if (b_img) tc::mbar_wait(&bar_b[s], (stage_uses >> 1) & 1);  // weight stage landed
         const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(a), 128 * 16, 128);
         const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(b), NT * 16, 128);
@@ -213,8 +252,10 @@ dense_tc4_kernel(const DenseArgs A) {
         if (st == st1 - 1) tc::commit(&bar_acc);
       }
       // prefetch the next stage (next tile's first stage after the last one)
-      if (st + 1 < st1) load_stage(img0, st + 1);
-      else if (tile + (int)gridDim.x < ntiles) load_stage((tile + (int)gridDim.x) * 128, st0);
+      if (!TMAX || !b_img) {  // (TMAX: only the weight words, when there is no weight image)
+        if (st + 1 < st1) load_stage(img0, st + 1);
+        else if (tile + (int)gridDim.x < ntiles) load_stage((tile + (int)gridDim.x) * 128, st0);
+      }
     }
     // epilogue: warps 0-3, thread = image
     tc::mbar_wait(&bar_acc, acc_uses & 1);

@@ -305,11 +305,12 @@ def test_dense(cuda, orc, n, d, l):
 
 @pytest.mark.parametrize("n,d,l,flip", [(300, 18432, 100, False), (256, 2040, 10, True), (400, 1024, 300, True),
                                         (129, 4096, 129, False), (8192, 18432, 100, True)])
-@pytest.mark.parametrize("ksplit", [1, 0])
-def test_dense_tensor_core(cuda, orc, n, d, l, flip, ksplit):
+@pytest.mark.parametrize("ksplit,tma", [(1, 1), (0, 1), (1, 0), (0, 0)])
+def test_dense_tensor_core(cuda, orc, n, d, l, flip, ksplit, tma):
     """Large-batch dense on tcgen05 (kind::mxf4): ragged image tiles, d with a partial last word,
     l > 256 (two output groups), thresholds + flips, fused argmax (l <= NT) or the argmax kernel;
-    ksplit = 1: K split over grid.z + the reduction kernel where the tile grid is small (FC1 shapes)."""
+    ksplit = 1: K split over grid.z + the reduction kernel where the tile grid is small (FC1 shapes);
+    tma = 1: activation stages by TMA into a shared ring (out-of-range rows / words zero-filled)."""
     xs = synth.pm1((n, d), 95 + d)
     ws = synth.pm1((l, d), 96 + l)
     t = synth.int_thresholds(l, 97, -40, 41)
@@ -317,11 +318,13 @@ def test_dense_tensor_core(cuda, orc, n, d, l, flip, ksplit):
     xp = cuda.pack(dev(xs).view(n, 1, 1, d)).view(n, -1)
     try:
         cuda.set_option("dense_ksplit", ksplit)
+        cuda.set_option("dense_tma", tma)
         y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None if f is None else dev(f),
                                  want_acc=True, want_cls=True)
         torch.cuda.synchronize()
     finally:
         cuda.set_option("dense_ksplit", 1)
+        cuda.set_option("dense_tma", 1)
     acc, y, cls = acc.cpu().numpy(), u32(y), cls.cpu().numpy()
     for i in range(0, n, 7 if n < 1000 else 331):
         ra = orc.dense(xs[i].numpy(), ws.numpy())
