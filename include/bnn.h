@@ -99,6 +99,9 @@ BNN_API int bnn_version(void);
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
  *   "first_fp4"     1 (default): binarized pooled u8 first layers run conv1_fp4_pool_kernel (kind::mxf4,
  *                   {0,1} activations, one CTA per SM); 0: the int8 TMA kernel (kind::i8).
+ *   "luma_fused"    1 (default): a THRESH_GRAY net's first layer computes the luma from the raw RGB box itself
+ *                   (no intermediate image); 2: LBP nets too (slower than the pre-pass, a comparison path);
+ *                   0: both go through luma_u8img4_kernel's 0/1 image.
  *   "first_real_tma" 1 (default): pooled real-u8 first layers (mode NONE, c_in = 3) use the same TMA
  *                   kernel with the pixels as the unsigned int8 operand; 0: the register-staged kernel.
  *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);

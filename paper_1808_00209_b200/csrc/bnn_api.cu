@@ -135,6 +135,7 @@ int g_opt_first_fp4 = 1;     // 1: the binarized TMA first layer is conv1_fp4_po
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
 int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (diagnostics build only; see exp_bits)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
+int g_opt_luma_fused = 1;    // 1: THRESH_GRAY nets compute the luma inside conv1_fp4 (no 0/1 image in HBM); 2: LBP too
 int g_opt_first_real_tma = 1;  // 1: real u8 first layers (mode NONE) use the TMA kernel (u8 x +/-1 kind::i8)
 unsigned long long* g_trace = nullptr;  // bnn_set_trace (diagnostics build)
 int g_trace_cap = 0;
@@ -422,10 +423,10 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
 }
 
 // The mxf4 pooled first layer (k_conv1_fp4.cuh): one CTA per SM, {0, 1} activations, TMA-fed.
-template <int K, bool SPIN = false>
+template <int K, bool SPIN = false, int BIN = kBinRgb>
 bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cudaStream_t s) {
   using C = Conv1Fp4Cfg<K>;
-  auto kfn = conv1_fp4_pool_kernel<K, SPIN>;
+  auto kfn = conv1_fp4_pool_kernel<K, SPIN, BIN>;
   const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, C::THREADS);
   A.exp = g_opt_first_exp;
   A.trace = g_trace;
@@ -440,7 +441,7 @@ bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cu
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
   const cuuint64_t strides[2] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H * A.W * 3};
-  const cuuint32_t box[3] = {(cuuint32_t)C::RAW_W, (cuuint32_t)C::IR, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)C::RAW_W, (cuuint32_t)(C::IR + (BIN == kBinLbp ? 2 : 0)), 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = tma_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(xu8), dims, strides, box,
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -920,6 +921,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "conv_tc_fp4") == 0) { g_opt_conv_tc_fp4 = value; return BNN_OK; }
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
   if (strcmp(key, "dense_tma") == 0) { g_opt_dense_tma = value; return BNN_OK; }
+  if (strcmp(key, "luma_fused") == 0) { g_opt_luma_fused = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 
@@ -1167,6 +1169,14 @@ bool use_luma_tma(const bnn_net* net) {
          net->packed_in_words * 4 >= (int64_t)P.H * P.W * 3;
 }
 
+// THRESH_GRAY (luma_fused >= 1) / LBP (luma_fused == 2) with the luma computed inside conv1_fp4_pool_kernel
+// (no luma pre-pass).  LBP's in-kernel neighbour pass is byte-granular and measured slower than the
+// pre-pass (config 2: 5.6 vs 9.4 M images/s), so LBP keeps luma_u8img4_kernel by default.
+bool luma_fused(const bnn_net* net) {
+  const bool mode_ok = net->mode == BNN_THRESH_GRAY ? g_opt_luma_fused >= 1 : (net->mode == BNN_LBP && g_opt_luma_fused == 2);
+  return mode_ok && g_opt_first_fp4 && use_luma_tma(net);
+}
+
 // Small batches of a vehicle-shaped net run as one cooperative kernel (k_fused_small.cuh).
 bool use_fused_small(const bnn_net* net, int nb) {
   if (nb < 1 || nb > g_opt_fused_max_n || net->fused_ctr == nullptr || net->fused_w1 == nullptr) return false;
@@ -1237,6 +1247,26 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     cur = net->buf[0];
     cur_dt = BNN_BITS;
     first = 1;
+  } else if (luma_fused(net)) {
+    // THRESH_GRAY / LBP fused into the first layer: the builders compute the integer luma from the raw RGB box
+    const LayerPlan& P = net->L[0];
+    ProfScope ps(net, 1, s);
+    ConvArgs A{};
+    A.wt = P.wt; A.thr = P.thr; A.flip = P.flip; A.y = net->buf[0];
+    A.n = nb; A.H = P.H; A.W = P.W; A.cw = 1; A.c_in = P.c_in; A.c_out = P.c_out;
+    A.cwo = (P.c_out + 31) / 32; A.pool = P.pool;
+    A.bimg = (P.bimg_fp4 == 1) ? P.bimg : nullptr;
+    bnn_status st;
+    if (net->mode == BNN_LBP)
+      st = P.k == 5 ? launch_conv1_fp4_t<5, false, kBinLbp>(A, (const uint8_t*)images, nullptr, s)
+                    : launch_conv1_fp4_t<3, false, kBinLbp>(A, (const uint8_t*)images, nullptr, s);
+    else
+      st = P.k == 5 ? launch_conv1_fp4_t<5, false, kBinGray>(A, (const uint8_t*)images, net->T, s)
+                    : launch_conv1_fp4_t<3, false, kBinGray>(A, (const uint8_t*)images, net->T, s);
+    if (st != BNN_OK) return st;
+    cur = net->buf[0];
+    cur_dt = BNN_BITS;
+    first = 1;
   } else if (use_luma_tma(net)) {
     {
       ProfScope ps(net, 0, s);
@@ -1297,7 +1327,7 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
 
 int launches_per_chunk(const bnn_net* net, bool want_cls, int nb) {
   if (use_fused_small(net, nb)) return 1;
-  int n = (net->mode != BNN_MODE_NONE && !fused_input(net) ? 1 : 0) + (int)net->L.size();
+  int n = (net->mode != BNN_MODE_NONE && !fused_input(net) && !luma_fused(net) ? 1 : 0) + (int)net->L.size();
   if (want_cls && net->L.back().l > 32) n += 1;
   for (const LayerPlan& P : net->L)  // K-split dense layers add their reduction kernel
     if (P.kind == 2 && dense_ks(nb, P.l, (P.d + 31) / 32) > 1) n += 1;

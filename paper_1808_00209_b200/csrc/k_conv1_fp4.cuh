@@ -51,7 +51,15 @@ struct Conv1Fp4Cfg {
   static constexpr int C0 = (WB - XOFF + 3 * 32) % 3;   // channel of box byte WB (box byte 16 = channel 0)
   static constexpr int RAW_W = 80;
   static constexpr uint32_t RAW_BYTES = IR * RAW_W;
-  static constexpr uint32_t RAW_STRIDE = (RAW_BYTES + 127) / 128 * 128;
+  static constexpr uint32_t RAW_BYTES_LBP = (IR + 2) * RAW_W;  // kBinLbp box: one more row above and below
+  static constexpr uint32_t RAW_STRIDE = (RAW_BYTES_LBP + 127) / 128 * 128;
+  // kBinLbp per builder group: luma of box pixels k = 2 .. IC + 3 (LW columns) x IR + 2 rows, and the
+  // synthetic box (IR rows x RAW_W bytes) of neighbour bits
+  static constexpr int LW = IC + 2, LP = (LW + 3) / 4 * 4;
+  static constexpr int KL0 = (XOFF / 3) - R - 1;  // box pixel k sits at box byte 1 + 3 k (image column ox0 - 5 + k)
+  static_assert(XOFF == 16, "box pixel k <-> box byte 1 + 3 k, image column ox0 - 5 + k");
+  static constexpr uint32_t LUMA_BYTES = (IR + 2) * LP, SYN_BYTES = IR * RAW_W;
+  static constexpr uint32_t LBP_BYTES = 2 * (LUMA_BYTES + SYN_BYTES);
   static constexpr int NRAW = 8;
   static constexpr int KS = K + 1;     // strip rows of one pooled row's window (dy = 0, 1)
   static constexpr int SB = KS * CIN;  // data bytes of a strip (6 taps x 3 channels for K = 5)
@@ -85,7 +93,7 @@ struct Conv1Fp4Cfg {
   static constexpr int NE = NACC;                  // epilogue groups of 4 warps (group = accumulator set)
   static constexpr int THREADS = 32 * (2 + NBG * NB + 4 * NE);
   static constexpr bool LDS64 = WB % 8 == 0 && (6 * SPI) % 8 == 0;  // item words 8-byte aligned: LDS.64
-  static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + CONST_BYTES + 1024;
+  static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + CONST_BYTES + LBP_BYTES + 1024;
   static_assert(KS % 2 == 0 && GROUPS <= NB * 32, "config");
   static_assert(WB + 4 * NWI + 6 * SPI * (PW / SPI - 1) <= RAW_W && E + 6 * (SPI - 1) + SB <= 4 * NWI,
                 "item words inside the box row");
@@ -190,18 +198,29 @@ BNN_DEV void conv1_nibbles(const uint32_t (&m)[5], uint32_t (&v)[4]) {
   }
 }
 
-template <int K, bool SPIN = false>
+// Input binarization of the builders (Section 2.3):
+//   kBinRgb  : per-channel thresholds, bit_c = x_c > t_c (THRESH_RGB / SIGN, and 0/1 images with t = 0)
+//   kBinGray : THRESH_GRAY fused: Y = (299 R + 587 G + 114 B + 500) div 1000 (R15) from the raw RGB box,
+//              bit = Y > t, i.e. 299 R + 587 G + 114 B >= 1000 (t + 1) - 500 (two DP2A per pixel); the
+//              layer's c_in = 1 (channels 1, 2 of each strip tap carry zero weights)
+//   kBinLbp  : LBP fused (R16): the box holds one extra row above and below; each builder group first
+//              computes the luma of the box pixels (shared memory), then the three neighbour bits of every
+//              tile pixel (replicate border) as 0xFF / 0x00 bytes in a synthetic box that the item build reads
+constexpr int kBinRgb = 0, kBinGray = 1, kBinLbp = 2;
+
+template <int K, bool SPIN = false, int BIN = kBinRgb>
 __global__ void __launch_bounds__(Conv1Fp4Cfg<K>::THREADS, 1)
 conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
   using C = Conv1Fp4Cfg<K>;
-  constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W, N = C::N, NT = C::NT;
+  constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, RAW_W = C::RAW_W, N = C::N, NT = C::NT, IR_ = C::IR;
   constexpr int CIN = C::CIN, NB = C::NB, NA = C::NA, NACC = C::NACC, NRAW = C::NRAW, NE = C::NE;
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sRaw = dsm;                           // NRAW x RAW_STRIDE
   uint8_t* sA = sRaw + NRAW * C::RAW_STRIDE;     // NA x A_BYTES: [strip row][px][16 B]
   uint8_t* sB = sA + NA * C::A_BYTES;            // B_BYTES
   uint8_t* sC = sB + C::B_BYTES;                 // CONST_BYTES: offset MMA's A, then its B
+  uint8_t* sLbp = sC + C::CONST_BYTES;           // kBinLbp: per builder group [luma | synthetic box]
   __shared__ int32_t s_bias[NT];  // thr' + 1 (debug acc output)
   __shared__ uint64_t raw_full[NRAW], raw_empty[NRAW], a_full[NA], a_free[NA], acc_full[NACC], acc_empty[NACC];
   __shared__ uint64_t w_bar, scale_bar;
@@ -315,11 +334,13 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
         int img, oy0, ox0;
         tile_origin((int)blockIdx.x + it * stride, img, oy0, ox0);
         const uint32_t bar = raw_full0 + 8 * slot;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(C::RAW_BYTES) : "memory");
+        constexpr uint32_t box_bytes = BIN == kBinLbp ? C::RAW_BYTES_LBP : C::RAW_BYTES;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(box_bytes) : "memory");
         asm volatile(
             "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
                 raw0 + slot * C::RAW_STRIDE),
-            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(ox0 * CIN - C::XOFF), "r"(oy0 - R), "r"(img), "r"(bar)
+            "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(ox0 * CIN - C::XOFF), "r"(oy0 - R - (BIN == kBinLbp ? 1 : 0)),
+            "r"(img), "r"(bar)
             : "memory");
         slot = (slot + 1 == NRAW) ? 0 : slot + 1;
       }
@@ -332,9 +353,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     bool zero_ok = true;  // an all-zero (out-of-image) byte thresholds to b = 0 (-1) for every channel
 #pragma unroll
     for (int c = 0; c < CIN; ++c) {
-      t[c] = (Tt != nullptr) ? u8_threshold(-Tt[c]) : 0;
+      t[c] = (Tt != nullptr && (BIN == kBinRgb || c == 0)) ? u8_threshold(-Tt[c]) : 0;
       zero_ok = zero_ok && t[c] >= 0;
     }
+    const int gray_lim = 1000 * (t[0] + 1) - 500;  // kBinGray: luma bit <=> s >= gray_lim (t in [-1, 255])
     uint32_t Ev[3], Od[3];
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
@@ -352,8 +374,43 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       wait_x(SPIN ? 16 : 0, &raw_full[slot], (uint32_t)((it / NRAW) & 1));
       if (it >= NA) wait_x(SPIN ? 16 : 0, &a_free[ab], (uint32_t)(((it / NA) - 1) & 1));
       if (bt == 0) trace_ev(A, it, 4);
+      const uint8_t* box = sRaw + slot * C::RAW_STRIDE;
+      if constexpr (BIN == kBinLbp) {
+        // phase 1: luma of box pixel (row rr, column k = kk + 2); box pixel k starts at box byte 1 + 3 k
+        uint8_t* lum = sLbp + grp * (C::LUMA_BYTES + C::SYN_BYTES);
+        uint8_t* syn = lum + C::LUMA_BYTES;
+        for (int idx = bt; idx < (IR_ + 2) * C::LW; idx += NB * 32) {
+          const int rr = idx / C::LW, kk = idx - rr * C::LW, k = kk + C::KL0;
+          const uint8_t* p = box + rr * RAW_W + 1 + 3 * k;
+          const uint32_t sy = 299u * p[0] + 587u * p[1] + 114u * p[2];
+          lum[rr * C::LP + kk] = (uint8_t)((sy + 500u) / 1000u);  // R15
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NB * 32) : "memory");
+        // phase 2: neighbour bits (R16: TL, R, BL; strict >; replicate border) of tile pixel (strip row r2,
+        // column k = kk + 3), channel j at synthetic box byte 1 + 3 k + j; out-of-image pixels stay -1
+        int img, oy0, ox0;
+        tile_origin(tile, img, oy0, ox0);
+        for (int idx = bt; idx < IR_ * (C::LW - 2); idx += NB * 32) {
+          const int r2 = idx / (C::LW - 2), kc = idx - r2 * (C::LW - 2) + 1, k = kc + C::KL0;
+          const int gy = oy0 - R + r2, gx = ox0 - 5 + k;
+          uint32_t b3 = 0u;
+          if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) {
+            const int rr = r2 + 1;
+            const int ru = gy > 0 ? rr - 1 : rr, rd = gy + 1 < A.H ? rr + 1 : rr;
+            const int kl = gx > 0 ? kc - 1 : kc, kr = gx + 1 < A.W ? kc + 1 : kc;
+            const int y = lum[rr * C::LP + kc];
+            b3 = (lum[ru * C::LP + kl] > y ? 0xFFu : 0u) | (lum[rr * C::LP + kr] > y ? 0xFF00u : 0u) |
+                 (lum[rd * C::LP + kl] > y ? 0xFF0000u : 0u);
+          }
+          uint8_t* q = syn + r2 * RAW_W + 1 + 3 * k;
+          q[0] = (uint8_t)b3;
+          q[1] = (uint8_t)(b3 >> 8);
+          q[2] = (uint8_t)(b3 >> 16);
+        }
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NB * 32) : "memory");
+      }
       if (bt < C::GROUPS && !(exp_bits(A) & 2)) {  // (diagnostics build: exp bit 2 skips the build)
-        const uint8_t* src = sRaw + slot * C::RAW_STRIDE + item_off;
+        const uint8_t* src = (BIN == kBinLbp ? sLbp + grp * (C::LUMA_BYTES + C::SYN_BYTES) + C::LUMA_BYTES : box) + item_off;
         uint32_t X[C::NWI];
         if constexpr (C::LDS64) {
 #pragma unroll
@@ -367,9 +424,28 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
           for (int w = 0; w < C::NWI; ++w) X[w] = reinterpret_cast<const uint32_t*>(src)[w];
         }
         uint32_t M[C::NWI];  // 0xFF where the byte is b = 1 (x > t_c, R14)
+        if constexpr (BIN == kBinLbp) {
 #pragma unroll
-        for (int w = 0; w < C::NWI; ++w) M[w] = thresh_mask4(X[w], Ev[(C::C0 + w) % 3], Od[(C::C0 + w) % 3]);
-        if (!zero_ok) {  // out-of-image bytes must be b = 0 whatever the threshold (uniform branch)
+          for (int w = 0; w < C::NWI; ++w) M[w] = X[w];  // the synthetic box holds the bits as bytes
+        } else if constexpr (BIN == kBinRgb) {
+#pragma unroll
+          for (int w = 0; w < C::NWI; ++w) M[w] = thresh_mask4(X[w], Ev[(C::C0 + w) % 3], Od[(C::C0 + w) % 3]);
+        } else {
+          // pixel m of the item starts at item byte E + 3 m (a strip start is a pixel start); its channel-0
+          // byte carries the luma bit, channels 1 and 2 stay 0 (zero weights)
+          constexpr int NPIX_I = (6 * (C::SPI - 1) + C::SB) / 3;
+#pragma unroll
+          for (int w = 0; w < C::NWI; ++w) M[w] = 0u;
+#pragma unroll
+          for (int m = 0; m < NPIX_I; ++m) {
+            const int i = C::E + 3 * m, wi = i >> 2, oi = i & 3;
+            const uint32_t rgb = __byte_perm(X[wi], wi + 1 < C::NWI ? X[wi + 1] : 0u,
+                                             (uint32_t)(oi | ((oi + 1) << 4) | ((oi + 2) << 8)));
+            const uint32_t sy = __dp2a_hi(114u, rgb, __dp2a_lo((587u << 16) | 299u, rgb, 0u));  // 299R + 587G + 114B
+            M[wi] |= ((int)sy >= gray_lim ? 0xFFu : 0u) << (8 * oi);
+          }
+        }
+        if (BIN != kBinLbp && !zero_ok) {  // out-of-image bytes must be b = 0 whatever the threshold (uniform branch)
           int img, oy0, ox0;
           tile_origin(tile, img, oy0, ox0);
           const int gy = oy0 - R + r;

@@ -642,13 +642,19 @@ def test_forward_scores_vehicle(cuda, orc, mode):
 
 
 # ------------------------------------------------------------------------------------ GRAY / LBP first layer
-@pytest.mark.parametrize("tma", [1, 0])
-@pytest.mark.parametrize("h,w,k,cout", [(32, 48, 5, 32), (18, 16, 3, 40), (34, 64, 5, 64)])
+@pytest.mark.parametrize("tma", [2, 1, 0])
+@pytest.mark.parametrize("h,w,k,cout,T", [(32, 48, 5, 32, -100.0), (18, 16, 3, 40, -100.0), (34, 64, 5, 64, -100.0),
+                                          (32, 48, 5, 32, 5.0), (32, 16, 3, 32, -255.5)])
 @pytest.mark.parametrize("mode", [2, 3])
-def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, tma):
-    """THRESH_GRAY (c_in = 1: zero weights on the two dummy channels) and LBP through luma_u8img4_kernel
-    + the TMA-fed first layer (tma = 1) or the packed-bit path (tma = 0), with BN thresholds / flips on
-    the first layer, ragged tiles and channel groups, against the oracle."""
+def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, T, tma):
+    """THRESH_GRAY (c_in = 1: zero weights on the two dummy channels) and LBP: luma (and the LBP neighbour
+    bits, replicate border) computed inside the TMA-fed first layer (tma = 2), luma_u8img4_kernel + the
+    TMA-fed first layer (tma = 1) or the
+    packed-bit path (tma = 0), with BN thresholds / flips on the first layer, ragged tiles and channel
+    groups, against the oracle.  GRAY T = -100 (Y + T = 0 ties), 5 (every pixel +1: the out-of-image
+    bytes must still be -1), -255.5 (every pixel -1)."""
+    if mode == 3 and T != -100.0:
+        pytest.skip("T applies to THRESH_GRAY only")
     cin = 1 if mode == 2 else 3
     tail = [dict(kind="conv", k=1, c_out=32, pool=1)] if cout % 32 else []
     spec = dict(h=h, w=w, c=3, layers=[dict(kind="conv", k=k, c_out=cout, pool=2)] + tail + [dict(kind="dense", l=10)])
@@ -659,18 +665,22 @@ def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, tma):
     layers[0]["flip"] = synth.flips(cout, seed + 1)
     dl = [dict(L, wt=cuda.pack_weights(dev(L["wt"]))) for L in layers]
     dl[0]["thr"], dl[0]["flip"] = dev(layers[0]["thr"]), dev(layers[0]["flip"])
-    T = torch.tensor([-100.0]) if mode == 2 else None  # integer T: Y + T = 0 ties occur
+    T = torch.tensor([T]) if mode == 2 else None  # integer T: Y + T = 0 ties occur
     imgs = synth.images(5, h, w, 3, seed + 2)
     imgs[0, :3, :3] = 100
     try:
-        cuda.set_option("first_tma", tma)
+        cuda.set_option("first_tma", 1 if tma else 0)
+        cuda.set_option("luma_fused", 2 if tma == 2 else 0)
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if T is None else dev(T), dl, max_batch=8)
         if tma:
             assert net.layer_kernel(0, 5) == "conv1_fp4_pool_kernel"
         lg, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
+        if tma == 2:
+            assert cuda.forward_launches(net, 5) == len(spec["layers"]), "no luma pre-pass"
     finally:
         cuda.set_option("first_tma", 1)
+        cuda.set_option("luma_fused", 1)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
@@ -716,8 +726,8 @@ def test_forward_chunked_two_streams_modes(cuda, orc, mode):
     ref_l, ref_c = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=8)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
     assert net.layer_kernel(0, 16) == ("conv_first_tma_pool_kernel" if mode == -1 else "conv1_fp4_pool_kernel")
-    # per chunk: (pack / luma kernel unless fused) + 5 layers
-    per_chunk = 6 if mode in (2, 3) else 5
+    # per chunk: 5 layers (+ LBP's luma pre-pass; GRAY computes its luma inside conv1; NONE reads the pixels)
+    per_chunk = 6 if mode == 3 else 5
     assert cuda.forward_launches(net, 37) == 3 * per_chunk
 
 
