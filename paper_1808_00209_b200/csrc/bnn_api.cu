@@ -28,6 +28,7 @@
 #include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
 #include "k_fused_small.cuh"
+#include "k_fused_cluster.cuh"
 #include "k_alg1.cuh"
 #include "k_pack.cuh"
 
@@ -143,6 +144,7 @@ int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
 
+int g_opt_fused_cluster = 1;  // 1: the fused small-batch path is the thread-block-cluster kernel (DSMEM, cluster barriers); 0: cooperative
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
 int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison
@@ -922,6 +924,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "dense_tc") == 0) { g_opt_dense_tc = value; return BNN_OK; }
   if (strcmp(key, "dense_tma") == 0) { g_opt_dense_tma = value; return BNN_OK; }
   if (strcmp(key, "luma_fused") == 0) { g_opt_luma_fused = value; return BNN_OK; }
+  if (strcmp(key, "fused_cluster") == 0) { g_opt_fused_cluster = value; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 
@@ -1215,9 +1218,81 @@ bnn_status launch_fused_small(bnn_net* net, const void* images, int nb, int32_t*
   return check_launch("fused_small_kernel");
 }
 
+// Cluster size of fused_cluster_kernel on the current device: 16 (non-portable) if the device runs a
+// 16-CTA cluster of it, else 8; 0 if neither (then the cooperative kernel serves)
+template <typename F>
+int fused_cluster_size(F kfn, size_t smem) {
+  return dev_cached(reinterpret_cast<const char*>(kfn) + 2, [&] {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int cs : {kClusterMax, 8}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)cs);
+      cfg.blockDim = dim3(kFusedWarps * 32);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = (unsigned)cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters >= 1) {
+        (void)cudaGetLastError();
+        return cs;
+      }
+      (void)cudaGetLastError();
+    }
+    return 0;
+  });
+}
+
+bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s,
+                                bool* launched) {
+  *launched = false;
+  const LayerPlan &a = net->L[0], &b = net->L[1], &d1 = net->L[2], &d2 = net->L[3], &d3 = net->L[4];
+  FusedSmallArgs A{};
+  A.x = (const uint8_t*)images; A.T = (net->mode == BNN_THRESH_RGB) ? net->T : nullptr;
+  A.n = nb; A.H = net->h; A.W = net->w; A.C = net->c; A.K1 = a.k; A.K2 = b.k;
+  A.w1 = a.wt; A.w1p = net->fused_w1; A.thr1 = a.thr; A.flip1 = a.flip; A.w2 = b.wt; A.thr2 = b.thr; A.flip2 = b.flip;
+  A.f1 = d1.wt; A.f2 = d2.wt; A.f3 = d3.wt; A.thr_f1 = d1.thr; A.thr_f2 = d2.thr; A.flip_f1 = d1.flip; A.flip_f2 = d2.flip;
+  A.l1 = d1.l; A.l2 = d2.l; A.l3 = d3.l;
+  A.logits = logits; A.cls = cls;
+  const size_t smem = fused_cluster_smem(net->h, net->w);
+  if (smem > 200 * 1024) return BNN_OK;
+  auto go = [&](auto kfn) -> bnn_status {
+    const int cs = fused_cluster_size(kfn, smem);
+    if (cs == 0) return BNN_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cs);
+    cfg.blockDim = dim3(kFusedWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kfn, A);
+    *launched = true;
+    return check_launch("fused_cluster_kernel");
+  };
+  if (b.k == 5) return go(fused_cluster_kernel<5>);
+  if (b.k == 3) return go(fused_cluster_kernel<3>);
+  return go(fused_cluster_kernel<1>);
+}
+
 bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logits, int32_t* cls, cudaStream_t s) {
   if (use_fused_small(net, nb)) {
     ProfScope ps(net, 1, s);
+    if (g_opt_fused_cluster) {
+      bool launched = false;
+      const bnn_status st = launch_fused_cluster(net, images, nb, logits, cls, s, &launched);
+      if (st != BNN_OK || launched) return st;
+    }
     return launch_fused_small(net, images, nb, logits, cls, s);
   }
   const void* cur = images;

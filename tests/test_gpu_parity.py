@@ -376,11 +376,12 @@ def oracle_net(orc, spec, mode, layers, T):
     return orc.Net(spec["h"], spec["w"], spec["c"], om, None if T is None else T.numpy(), ol)
 
 
-@pytest.mark.parametrize("fused", [8, 0])
+@pytest.mark.parametrize("fused", [8, -8, 0])
 @pytest.mark.parametrize("mode", [1, 2, 3, -1, 0])
 def test_forward_vehicle(cuda, orc, mode, fused):
-    """All input modes end to end; fused = 8: batches of <= 8 images run as the single cooperative
-    whole-network kernel (RGB / SIGN), fused = 0: layer by layer."""
+    """All input modes end to end; fused = 8: batches of <= 8 images run as one thread-block cluster
+    (whole network, activations in DSMEM; RGB / SIGN), -8: the cooperative whole-network kernel,
+    0: layer by layer."""
     forward_vehicle_case(cuda, orc, mode, fused)
 
 
@@ -388,11 +389,13 @@ def forward_vehicle_case(cuda, orc, mode, fused):
     net, layers, T = build_net(cuda, synth.VEHICLE, mode, 500 + mode)
     imgs = synth.images(6, 96, 96, 3, 600 + mode)
     try:
-        cuda.set_option("fused_max_n", fused)
+        cuda.set_option("fused_max_n", abs(fused))
+        cuda.set_option("fused_cluster", 0 if fused < 0 else 1)
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
         cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_cluster", 1)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=6)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
@@ -547,13 +550,14 @@ def test_forward_host_equals_forward(cuda):
     assert cuda.forward_launches(net, 9000) == 3 * 6  # pack-fused conv1, conv2, FC1 (+ K-split reduction), FC2, FC3
 
 
-@pytest.mark.parametrize("fused", [8, 0])
+@pytest.mark.parametrize("fused", [8, -8, 0])
 @pytest.mark.parametrize("pdl", [1, 0])
 def test_forward_staged_graph(cuda, orc, pdl, fused):
     """The graph-replayed latency path (config 1) equals the oracle, for n = 1 and n = 3, and a
     replay after new images were staged uses the new images."""
     cuda.set_option("pdl", pdl)  # programmatic dependent launch between the graph's kernels
-    cuda.set_option("fused_max_n", fused)  # one cooperative whole-network kernel per replay
+    cuda.set_option("fused_max_n", abs(fused))  # one whole-network kernel per replay
+    cuda.set_option("fused_cluster", 0 if fused < 0 else 1)  # cluster (8) or cooperative (-8) kernel
     try:
         net, layers, T = build_net(cuda, synth.VEHICLE, 1, 1400, max_batch=64)
         onet = oracle_net(orc, synth.VEHICLE, 1, layers, T)
@@ -569,6 +573,7 @@ def test_forward_staged_graph(cuda, orc, pdl, fused):
     finally:
         cuda.set_option("pdl", 1)
         cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_cluster", 1)
 
 
 def test_forward_cifar(cuda, orc):
