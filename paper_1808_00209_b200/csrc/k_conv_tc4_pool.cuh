@@ -39,7 +39,8 @@ struct ConvTc4PoolCfg {
   static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
   static constexpr uint32_t TMEM_COLS = 256;       // N accumulator columns + block scales
   static constexpr int PF = (NPIX + 255) / 256;
-  static constexpr uint32_t SMEM = B_BYTES + 2 * A_BYTES + 256 * 4 + NT * 4 + 64;
+  static constexpr int LUTC = 8;  // interleaved LUT copies (lane & 7): fewer bank conflicts in the loaders
+  static constexpr uint32_t SMEM = B_BYTES + 2 * A_BYTES + 256 * 4 * (1 + LUTC) + NT * 4 + 64;
   static_assert(KS % 2 == 0 && PW + (KS - 1) / 2 <= CH, "window");
 };
 
@@ -49,6 +50,10 @@ BNN_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
       "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
+
+// Output channel of TMEM column c (0..31) of each pool-offset block: the epilogue's LEA.HI shift leaves
+// column 2j at bit j and column 2j + 1 at bit 16 + j of the packed word; channel o belongs at bit 31 - o.
+__host__ __device__ constexpr int tc4_col_channel(int c) { return (c & 1) ? 15 - (c >> 1) : 31 - (c >> 1); }
 
 // The shared-memory image of the weight operand for channel group g ([mma][K chunk][N][16 B]):
 // MMA i = (row pair sp, window column t), K-chunk kc -> window row s = 2 sp + kc; column
@@ -61,7 +66,7 @@ BNN_DEV void stage_b_tc4_pool(const ConvArgs& A, int g, uint8_t* dst, const uint
   for (int i = i0; i < C::NMMA * 2 * N; i += step) {
     const int n = i % N, kc = (i / N) & 1, mi = i / (2 * N);
     const int sp = mi / KS, t = mi % KS, s = 2 * sp + kc;
-    const int q = n / NT, o = g * NT + n % NT, dy = q >> 1, dx = q & 1;
+    const int q = n / NT, o = g * NT + tc4_col_channel(n % NT), dy = q >> 1, dx = q & 1;
     const int ky = s - dy, kx = t - dx;
     uint32_t o4[4] = {0u, 0u, 0u, 0u};
     if (o < A.c_out && ky >= 0 && ky < K && kx >= 0 && kx < K) {
@@ -116,8 +121,9 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sB = dsm;                                              // [mma][K-chunk][N][16]
   uint8_t* sA = dsm + C::B_BYTES;                                 // 2 x [plane][row][colhalf][16]
-  uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries
-  float* s_init = reinterpret_cast<float*>(s_lut + 256);             // -(thr' + 1) per channel
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries (weight staging)
+  uint32_t* s_lutr = s_lut + 256;                                      // LUTC interleaved copies (loaders)
+  float* s_init = reinterpret_cast<float*>(s_lutr + 256 * C::LUTC);   // C0 - (thr' + 1) per TMEM column
   __shared__ uint64_t a_full[2], mma_done[2], acc_empty, w_bar;
   __shared__ uint32_t tmem_base_s;
 
@@ -125,15 +131,21 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   const int g = blockIdx.y;
   const int stride = gridDim.x, ntiles = (int)A.total_tiles;  // < 2^31 (host check)
   const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
-  if (tid < 256) fill_lut_fp4(s_lut, tid);
+  if (tid < 256) {
+    fill_lut_fp4(s_lut, tid);
+#pragma unroll
+    for (int c = 0; c < C::LUTC; ++c) s_lutr[C::LUTC * tid + c] = s_lut[tid];
+  }
   if (tid < NT) {
-    const int o = g * NT + tid;
+    const int o = g * NT + tc4_col_channel(tid);
     const bool ok = o < A.c_out;
     const bool f = ok && A.flip != nullptr && A.flip[o] != 0;
     int tt = (ok && A.thr != nullptr) ? A.thr[o] : 0;
     tt = max(-S_TOT - 1, min(S_TOT, tt));
     if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
-    s_init[tid] = ok ? -(float)(tt + 1) : -1.0f;  // invalid channels: acc' = -1 -> bit 0
+    // start value C0 - (thr' + 1), C0 = 1.5 * 2^23: the result's fp32 bit pattern is 0x4B400000 + acc' and its
+    // low 16 bits are acc' as an s16 (exact: tools/probes/acc_probe.cu); invalid channels: acc' = -1 -> bit 0
+    s_init[tid] = 12582912.0f - (float)(ok ? tt + 1 : 1);
   }
   if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
   if (tid == 0) {
@@ -241,7 +253,9 @@ conv_tc4_pool_kernel(const ConvArgs A) {
         if (p < NPIX) {
           const int r = p / IC, c = p - r * IC;
           uint32_t o4[4];
-          expand_word_fp4(pref[q], s_lut, o4);
+          const uint32_t* my_lut = s_lutr + (lane & (C::LUTC - 1));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o4[k] = my_lut[C::LUTC * ((pref[q] >> (24 - 8 * k)) & 0xFFu)];
           *reinterpret_cast<uint4*>(a + (c & 1) * C::PLANE + r * C::ROWB + (c >> 1) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
         }
       }
@@ -260,6 +274,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
     const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    static_assert(NT == 32, "two 16-column start-value blocks");
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
       const int buf = it & 1;
@@ -280,47 +295,46 @@ conv_tc4_pool_kernel(const ConvArgs A) {
             tc::tmem_ld_wait();
             const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
             if (in && oy < A.H && ox < A.W) {
-              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT + cb;
-              for (int c = 0; c < 16 && g * NT + cb + c < A.c_out; ++c) {
-                const int o = g * NT + cb + c;
+              int32_t* dst = A.acc + (((int64_t)img * A.H + oy) * A.W + ox) * A.c_out + g * NT;
+              for (int c = 0; c < 16; ++c) {  // TMEM column cb + c holds channel tc4_col_channel(cb + c)
+                const int oc = tc4_col_channel(cb + c), o = g * NT + oc;
+                if (o >= A.c_out) continue;
                 const int a = (int)(__int_as_float(vv[c]) - s_init[cb + c]);
-                dst[c] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
+                dst[oc] = (A.flip != nullptr && A.flip[o] != 0) ? -a : a;
               }
             }
           }
       }
-      uint32_t neg = 0, negp[4] = {0u, 0u, 0u, 0u};
+      // acc' of the 4 pool offsets as s16 pairs (low halves of C0 + acc', .pack::16b), then the next tile's
+      // start values, then release: the MMA may run while the sign bits are gathered
+      uint32_t a[16], b[16], c[16], d[16];
+      tc::tmem_ld16_p16(lane_base + (uint32_t)(0 * NT), a);
+      tc::tmem_ld16_p16(lane_base + (uint32_t)(1 * NT), b);
+      tc::tmem_ld16_p16(lane_base + (uint32_t)(2 * NT), c);
+      tc::tmem_ld16_p16(lane_base + (uint32_t)(3 * NT), d);
+      tc::tmem_ld_wait();
 #pragma unroll
-      for (int cb = 0; cb < NT; cb += 16) {
-        int a[16], b[16], c[16];
-        tc::tmem_ld16(lane_base + (uint32_t)(0 * NT + cb), a);
-        tc::tmem_ld16(lane_base + (uint32_t)(1 * NT + cb), b);
-        tc::tmem_ld_wait();
+      for (int cb = 0; cb < NT; cb += 16) {  // start values (broadcast shared loads: few live registers)
+        uint32_t iv[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) a[k] = max(a[k], b[k]);
-        tc::tmem_ld16(lane_base + (uint32_t)(2 * NT + cb), b);
-        tc::tmem_ld16(lane_base + (uint32_t)(3 * NT + cb), c);
-        tc::tmem_ld_wait();
+        for (int k = 0; k < 16; ++k) iv[k] = __float_as_uint(s_init[cb + k]);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {  // 4 independent 8-channel shift chains (ILP), merged below
-          uint32_t& nk = negp[(cb + k) >> 3];
-          nk = __funnelshift_l((uint32_t)__vimax3_s32(a[k], b[k], c[k]), nk, 1);
-        }
-      }
-      neg = (negp[0] << 24) | (negp[1] << 16) | (negp[2] << 8) | negp[3];
-      // start values for the next tile's accumulation
-#pragma unroll
-      for (int cb = 0; cb < NT; cb += 16) {
-        uint32_t initv[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) initv[k] = __float_as_uint(s_init[cb + k]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT + cb), initv);
+        for (int q = 0; q < 4; ++q) tmem_st16(lane_base + (uint32_t)(q * NT + cb), iv);
       }
       tc::tmem_st_wait();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&acc_empty);
+      // pooled bit = NOT(all four acc'_q < 0): two LOP3 AND the s16 sign bits, LEA.HI shifts them into the
+      // word; the B column order (tc4_col_channel) makes it MSB-first
+      uint32_t neg = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        uint32_t x;
+        asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(x) : "r"(a[j]), "r"(b[j]), "r"(c[j]));  // a & b & c
+        x = x & d[j] & 0x80008000u;
+        neg = __umulhi(neg, 0x80000000u) + x;
+      }
       if (A.y != nullptr && in)
         A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;
     }
