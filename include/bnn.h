@@ -95,6 +95,9 @@ BNN_API int bnn_version(void);
  *                   exists; 0: XOR-popcount integer pipe only (Eq. 4).
  *   "conv_tc_fp4"   1 (default): tensor-core convs use packed e2m1 operands (kind::mxf4); 0: int8.
  *   "conv_pool_tc"  1 (default): pooled 32-channel convs fold the 2x2 window into the MMA N.
+ *   "conv_pair"     1 (default): inside a net, conv1_fp4 and the pooled 32-channel conv run as CTA pairs
+ *                   (cta_group::2, M = 256: each SM stages half of the weight operand); 0: one CTA per
+ *                   M = 128 tile.
  *   "first_pool_tc" 1 (default): pooled first layers use the pool-window-ordered kernels.
  *   "first_tma"     1 (default): pooled u8 RGB / SIGN first layers use the TMA-fed kernel.
  *   "first_fp4"     1 (default): binarized pooled u8 first layers run conv1_fp4_pool_kernel (kind::mxf4,

@@ -24,6 +24,7 @@
 #include "k_conv1_fp4.cuh"
 #include "k_conv_tc4.cuh"
 #include "k_conv_tc4_pool.cuh"
+#include "k_conv_tc4_pool3.cuh"
 #include "k_dense_tc4.cuh"
 #include "k_conv_tc4_big.cuh"
 #include "k_dense.cuh"
@@ -131,6 +132,8 @@ int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
+int g_opt_conv_pair = 1;      // 1: conv1_fp4 / conv_tc4_pool run as CTA pairs (cta_group::2, M = 256, half of B per SM)
+int g_opt_conv_pool3 = 1;     // 1: conv_tc4_pool runs as conv_tc4_pool3_kernel (1 CTA/SM, 3 accumulator sets); 0: 2 CTAs/SM x 1 set
 int g_opt_conv_pool_tc = 1;   // 1: pooled 32-channel binary convs fold the pool window into the MMA N (conv_tc4_pool)
 int g_opt_first_fp4 = 1;     // 1: the binarized TMA first layer is conv1_fp4_pool_kernel (kind::mxf4, {0,1} operands, 1 CTA/SM); 0: the int8 kernel
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
@@ -140,6 +143,7 @@ int g_opt_luma_fused = 1;    // 1: THRESH_GRAY nets compute the luma inside conv
 int g_opt_first_real_tma = 1;  // 1: real u8 first layers (mode NONE) use the TMA kernel (u8 x +/-1 kind::i8)
 unsigned long long* g_trace = nullptr;  // bnn_set_trace (diagnostics build)
 int g_trace_cap = 0;
+int g_trace_layer = 0;  // diagnostics build: 0 traces conv1_fp4 / the int8 TMA first layer, 1 conv_tc4_pool
 int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
@@ -167,6 +171,26 @@ void launch_pdl(void (*kfn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   at[0].val.programmaticStreamSerializationAllowed = g_opt_pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kfn, std::forward<Args>(args)...);
+}
+
+// The same with a (cx, 1, 1) thread-block cluster (CTA pairs of the cta_group::2 kernels)
+template <typename... KArgs, typename... Args>
+void launch_pdl_cluster(void (*kfn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cx, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_opt_pdl ? 1 : 0;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = (unsigned)cx;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kfn, std::forward<Args>(args)...);
 }
 
@@ -407,7 +431,7 @@ bnn_status launch_conv_first_tma_t(ConvArgs A, const uint8_t* xu8, const float* 
   A.fd_tx = FastDiv((uint32_t)A.tiles_x);
   A.tiles_per_cta = 0;
   A.exp = g_opt_first_exp;
-  A.trace = g_trace;
+  A.trace = g_trace_layer == 0 ? g_trace : nullptr;
   A.trace_cap = g_trace_cap;
   CUtensorMap map;
   const cuuint64_t dims[3] = {(cuuint64_t)A.W * 3, (cuuint64_t)A.H, (cuuint64_t)A.n};
@@ -431,7 +455,7 @@ bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cu
   auto kfn = conv1_fp4_pool_kernel<K, SPIN, BIN>;
   const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, C::THREADS);
   A.exp = g_opt_first_exp;
-  A.trace = g_trace;
+  A.trace = g_trace_layer == 0 ? g_trace : nullptr;
   A.trace_cap = g_trace_cap;
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
@@ -449,6 +473,14 @@ bnn_status launch_conv1_fp4_t(ConvArgs A, const uint8_t* xu8, const float* T, cu
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BNN_E_CUDA, "conv1_fp4: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  if (g_opt_conv_pair && A.bimg != nullptr && !SPIN) {  // CTA pairs (cta_group::2): each SM reads half of B per MMA
+    auto kp = conv1_fp4_pool_kernel<K, SPIN, BIN, true>;
+    const int occp = tc_occupancy(kp, C::SMEM, C::TMEM_COLS, C::THREADS);
+    const int64_t pairs = std::min<int64_t>((A.total_tiles + 1) / 2, (int64_t)num_sms() * occp / 2);
+    dim3 grid((unsigned)(2 * std::max<int64_t>(pairs, 1)), (unsigned)((A.c_out + C::NT - 1) / C::NT));
+    launch_pdl_cluster(kp, grid, dim3(C::THREADS), C::SMEM, s, 2, A, map, T);
+    return check_launch("conv1_fp4_pool_kernel<pair>");
+  }
   const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
   dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)((A.c_out + C::NT - 1) / C::NT));
   launch_pdl(kfn, grid, dim3(C::THREADS), C::SMEM, s, A, map, T);
@@ -588,11 +620,60 @@ bnn_status launch_conv_tc4_t(ConvArgs A, cudaStream_t s) {
   return check_launch("conv_tc4_kernel");
 }
 
+template <int K, bool PAIR>
+bnn_status launch_conv_tc4_pool3_t(ConvArgs A, cudaStream_t s) {
+  using CF = ConvTc4Pool3Cfg<K, PAIR>;
+  auto kfn = conv_tc4_pool3_kernel<K, PAIR>;
+  const int occ = tc_occupancy(kfn, CF::SMEM, CF::TMEM_COLS, CF::THREADS);
+  A.trace = g_trace_layer == 1 ? g_trace : nullptr;
+  A.trace_cap = g_trace_cap;
+  A.tiles_y = (A.H + CF::P::TH - 1) / CF::P::TH;
+  A.tiles_x = (A.W + CF::P::TW - 1) / CF::P::TW;
+  A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+  if (A.total_tiles >= (1ll << 31) - 1) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+  A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+  A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+  A.tiles_per_cta = 0;
+  const unsigned gy = (unsigned)((A.c_out + CF::P::NT - 1) / CF::P::NT);
+  if (PAIR) {
+    const int64_t pairs = std::min<int64_t>((A.total_tiles + 1) / 2, (int64_t)num_sms() * occ / 2);
+    launch_pdl_cluster(kfn, dim3((unsigned)(2 * std::max<int64_t>(pairs, 1)), gy), dim3(CF::THREADS), CF::SMEM, s, 2, A);
+  } else {
+    const int64_t gx = std::min<int64_t>(A.total_tiles, (int64_t)num_sms() * occ);
+    launch_pdl(kfn, dim3((unsigned)std::max<int64_t>(gx, 1), gy), dim3(CF::THREADS), CF::SMEM, s, A);
+  }
+  return check_launch(PAIR ? "conv_tc4_pool3_kernel<pair>" : "conv_tc4_pool3_kernel");
+}
+
 template <int K>
 bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
   using C = ConvTc4PoolCfg<K>;
   auto kfn = conv_tc4_pool_kernel<K>;
+  if (g_opt_conv_pool3) {
+    if (g_opt_conv_pair && A.bimg != nullptr) return launch_conv_tc4_pool3_t<K, true>(A, s);
+    return launch_conv_tc4_pool3_t<K, false>(A, s);
+  }
+  if (g_opt_conv_pair && A.bimg != nullptr) {  // CTA pairs (cta_group::2): each SM reads half of B per MMA
+    using CP = ConvTc4PoolCfg<K, true>;
+    auto kp = conv_tc4_pool_kernel<K, true>;
+    const int occ = tc_occupancy(kp, CP::SMEM, CP::TMEM_COLS, kTc4PoolThreads);
+    A.tiles_y = (A.H + CP::TH - 1) / CP::TH;
+    A.tiles_x = (A.W + CP::TW - 1) / CP::TW;
+    A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
+    if (A.total_tiles >= (1ll << 31) - 1) return fail(BNN_E_UNSUPPORTED, "conv: too many tiles (%lld) for one launch", (long long)A.total_tiles);
+    A.fd_img = FastDiv((uint32_t)(A.tiles_x * A.tiles_y));
+    A.fd_tx = FastDiv((uint32_t)A.tiles_x);
+    A.tiles_per_cta = 0;
+    A.trace = g_trace_layer == 1 ? g_trace : nullptr;
+    A.trace_cap = g_trace_cap;
+    const int64_t pairs = std::min<int64_t>((A.total_tiles + 1) / 2, (int64_t)num_sms() * occ / 2);
+    dim3 grid((unsigned)(2 * std::max<int64_t>(pairs, 1)), (unsigned)((A.c_out + CP::NT - 1) / CP::NT));
+    launch_pdl_cluster(kp, grid, dim3(kTc4PoolThreads), CP::SMEM, s, 2, A);
+    return check_launch("conv_tc4_pool_kernel<pair>");
+  }
   const int occ = tc_occupancy(kfn, C::SMEM, C::TMEM_COLS, kTc4PoolThreads);
+  A.trace = g_trace_layer == 1 ? g_trace : nullptr;
+  A.trace_cap = g_trace_cap;
   A.tiles_y = (A.H + C::TH - 1) / C::TH;
   A.tiles_x = (A.W + C::TW - 1) / C::TW;
   A.total_tiles = (int64_t)A.n * A.tiles_x * A.tiles_y;
@@ -904,12 +985,15 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "tiles_per_cta") == 0) { g_opt_tiles_per_cta = value; return BNN_OK; }
   if (strcmp(key, "gemv_max_n") == 0) { g_opt_gemv_max_n = value; return BNN_OK; }
   if (strcmp(key, "conv_tc") == 0) { g_opt_conv_tc = value; return BNN_OK; }
+  if (strcmp(key, "conv_pair") == 0) { g_opt_conv_pair = value; return BNN_OK; }
+  if (strcmp(key, "conv_pool3") == 0) { g_opt_conv_pool3 = value; return BNN_OK; }
   if (strcmp(key, "first_pool_tc") == 0) { g_opt_first_pool_tc = value; return BNN_OK; }
   if (strcmp(key, "first_tma") == 0) { g_opt_first_tma = value; return BNN_OK; }
   if (strcmp(key, "first_fp4") == 0) { g_opt_first_fp4 = value; return BNN_OK; }
   if (strcmp(key, "first_db") == 0) { g_opt_first_db = value; return BNN_OK; }
 #ifdef BNN_TRACE
   if (strcmp(key, "first_exp") == 0) { g_opt_first_exp = value; return BNN_OK; }  // diagnostics build only
+  if (strcmp(key, "trace_layer") == 0) { g_trace_layer = value; return BNN_OK; }  // diagnostics build only
 #endif
   if (strcmp(key, "dense_ksplit") == 0) { g_opt_dense_ksplit = value; return BNN_OK; }
   if (strcmp(key, "first_real_tma") == 0) { g_opt_first_real_tma = value; return BNN_OK; }

@@ -60,7 +60,10 @@ struct Conv1Fp4Cfg {
   static_assert(XOFF == 16, "box pixel k <-> box byte 1 + 3 k, image column ox0 - 5 + k");
   static constexpr uint32_t LUMA_BYTES = (IR + 2) * LP, SYN_BYTES = IR * RAW_W;
   static constexpr uint32_t LBP_BYTES = 2 * (LUMA_BYTES + SYN_BYTES);
-  static constexpr int NRAW = 8;
+#ifndef BNN_C1_NRAW
+#define BNN_C1_NRAW 8
+#endif
+  static constexpr int NRAW = BNN_C1_NRAW;  // raw-box ring depth (TMA loads in flight)
   static constexpr int KS = K + 1;     // strip rows of one pooled row's window (dy = 0, 1)
   static constexpr int SB = KS * CIN;  // data bytes of a strip (6 taps x 3 channels for K = 5)
   static constexpr int NWS = (SB + 3) / 4;                // mask words of a strip
@@ -208,7 +211,14 @@ BNN_DEV void conv1_nibbles(const uint32_t (&m)[5], uint32_t (&v)[4]) {
 //              tile pixel (replicate border) as 0xFF / 0x00 bytes in a synthetic box that the item build reads
 constexpr int kBinRgb = 0, kBinGray = 1, kBinLbp = 2;
 
-template <int K, bool SPIN = false, int BIN = kBinRgb>
+// PAIR (cta_group::2, (2, 1, 1) clusters, one CTA per SM): the two CTAs of a TPC run one M = 256 MMA per K
+// step -- rank r's tile is A rows [128 r, 128 r + 128) and it holds B columns [64 r, 64 r + 64) (pool offsets
+// 2r, 2r + 1) of the weight image and of the offset MMA's constant, so each SM reads 4 + 2 KB of operands
+// per MMA instead of 4 + 4 KB, and the leader's (rank 0) single MMA thread issues once per two tiles.  Its
+// a_full / acc_empty barriers count both CTAs' builders / epilogues (remote arrivals); a_free / acc_full
+// commits are multicast to both CTAs.  Pair p runs tile pairs (2 t, 2 t + 1), t = p, p + npairs, ...; the
+// second half of an odd last pair is built from tile 0's box and not stored.
+template <int K, bool SPIN = false, int BIN = kBinRgb, bool PAIR = false>
 __global__ void __launch_bounds__(Conv1Fp4Cfg<K>::THREADS, 1)
 conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap, const float* __restrict__ Tt) {
   griddep_launch();
@@ -228,9 +238,17 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
-  const int stride = gridDim.x, ntiles = (int)A.total_tiles;
+  const int ntiles = (int)A.total_tiles;
+  // tile schedule: single CTA: blockIdx.x, + gridDim.x; pair: 2 t + rank over tile pairs t = pair, + npairs
+  const int rank = PAIR ? (int)tc::cluster_rank() : 0;
+  const int first = PAIR ? 2 * (int)(blockIdx.x >> 1) + rank : (int)blockIdx.x;
+  const int stride = PAIR ? 2 * (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tile_end = PAIR ? ntiles + (ntiles & 1) : ntiles;  // a pair runs both halves of the last pair
 
-  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  if (warp == 0) {
+    if constexpr (PAIR) tc::tmem_alloc_pair<C::TMEM_COLS>(&tmem_base_s);
+    else tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  }
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < NRAW; ++i) {
@@ -239,13 +257,13 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     }
 #pragma unroll
     for (int i = 0; i < NA; ++i) {
-      tc::mbar_init(&a_full[i], NB);
+      tc::mbar_init(&a_full[i], PAIR ? 2 * NB : NB);
       tc::mbar_init(&a_free[i], 1);
     }
 #pragma unroll
     for (int i = 0; i < NACC; ++i) {
       tc::mbar_init(&acc_full[i], 1);
-      tc::mbar_init(&acc_empty[i], 4);  // the 4 warps of epilogue group i
+      tc::mbar_init(&acc_empty[i], PAIR ? 8 : 4);  // the 4 warps of epilogue group i (of both CTAs)
     }
     tc::mbar_init(&w_bar, 1);
     tc::mbar_init(&scale_bar, 4);
@@ -261,7 +279,23 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
   };
 
   if (tid < NT) s_bias[tid] = first_tma_bias<K>(A, g * NT + tid);
-  if (A.bimg != nullptr) {
+  if (PAIR) {  // this CTA's half of N of every (MMA, K chunk) block of the image (the host requires the image)
+    if (tid == 0) {
+      constexpr uint32_t HB = (N / 2) * 16;
+      tc::mbar_arrive_expect_tx(&w_bar, C::B_BYTES / 2);
+      const uint8_t* src = A.bimg + (size_t)g * C::B_BYTES + rank * HB;
+      for (int blk = 0; blk < C::NMMA * 2; ++blk) tc::bulk_g2s(sB + blk * HB, src + (size_t)blk * N * 16, HB, &w_bar);
+      tc::mbar_wait(&w_bar, 0);  // the leader's MMAs read this half after the cluster barrier below
+    }
+    if (warp < 4) {  // block scales of both CTAs before the cluster barrier (warp w: TMEM lanes 32 w ..)
+      tc::fence_after();
+      const uint32_t lb = tmem_base_s + ((uint32_t)(warp * 32) << 16);
+      tc::tmem_st8_same(lb + C::SF_COL, 0x7F7F7F7Fu);
+      tc::tmem_st8_same(lb + C::SF_COL + 8, 0x7F7F7F7Fu);
+      tc::tmem_st8_same(lb + C::SF_COL + 16, 0x93939393u);  // 2^20
+      tc::tmem_st_wait();
+    }
+  } else if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
     stage_b_conv1_fp4<K>(A, g, sB, tid, C::THREADS);
@@ -274,50 +308,67 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
   griddep_wait();  // the image and output buffers belong to the predecessors' stream order
   tc::fence_async_smem();
   tc::fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // both CTAs' barriers, B halves and block scales are set
+  else __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tmem_base_s;
 
-  const int my_tiles = (ntiles - (int)blockIdx.x + stride - 1) / stride;
+  const int my_tiles = (tile_end - first + stride - 1) / stride;
   if (warp == 0) {
-    // ------------------------------------------------------------ MMA issuer (converged warp, elected lane)
-    constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
-    const uint32_t sfa = tmem + C::SF_COL, sfb = tmem + C::SF_COL + 8, sfb_c = tmem + C::SF_COL + 16;
-    const uint64_t adesc_c = tc::desc_kmajor(tc::smem_addr(sC), 128 * 16, 128);
-    const uint64_t bdesc_c = tc::desc_kmajor(tc::smem_addr(sC) + C::CONST_BYTES / 2, 128 * 16, 128);
-    const uint32_t a_full0 = tc::smem_addr(&a_full[0]), a_free0 = tc::smem_addr(&a_free[0]);
-    const uint32_t acc_full0 = tc::smem_addr(&acc_full[0]), acc_empty0 = tc::smem_addr(&acc_empty[0]);
-    // strip rows 2p, 2p + 1 (+ 2 per pooled row): LBO = one strip row, SBO = two; buffer ab at + ab A_BYTES
-    const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA), C::ROWP, 2 * C::ROWP);
-    uint64_t bdesc[C::NMMA];
+    // ------------------------------------------------------------ MMA issuer (converged warp, elected lane;
+    // in a pair the leader issues for both CTAs)
+    // (a whole-warp loop with elected-lane issue measured faster than a lane-0 loop unrolled over buffers / sets,
+    // 0.537 vs 0.60 ms per 16384 images, and than waiting for tile it + 1 between tile it's MMAs, 0.60 ms)
+    if (!PAIR || rank == 0) {
+      constexpr uint32_t idesc = tc::idesc_mxf4(PAIR ? 256 : 128, N);
+      constexpr uint32_t NB16 = (PAIR ? N / 2 : N) * 16;  // LBO of B: the CTA's N columns x 16 B
+      const uint32_t sfa = tmem + C::SF_COL, sfb = tmem + C::SF_COL + 8, sfb_c = tmem + C::SF_COL + 16;
+      const uint64_t adesc_c = tc::desc_kmajor(tc::smem_addr(sC), 128 * 16, 128);
+      const uint64_t bdesc_c = tc::desc_kmajor(tc::smem_addr(sC) + C::CONST_BYTES / 2, NB16, 128);
+      const uint32_t a_full0 = tc::smem_addr(&a_full[0]), a_free0 = tc::smem_addr(&a_free[0]);
+      const uint32_t acc_full0 = tc::smem_addr(&acc_full[0]), acc_empty0 = tc::smem_addr(&acc_empty[0]);
+      // strip rows 2p, 2p + 1 (+ 2 per pooled row): LBO = one strip row, SBO = two; buffer ab at + ab A_BYTES
+      const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA), C::ROWP, 2 * C::ROWP);
+      uint64_t bdesc[C::NMMA];
 #pragma unroll
-    for (int p = 0; p < C::NMMA; ++p) bdesc[p] = tc::desc_kmajor(tc::smem_addr(sB) + (uint32_t)(p * 2 * N * 16), N * 16, 128);
-    if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);
-    tc::mbar_wait(&scale_bar, 0);  // block scales written by epilogue group 0
-    uint32_t ab = 0, cb = 0, ph_full = 0, ph_empty = 0;
-#pragma unroll 1
-    for (int it = 0; it < my_tiles; ++it) {
-      trace_ev(A, it, 0);
-      tc::mbar_wait_at(a_full0 + 8 * ab, (ph_full >> ab) & 1u);
-      ph_full ^= 1u << ab;
-      trace_ev(A, it, 1);
-      if (it >= NACC) {  // the set's previous tile has been drained
-        tc::mbar_wait_at(acc_empty0 + 8 * cb, (ph_empty >> cb) & 1u);
-        ph_empty ^= 1u << cb;
+      for (int p = 0; p < C::NMMA; ++p) bdesc[p] = tc::desc_kmajor(tc::smem_addr(sB) + (uint32_t)(p * 2 * NB16), NB16, 128);
+      if (!PAIR) {
+        if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);
+        tc::mbar_wait(&scale_bar, 0);  // block scales written by epilogue group 0
       }
-      trace_ev(A, it, 2);
-      tc::fence_after();
-      const uint32_t d_tmem = tmem + cb * N;
-      const uint64_t ad = adesc0 + (uint64_t)(ab * (C::A_BYTES >> 4));
-      tc::mma_mxf4_elect(d_tmem, adesc_c, bdesc_c, idesc, sfa, sfb_c, 0u);  // D = C0
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t sfb_, uint32_t acc) {
+        if constexpr (PAIR) tc::mma_mxf4_pair_elect(d, ad, bd, idesc, sfa, sfb_, acc);
+        else tc::mma_mxf4_elect(d, ad, bd, idesc, sfa, sfb_, acc);
+      };
+      uint32_t ab = 0, cb = 0, ph_full = 0, ph_empty = 0;
+#pragma unroll 1
+      for (int it = 0; it < my_tiles; ++it) {
+        trace_ev(A, it, 0);
+        tc::mbar_wait_at(a_full0 + 8 * ab, (ph_full >> ab) & 1u);
+        ph_full ^= 1u << ab;
+        trace_ev(A, it, 1);
+        if (it >= NACC) {  // the set's previous tile has been drained
+          tc::mbar_wait_at(acc_empty0 + 8 * cb, (ph_empty >> cb) & 1u);
+          ph_empty ^= 1u << cb;
+        }
+        trace_ev(A, it, 2);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem + cb * N;
+        const uint64_t ad = adesc0 + (uint64_t)(ab * (C::A_BYTES >> 4));
+        mma(d_tmem, adesc_c, bdesc_c, sfb_c, 0u);  // D = C0 (the offset MMA)
 #pragma unroll
-      for (int p = 0; p < C::NMMA; ++p)
-        tc::mma_mxf4_elect(d_tmem, ad + (uint64_t)(p * ((2 * C::ROWP) >> 4)), bdesc[p], idesc, sfa, sfb, 1u);
-      tc::commit_elect(a_free0 + 8 * ab);
-      tc::commit_elect(acc_full0 + 8 * cb);
-      trace_ev(A, it, 3);
-      ab = (ab + 1) & (NA - 1);
-      cb = (cb + 1 == NACC) ? 0 : cb + 1;
+        for (int p = 0; p < C::NMMA; ++p) mma(d_tmem, ad + (uint64_t)(p * ((2 * C::ROWP) >> 4)), bdesc[p], sfb, 1u);
+        if constexpr (PAIR) {
+          tc::commit_pair_elect(a_free0 + 8 * ab);
+          tc::commit_pair_elect(acc_full0 + 8 * cb);
+        } else {
+          tc::commit_elect(a_free0 + 8 * ab);
+          tc::commit_elect(acc_full0 + 8 * cb);
+        }
+        trace_ev(A, it, 3);
+        ab = (ab + 1) & (NA - 1);
+        cb = (cb + 1 == NACC) ? 0 : cb + 1;
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ TMA producer
@@ -332,7 +383,8 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
           ph ^= 1u << slot;
         }
         int img, oy0, ox0;
-        tile_origin((int)blockIdx.x + it * stride, img, oy0, ox0);
+        const int tile = first + it * stride;
+        tile_origin(tile < ntiles ? tile : 0, img, oy0, ox0);  // (an odd pair's empty half: any valid box)
         const uint32_t bar = raw_full0 + 8 * slot;
         constexpr uint32_t box_bytes = BIN == kBinLbp ? C::RAW_BYTES_LBP : C::RAW_BYTES;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(box_bytes) : "memory");
@@ -367,9 +419,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     const int r = bt / IPR, j = bt % IPR;  // item: strip row r, pooled columns SPI j .. SPI j + SPI - 1
     const uint32_t item_off = (uint32_t)(r * RAW_W + C::WB + 6 * C::SPI * j);
     uint8_t* const a_item = sA + r * C::ROWP + C::SPI * j * 16;
+    const uint32_t a_full_leader = PAIR ? tc::mapa(tc::smem_addr(&a_full[0]), 0) : 0u;
     int it = grp;
 #pragma unroll 1
-    for (int tile = blockIdx.x + grp * stride; tile < ntiles; tile += C::NBG * stride, it += C::NBG) {
+    for (int tile = first + grp * stride; tile < tile_end; tile += C::NBG * stride, it += C::NBG) {
       const int slot = it % NRAW, ab = it % NA;
       wait_x(SPIN ? 16 : 0, &raw_full[slot], (uint32_t)((it / NRAW) & 1));
       if (it >= NA) wait_x(SPIN ? 16 : 0, &a_free[ab], (uint32_t)(((it / NA) - 1) & 1));
@@ -389,7 +442,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
         // phase 2: neighbour bits (R16: TL, R, BL; strict >; replicate border) of tile pixel (strip row r2,
         // column k = kk + 3), channel j at synthetic box byte 1 + 3 k + j; out-of-image pixels stay -1
         int img, oy0, ox0;
-        tile_origin(tile, img, oy0, ox0);
+        tile_origin(tile < ntiles ? tile : 0, img, oy0, ox0);
         for (int idx = bt; idx < IR_ * (C::LW - 2); idx += NB * 32) {
           const int r2 = idx / (C::LW - 2), kc = idx - r2 * (C::LW - 2) + 1, k = kc + C::KL0;
           const int gy = oy0 - R + r2, gx = ox0 - 5 + k;
@@ -447,7 +500,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
         }
         if (BIN != kBinLbp && !zero_ok) {  // out-of-image bytes must be b = 0 whatever the threshold (uniform branch)
           int img, oy0, ox0;
-          tile_origin(tile, img, oy0, ox0);
+          tile_origin(tile < ntiles ? tile : 0, img, oy0, ox0);
           const int gy = oy0 - R + r;
           const bool row_ok = gy >= 0 && gy < A.H;
 #pragma unroll
@@ -479,7 +532,8 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       if (lane == 0) {
         if (bt == 0) trace_ev(A, it, 5);
         if (bt == 32 * (NB - 1)) trace_ev(A, it, 6);
-        tc::mbar_arrive(&a_full[ab]);
+        if constexpr (PAIR) tc::mbar_arrive_cluster(a_full_leader + 8 * ab);
+        else tc::mbar_arrive(&a_full[ab]);
         tc::mbar_arrive(&raw_empty[slot]);
       }
     }
@@ -492,10 +546,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     const uint32_t vmask = nvalid >= 32 ? 0xFFFFFFFFu : ~(0xFFFFFFFFu >> nvalid);
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const uint32_t acc_base = lane_base + (uint32_t)(grp * N);  // this group's accumulator set
-    const uint32_t empty_bar = tc::smem_addr(&acc_empty[grp]);
+    const uint32_t empty_bar = PAIR ? tc::mapa(tc::smem_addr(&acc_empty[grp]), 0) : tc::smem_addr(&acc_empty[grp]);
     const bool want_acc = A.acc != nullptr;
     uint32_t* const ybase = A.y;
-    if (grp == 0) {  // block scales of A (lanes = rows) and B: 1.0 (E8M0 127)
+    if (!PAIR && grp == 0) {  // block scales of A (lanes = rows) and B: 1.0 (E8M0 127)
       tc::tmem_st8_same(lane_base + C::SF_COL, 0x7F7F7F7Fu);
       tc::tmem_st8_same(lane_base + C::SF_COL + 8, 0x7F7F7F7Fu);
       tc::tmem_st8_same(lane_base + C::SF_COL + 16, 0x93939393u);  // 2^20
@@ -511,11 +565,11 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
     constexpr uint32_t C0_BITS = 0x4B400000u;
     uint32_t ph = 0;
 #pragma unroll 1
-    for (int tile = blockIdx.x + grp * stride, it = grp; tile < ntiles; tile += NE * stride, it += NE, ph ^= 1u) {
+    for (int tile = first + grp * stride, it = grp; tile < tile_end; tile += NE * stride, it += NE, ph ^= 1u) {
       int img, oy0, ox0;
-      tile_origin(tile, img, oy0, ox0);
+      tile_origin(tile < ntiles ? tile : 0, img, oy0, ox0);
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
-      const bool in = py < Ho && px < Wo;
+      const bool in = py < Ho && px < Wo && tile < ntiles;
       wait_x(SPIN ? 16 : 0, &acc_full[grp], ph);
       if (lane == 0 && quarter == 0) trace_ev(A, it, 7);
       __syncwarp();
@@ -543,7 +597,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       if (exp_bits(A) & 1) {  // diagnostics build: exp bit 1 releases the set without draining it
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_at(empty_bar);
+        if (lane == 0) {
+          if (PAIR) tc::mbar_arrive_cluster(empty_bar);
+          else tc::mbar_arrive_at(empty_bar);
+        }
         continue;
       }
       uint32_t a[16], b[16], c[16], d[16];
@@ -555,7 +612,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       tc::fence_before();
       __syncwarp();
       if (lane == 0 && quarter == 0) trace_ev(A, it, 8);
-      if (lane == 0) tc::mbar_arrive_at(empty_bar);  // all values are in registers: the MMA may overwrite
+      if (lane == 0) {  // all values are in registers: the MMA may overwrite
+        if (PAIR) tc::mbar_arrive_cluster(empty_bar);
+        else tc::mbar_arrive_at(empty_bar);
+      }
       // pooled bit = max_q V_q >= 0, i.e. NOT(all four V_q < 0): two LOP3 AND the sign bits (15, 31) of an s16
       // pair over the offsets and one LEA.HI, (neg >> 1) + x, shifts them into the word (3 ops per 2 channels);
       // the B column order (conv1_col_channel) makes the result MSB-first
@@ -570,8 +630,14 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       if (ybase != nullptr && in) ybase[(((int64_t)img * Ho + py) * Wo + px) * A.cwo + g] = ~neg & vmask;
     }
   }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  if constexpr (PAIR) {
+    tc::fence_before();
+    tc::cluster_sync();  // the leader's last MMAs and commits touched this CTA's TMEM and barriers
+    if (warp == 0) tc::tmem_dealloc_pair<C::TMEM_COLS>(tmem);
+  } else {
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
 }
 
 }  // namespace bnn

@@ -203,13 +203,15 @@ conv_first_tc_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, const fl
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
-      const uint32_t a0 = tc::smem_addr(&sA[buf][0]), b0 = tc::smem_addr(sB);
+      // base descriptors + constant start offsets (tools/probes/issue_probe.cu)
+      const uint64_t ab = tc::desc_kmajor(tc::smem_addr(&sA[buf][0]), TW * 16, TW * 16);
+      const uint64_t bb = tc::desc_kmajor(tc::smem_addr(sB), NT * 16, 128);
 #pragma unroll
       for (int mb = 0; mb < C::MB; ++mb)
 #pragma unroll
         for (int p = 0; p < NMMA; ++p) {
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)((16 * mb + 2 * p) * TW * 16), TW * 16, TW * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * NT * 16), NT * 16, 128);
+          const uint64_t ad = ab + (uint64_t)(((16 * mb + 2 * p) * TW * 16) >> 4);
+          const uint64_t bd = bb + (uint64_t)((p * 2 * NT * 16) >> 4);
           tc::mma_i8(tmem + (uint32_t)((buf * C::MB + mb) * NT), ad, bd, idesc, p > 0 ? 1u : 0u);
         }
       tc::commit(&bar[buf]);
@@ -481,15 +483,16 @@ conv_first_tc_pool_kernel(const ConvArgs A, const uint8_t* __restrict__ xu8, con
     __syncthreads();
     tc::fence_after();
     if (tid == 128) {
-      const uint32_t a0 = tc::smem_addr(&sA[buf][0]), b0 = tc::smem_addr(sB);
+      // base descriptors + constant start offsets (tools/probes/issue_probe.cu)
+      const uint64_t ab = tc::desc_kmajor(tc::smem_addr(&sA[buf][0]), PW * 16, 2 * PW * 16);
+      const uint64_t bb = tc::desc_kmajor(tc::smem_addr(sB), NT * 16, 128);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int dy = q >> 1, dx = q & 1;
 #pragma unroll
         for (int p = 0; p < NMMA; ++p) {
-          const uint64_t ad =
-              tc::desc_kmajor(a0 + (uint32_t)(((dx * SRR + dy + 2 * p) * PW) * 16), PW * 16, 2 * PW * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * NT * 16), NT * 16, 128);
+          const uint64_t ad = ab + (uint64_t)((((dx * SRR + dy + 2 * p) * PW) * 16) >> 4);
+          const uint64_t bd = bb + (uint64_t)((p * 2 * NT * 16) >> 4);
           tc::mma_i8(tmem + (uint32_t)(q * NT), ad, bd, idesc, p > 0 ? 1u : 0u);
         }
       }

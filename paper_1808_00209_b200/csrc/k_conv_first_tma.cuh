@@ -304,23 +304,24 @@ conv_first_tma_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap
         const uint32_t d_tmem = tmem + (DB ? (uint32_t)(buf * N) : 0u);
         trace_ev(A, it, 1);
         tc::fence_after();
+        // descriptors: base + constant start-address offsets (>> 4) -- no per-MMA descriptor arithmetic chain in
+        // front of the MMA (tools/probes/issue_probe.cu)
         const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
         if (FP4) {
           // MMA p: strip rows 2p, 2p+1 (+ 2 * pooled row): LBO = one strip row, SBO = 2 strip rows
+          const uint64_t ab = tc::desc_kmajor(a0, PW * 16, 2 * PW * 16), bb = tc::desc_kmajor(b0, N * 16, 128);
 #pragma unroll
-          for (int p = 0; p < C::NMMA; ++p) {
-            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(2 * p * PW * 16), PW * 16, 2 * PW * 16);
-            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(p * 2 * N * 16), N * 16, 128);
-            tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, p > 0 ? 1u : 0u);
-          }
+          for (int p = 0; p < C::NMMA; ++p)
+            tc::mma_mxf4(d_tmem, ab + (uint64_t)((2 * p * PW * 16) >> 4), bb + (uint64_t)((p * 2 * N * 16) >> 4), idesc, sfa,
+                         sfb, p > 0 ? 1u : 0u);
         } else {
           // MMA s: strip row s + 2 * (pooled row), both K chunks (LBO = one chunk plane, SBO = 2 strip rows)
+          const uint64_t ab = tc::desc_kmajor(a0, C::PLANE, 2 * C::ROWP), bb = tc::desc_kmajor(b0, N * 16, 128);
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
             if ((exp_bits(A) & 8) && s > 0) break;
-            const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)(s * C::ROWP), C::PLANE, 2 * C::ROWP);
-            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(s * 2 * N * 16), N * 16, 128);
-            tc::mma_i8(d_tmem, ad, bd, idesc, s > 0 ? 1u : 0u);
+            tc::mma_i8(d_tmem, ab + (uint64_t)((s * C::ROWP) >> 4), bb + (uint64_t)((s * 2 * N * 16) >> 4), idesc,
+                       s > 0 ? 1u : 0u);
           }
         }
         tc::commit(&mma_done[buf]);

@@ -260,7 +260,7 @@ conv_tc4_big_kernel(const ConvArgs A) {
       tc::fence_after();
       if (tid == 128) {
         if (A.bimg != nullptr) tc::mbar_wait(&w_bar[s], (stage_uses >> 1) & 1);  // weight stage landed
-        const uint32_t a0 = tc::smem_addr(a), b0 = tc::smem_addr(b);
+        const uint64_t ad_base = tc::desc_kmajor(tc::smem_addr(a), 0, ICI * 16), bd_base = tc::desc_kmajor(tc::smem_addr(b), NT * 16, 128);
         const uint32_t d_tmem = tmem + (uint32_t)(buf * NT);
 #pragma unroll
         for (int i = 0; i < C::NMMA; ++i) {
@@ -268,8 +268,10 @@ conv_tc4_big_kernel(const ConvArgs A) {
           const int off0 = ((u0 / KK) * NPIX + ((u0 % KK) / K) * IC + (u0 % KK) % K) * 16;
           const int off1 = ((u1 / KK) * NPIX + ((u1 % KK) / K) * IC + (u1 % KK) % K) * 16;
           const uint32_t lbo = (off1 > off0) ? (uint32_t)(off1 - off0) : 16u;
-          const uint64_t ad = tc::desc_kmajor(a0 + (uint32_t)off0, lbo, ICI * 16);
-          const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)(i * 2 * NT * 16), NT * 16, 128);
+          // base descriptor (LBO 0) + constant start offset and LBO fields: no per-MMA descriptor arithmetic chain
+          // in front of the MMA (tools/probes/issue_probe.cu)
+          const uint64_t ad = ad_base + (uint64_t)(off0 >> 4) + ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16);
+          const uint64_t bd = bd_base + (uint64_t)((i * 2 * NT * 16) >> 4);
           tc::mma_mxf4(d_tmem, ad, bd, idesc, sfa, sfb, (st > 0 || i > 0) ? 1u : 0u);
         }
         tc::commit(&bar_stage[s]);

@@ -24,7 +24,7 @@
 
 namespace bnn {
 
-template <int K>
+template <int K, bool PAIR = false>
 struct ConvTc4PoolCfg {
   static constexpr int R = (K - 1) / 2, PH = 16, PW = 8, TH = 2 * PH, TW = 2 * PW, NT = 32, N = 4 * NT;
   static constexpr int IR = TH + K - 1, IC = TW + K - 1, CH = (IC + 1) / 2, NPIX = IR * IC;
@@ -36,11 +36,12 @@ struct ConvTc4PoolCfg {
   // every STS.128 was a 2-way conflict, ncu)
   static constexpr uint32_t ROWB = CH * 16, PLANE = IR * ROWB + 64;
   static constexpr uint32_t A_BYTES = 2 * PLANE;
-  static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;
+  static constexpr uint32_t B_BYTES = NMMA * 2 * N * 16;   // the weight image of one channel group
+  static constexpr uint32_t B_SMEM = PAIR ? B_BYTES / 2 : B_BYTES;  // a CTA pair holds half of N per CTA
   static constexpr uint32_t TMEM_COLS = 256;       // N accumulator columns + block scales
   static constexpr int PF = (NPIX + 255) / 256;
   static constexpr int LUTC = 8;  // interleaved LUT copies (lane & 7): fewer bank conflicts in the loaders
-  static constexpr uint32_t SMEM = B_BYTES + 2 * A_BYTES + 256 * 4 * (1 + LUTC) + NT * 4 + 64;
+  static constexpr uint32_t SMEM = B_SMEM + 2 * A_BYTES + 256 * 4 * (1 + LUTC) + NT * 4 + 64;
   static_assert(KS % 2 == 0 && PW + (KS - 1) / 2 <= CH, "window");
 };
 
@@ -108,19 +109,29 @@ __global__ void __launch_bounds__(256) prep_tc4_pool_kernel(const ConvArgs A, ui
 //                        accumulator start values after draining)
 // a_full[b]: loaders (4) -> issuer; mma_done[b]: commit -> epilogue, loaders (A[b] reuse);
 // acc_empty: epilogue (4) -> issuer (single accumulator set).
+//
+// PAIR (cta_group::2, launched as (2, 1, 1) clusters): the two CTAs of a cluster sit on the two SMs of a TPC
+// and run ONE M = 256 MMA per (row pair, column): rank r's 128 pooled pixels are A rows [128 r, 128 r + 128)
+// and it holds B columns [64 r, 64 r + 64) (pool offsets 2r, 2r + 1) of the weight image at the same shared
+// offsets, so each SM reads 4 KB of A + 2 KB of B per MMA instead of 4 + 4 KB (an N = 128 SS MMA is bound by
+// the shared-memory operand path).  The leader (rank 0) issues every MMA and waits on its
+// a_full (both CTAs' loaders arrive: 8) and acc_empty (both epilogues: 8); commits are multicast to the
+// barriers of both CTAs; each TMEM holds its own 128 rows x all 128 columns, so the epilogue is unchanged.
+// Pair p takes tile pairs (2 t, 2 t + 1), t = p, p + npairs, ...; a tile >= ntiles (odd count) is computed
+// on zeros and not stored.
 constexpr int kTc4PoolThreads = 288;
 
-template <int K>
+template <int K, bool PAIR = false>
 __global__ void __launch_bounds__(kTc4PoolThreads, 2)
 conv_tc4_pool_kernel(const ConvArgs A) {
   griddep_launch();
-  using C = ConvTc4PoolCfg<K>;
+  using C = ConvTc4PoolCfg<K, PAIR>;
   constexpr int R = C::R, PW = C::PW, TH = C::TH, TW = C::TW, IC = C::IC, NPIX = C::NPIX, KS = C::KS;
   constexpr int N = C::N, NT = C::NT, NL = 4;  // loader warps
   constexpr int PF = (NPIX + NL * 32 - 1) / (NL * 32);
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sB = dsm;                                              // [mma][K-chunk][N][16]
-  uint8_t* sA = dsm + C::B_BYTES;                                 // 2 x [plane][row][colhalf][16]
+  uint8_t* sA = dsm + C::B_SMEM;                                  // 2 x [plane][row][colhalf][16]
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(sA + 2 * C::A_BYTES);  // 256 entries (weight staging)
   uint32_t* s_lutr = s_lut + 256;                                      // LUTC interleaved copies (loaders)
   float* s_init = reinterpret_cast<float*>(s_lutr + 256 * C::LUTC);   // C0 - (thr' + 1) per TMEM column
@@ -129,7 +140,12 @@ conv_tc4_pool_kernel(const ConvArgs A) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = blockIdx.y;
-  const int stride = gridDim.x, ntiles = (int)A.total_tiles;  // < 2^31 (host check)
+  const int ntiles = (int)A.total_tiles;  // < 2^31 (host check)
+  // tile schedule: single CTA: blockIdx.x, + gridDim.x; pair: 2 t + rank over tile pairs t = pair, + npairs
+  const int rank = PAIR ? (int)tc::cluster_rank() : 0;
+  const int first = PAIR ? 2 * (int)(blockIdx.x >> 1) + rank : (int)blockIdx.x;
+  const int stride = PAIR ? 2 * (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tile_end = PAIR ? ntiles + (ntiles & 1) : ntiles;  // a pair runs both halves of the last pair
   const int S_TOT = K * K * A.c_in;  // |acc| <= S_TOT
   if (tid < 256) {
     fill_lut_fp4(s_lut, tid);
@@ -147,13 +163,16 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     // low 16 bits are acc' as an s16 (exact: tools/probes/acc_probe.cu); invalid channels: acc' = -1 -> bit 0
     s_init[tid] = 12582912.0f - (float)(ok ? tt + 1 : 1);
   }
-  if (warp == 0) tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  if (warp == 0) {
+    if constexpr (PAIR) tc::tmem_alloc_pair<C::TMEM_COLS>(&tmem_base_s);
+    else tc::tmem_alloc<C::TMEM_COLS>(&tmem_base_s);
+  }
   if (tid == 0) {
-    tc::mbar_init(&a_full[0], NL);
-    tc::mbar_init(&a_full[1], NL);
+    tc::mbar_init(&a_full[0], PAIR ? 2 * NL : NL);
+    tc::mbar_init(&a_full[1], PAIR ? 2 * NL : NL);
     tc::mbar_init(&mma_done[0], 1);
     tc::mbar_init(&mma_done[1], 1);
-    tc::mbar_init(&acc_empty, 4);
+    tc::mbar_init(&acc_empty, PAIR ? 8 : 4);
     tc::mbar_init(&w_bar, 1);
     tc::fence_mbar_init();
   }
@@ -161,7 +180,15 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   const uint32_t tmem = tmem_base_s;
   const uint32_t sfa = tmem + N, sfb = tmem + N + 8;  // block scales: all 1.0 (UE8M0 0x7F)
 
-  if (A.bimg != nullptr) {
+  if (PAIR) {  // this CTA's half of N of every (MMA, K chunk) block of the image (the host requires the image)
+    if (tid == 0) {
+      constexpr uint32_t HB = (N / 2) * 16;
+      tc::mbar_arrive_expect_tx(&w_bar, C::B_SMEM);
+      const uint8_t* src = A.bimg + (size_t)g * C::B_BYTES + rank * HB;
+      for (int blk = 0; blk < C::NMMA * 2; ++blk) tc::bulk_g2s(sB + blk * HB, src + (size_t)blk * N * 16, HB, &w_bar);
+      tc::mbar_wait(&w_bar, 0);  // the leader's MMAs read this CTA's half after the cluster barrier below
+    }
+  } else if (A.bimg != nullptr) {
     if (tid == 0) tc::stage_image(sB, A.bimg + (size_t)g * C::B_BYTES, C::B_BYTES, &w_bar);
   } else {
     if (tid < 256) stage_b_tc4_pool<K>(A, g, sB, s_lut, tid, 256);
@@ -186,7 +213,8 @@ conv_tc4_pool_kernel(const ConvArgs A) {
   griddep_wait();  // the input map is the predecessor's output; y is ordered after its readers
   tc::fence_async_smem();
   tc::fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // both CTAs' barriers, B halves, start values and scales are set
+  else __syncthreads();
   tc::fence_after();
 
   auto tile_origin = [&](int tile, int& img, int& oy0, int& ox0) {
@@ -198,26 +226,41 @@ conv_tc4_pool_kernel(const ConvArgs A) {
 
   if (warp == 0) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_mxf4(128, N);
-      if (A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = tc::idesc_mxf4(PAIR ? 256 : 128, N);
+      constexpr uint32_t NB16 = (PAIR ? N / 2 : N) * 16;  // B: the CTA's N columns x 16 B per K chunk
+      const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA), C::ROWB, 2 * C::ROWB);
+      const uint64_t bdesc0 = tc::desc_kmajor(tc::smem_addr(sB), NB16, 128);
+      if (!PAIR && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
+      for (int tile = first; tile < tile_end; tile += stride, ++it) {
         const int buf = it & 1;
-        tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
-        if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // drained and re-armed
+        trace_ev(A, it, 0);
+        if constexpr (PAIR) {
+          tc::mbar_wait_cluster_at(tc::smem_addr(&a_full[buf]), (uint32_t)((it >> 1) & 1));
+          trace_ev(A, it, 1);
+          if (it >= 1) tc::mbar_wait_cluster_at(tc::smem_addr(&acc_empty), (uint32_t)((it - 1) & 1));
+        } else {
+          tc::mbar_wait(&a_full[buf], (uint32_t)((it >> 1) & 1));
+          trace_ev(A, it, 1);
+          if (it >= 1) tc::mbar_wait(&acc_empty, (uint32_t)((it - 1) & 1));  // drained and re-armed
+        }
+        trace_ev(A, it, 2);
         tc::fence_after();
-        const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
+        // base descriptor + constant start-address offsets (see k_conv_tc4_pool3.cuh / tools/probes/issue_probe.cu)
+        const uint64_t abuf = adesc0 + (uint64_t)(buf * (C::A_BYTES >> 4));
 #pragma unroll
         for (int sp = 0; sp < C::SP; ++sp)
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
-            const uint32_t off = (uint32_t)((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16);
-            const uint64_t ad = tc::desc_kmajor(a0 + off, C::ROWB, 2 * C::ROWB);
-            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)((sp * KS + t) * 2 * N * 16), N * 16, 128);
-            tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
+            const uint64_t ad = abuf + (uint64_t)(((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16) >> 4);
+            const uint64_t bd = bdesc0 + (uint64_t)(((sp * KS + t) * 2 * NB16) >> 4);
+            if constexpr (PAIR) tc::mma_mxf4_pair(tmem, ad, bd, idesc, sfa, sfb, 1u);
+            else tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
           }
-        tc::commit(&mma_done[buf]);
+        if constexpr (PAIR) tc::commit_pair(tc::smem_addr(&mma_done[buf]));
+        else tc::commit(&mma_done[buf]);
+        trace_ev(A, it, 3);
       }
     }
     __syncwarp();
@@ -233,7 +276,7 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     _Pragma("unroll") for (int q = 0; q < PF; ++q) {                                                 \
       const int p = lt + q * NL * 32;                                                                \
       uint32_t w = 0u; /* outside the map: all -1 (R4) */                                            \
-      if (p < NPIX) {                                                                                \
+      if (p < NPIX && (TILE) < ntiles) {                                                             \
         const int r = p / IC, c = p - r * IC;                                                        \
         const int gy = oy0_ - R + r, gx = ox0_ - R + c;                                              \
         if (gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) w = __ldg(xin + (int64_t)gy * A.W + gx);     \
@@ -241,11 +284,13 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       pref[q] = w;                                                                                   \
     }                                                                                                \
   } while (0)
-    if ((int)blockIdx.x < ntiles) BNN_TC4P_LOAD(blockIdx.x);
+    const uint32_t a_full_leader = PAIR ? tc::mapa(tc::smem_addr(&a_full[0]), 0) : 0u;
+    if (first < tile_end) BNN_TC4P_LOAD(first);
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
+    for (int tile = first; tile < tile_end; tile += stride, ++it) {
       const int buf = it & 1;
       if (it >= 2) tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)(((it - 2) >> 1) & 1));  // A[buf] read by MMA(it-2)
+      if (lt == 0) trace_ev(A, it, 4);
       uint8_t* a = sA + buf * C::A_BYTES;
 #pragma unroll
       for (int q = 0; q < PF; ++q) {
@@ -261,8 +306,12 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       }
       tc::fence_async_smem();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&a_full[buf]);
-      if (tile + stride < ntiles) BNN_TC4P_LOAD(tile + stride);
+      if (lane == 0) {
+        if constexpr (PAIR) tc::mbar_arrive_cluster(a_full_leader + 8 * buf);
+        else tc::mbar_arrive(&a_full[buf]);
+        if (lt == 0) trace_ev(A, it, 5);
+      }
+      if (tile + stride < tile_end) BNN_TC4P_LOAD(tile + stride);
     }
 #undef BNN_TC4P_LOAD
   } else {
@@ -275,16 +324,18 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     const int t_off = (m_py * Wo + m_pxl) * A.cwo + g;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     static_assert(NT == 32, "two 16-column start-value blocks");
+    const uint32_t acc_empty_leader = PAIR ? tc::mapa(tc::smem_addr(&acc_empty), 0) : 0u;
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += stride, ++it) {
+    for (int tile = first; tile < tile_end; tile += stride, ++it) {
       const int buf = it & 1;
       int img, oy0, ox0;
-      tile_origin(tile, img, oy0, ox0);
+      tile_origin(tile < ntiles ? tile : 0, img, oy0, ox0);
       tc::mbar_wait_sleep(&mma_done[buf], (uint32_t)((it >> 1) & 1));
+      if (lane == 0 && quarter == 0) trace_ev(A, it, 6);
       __syncwarp();
       tc::fence_after();
       const int py = (oy0 >> 1) + m_py, px = (ox0 >> 1) + m_pxl;
-      const bool in = py < Ho && px < Wo;
+      const bool in = py < Ho && px < Wo && tile < ntiles;
       if (A.acc != nullptr) {  // debug output: the 4 window pixels' true sums
 #pragma unroll 1
         for (int q = 0; q < 4; ++q)
@@ -324,7 +375,11 @@ conv_tc4_pool_kernel(const ConvArgs A) {
       tc::tmem_st_wait();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&acc_empty);
+      if (lane == 0) {
+        if constexpr (PAIR) tc::mbar_arrive_cluster(acc_empty_leader);
+        else tc::mbar_arrive(&acc_empty);
+        if (quarter == 0) trace_ev(A, it, 7);
+      }
       // pooled bit = NOT(all four acc'_q < 0): two LOP3 AND the s16 sign bits, LEA.HI shifts them into the
       // word; the B column order (tc4_col_channel) makes it MSB-first
       uint32_t neg = 0;
@@ -339,8 +394,14 @@ conv_tc4_pool_kernel(const ConvArgs A) {
         A.y[(((int64_t)img * Ho + (oy0 >> 1)) * Wo + (ox0 >> 1)) * A.cwo + t_off] = ~neg & vmask;
     }
   }
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  if constexpr (PAIR) {
+    tc::fence_before();
+    tc::cluster_sync();  // the leader's last MMAs and commits touched this CTA's TMEM and barriers
+    if (warp == 0) tc::tmem_dealloc_pair<C::TMEM_COLS>(tmem);
+  } else {
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
 }
 
 }  // namespace bnn

@@ -488,17 +488,24 @@ def test_first_layer_fused_pooled(cuda, orc, tma, h, w, k, cout, T, mode):
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
 
-def test_forward_pooled_layers_weight_images(cuda, orc):
+@pytest.mark.parametrize("pair", [1, 0])
+@pytest.mark.parametrize("k2,h,w,n", [(3, 32, 32, 7), (5, 40, 80, 9), (5, 96, 96, 5)])
+def test_forward_pooled_layers_weight_images(cuda, orc, pair, k2, h, w, n):
     """Nets whose pool-in-N layers stage weight images prepared once by bnn_net_create (first layer
     with two channel groups, a 32-channel conv with two channel groups), thresholds and flips on
-    every hidden layer, integer logits out of a dense layer."""
-    spec = dict(h=32, w=32, c=3, layers=[dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="conv", k=3, c_out=64, pool=2),
-                                         dict(kind="dense", l=8)])
-    net, layers, T = build_net(cuda, spec, 1, 3100, max_batch=4, thr=True)
+    every hidden layer, integer logits out of a dense layer.  pair = 1: the 32-channel conv runs as CTA
+    pairs (cta_group::2, M = 256; odd tile counts per chunk leave the last pair's second half empty)."""
+    spec = dict(h=h, w=w, c=3, layers=[dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="conv", k=k2, c_out=64, pool=2),
+                                       dict(kind="dense", l=8)])
+    net, layers, T = build_net(cuda, spec, 1, 3100 + k2, max_batch=4, thr=True)
     assert net.layer_kernel(0, 4) == "conv1_fp4_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool_kernel"
-    imgs = synth.images(7, 32, 32, 3, 3101)  # two chunks
-    lg, cls = net.forward(dev(imgs))
-    torch.cuda.synchronize()
+    imgs = synth.images(n, h, w, 3, 3101 + h)  # several chunks, the last one ragged
+    cuda.set_option("conv_pair", pair)
+    try:
+        lg, cls = net.forward(dev(imgs))
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("conv_pair", 1)
     ref_l, ref_c = oracle_net(orc, spec, 1, layers, T).forward(imgs.numpy(), threads=7)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 

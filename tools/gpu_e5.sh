@@ -1,0 +1,4 @@
+export PYTHONPATH=. BNN_TRACE_LIB=1
+timeout 120 python tools/trace_conv2.py 0 > gpurun_out/e5_tr2_0.log 2>&1; tail -8 gpurun_out/e5_tr2_0.log
+timeout 120 python tools/trace_conv2.py 1 > gpurun_out/e5_tr2_1.log 2>&1; tail -8 gpurun_out/e5_tr2_1.log
+timeout 120 python tools/trace_conv1.py 1 > gpurun_out/e5_tr1_1.log 2>&1; tail -6 gpurun_out/e5_tr1_1.log

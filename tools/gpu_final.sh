@@ -8,4 +8,4 @@ for c in latency modes cifar sweep alg1; do
   timeout 600 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/${T}_cfg_$c.jsonl 2> gpurun_out/${T}_cfg_$c.err; echo "$c rc=$?"
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/${T}_launches.log 2>&1; echo "launches rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"conv_first_tma|conv_tc4_pool|dense_tc4" -c 3 -o gpurun_out/${T}_full python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/${T}_full.log 2>&1; echo "full rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"conv1_fp4|conv_tc4_pool|dense_tc4" -c 3 -o gpurun_out/${T}_full python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/${T}_full.log 2>&1; echo "full rc=$?"
