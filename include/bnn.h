@@ -105,6 +105,8 @@ BNN_API int bnn_version(void);
  *   "luma_fused"    1 (default): a THRESH_GRAY net's first layer computes the luma from the raw RGB box itself
  *                   (no intermediate image); 2: LBP nets too (slower than the pre-pass, a comparison path);
  *                   0: both go through luma_u8img4_kernel's 0/1 image.
+ *   "luma_band"     1 (default): the GRAY / LBP pre-pass of the TMA first layer stages bands of image rows in
+ *                   shared memory and computes each luma once (luma_band_kernel); 0: luma_u8img4_kernel.
  *   "first_real_tma" 1 (default): pooled real-u8 first layers (mode NONE, c_in = 3) use the same TMA
  *                   kernel with the pixels as the unsigned int8 operand; 0: the register-staged kernel.
  *   "first_db"      1 (default): that (int8) kernel double-buffers its TMEM accumulators (2 CTAs/SM);

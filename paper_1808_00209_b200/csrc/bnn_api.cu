@@ -139,11 +139,12 @@ int g_opt_first_fp4 = 1;     // 1: the binarized TMA first layer is conv1_fp4_po
 int g_opt_first_db = 1;      // 1: the int8 TMA first layer double-buffers its TMEM accumulators (2 CTAs/SM; measured +6% whole step with the 8-deep raw ring)
 int g_opt_first_exp = 0;     // timing experiments on the TMA first layer (diagnostics build only; see exp_bits)
 int g_opt_first_tma = 1;     // 1: pooled u8 RGB / SIGN first layers use the TMA-fed kernel (thresholds folded into the MMA)
+int g_opt_luma_band = 1;     // 1: the GRAY / LBP pre-pass of the TMA first layer is luma_band_kernel; 0: luma_u8img4_kernel
 int g_opt_luma_fused = 1;    // 1: THRESH_GRAY nets compute the luma inside conv1_fp4 (no 0/1 image in HBM); 2: LBP too
 int g_opt_first_real_tma = 1;  // 1: real u8 first layers (mode NONE) use the TMA kernel (u8 x +/-1 kind::i8)
 unsigned long long* g_trace = nullptr;  // bnn_set_trace (diagnostics build)
 int g_trace_cap = 0;
-int g_trace_layer = 0;  // diagnostics build: 0 traces conv1_fp4 / the int8 TMA first layer, 1 conv_tc4_pool
+int g_trace_layer = 0;  // diagnostics build: 0 traces conv1_fp4 / the int8 TMA first layer, 1 conv_tc4_pool, 2 the fused cluster kernel
 int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile grid leaves SMs idle
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
@@ -997,6 +998,7 @@ int bnn_set_option(const char* key, int value) {
 #endif
   if (strcmp(key, "dense_ksplit") == 0) { g_opt_dense_ksplit = value; return BNN_OK; }
   if (strcmp(key, "first_real_tma") == 0) { g_opt_first_real_tma = value; return BNN_OK; }
+  if (strcmp(key, "luma_band") == 0) { g_opt_luma_band = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
@@ -1343,7 +1345,10 @@ bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_
   A.f1 = d1.wt; A.f2 = d2.wt; A.f3 = d3.wt; A.thr_f1 = d1.thr; A.thr_f2 = d2.thr; A.flip_f1 = d1.flip; A.flip_f2 = d2.flip;
   A.l1 = d1.l; A.l2 = d2.l; A.l3 = d3.l;
   A.logits = logits; A.cls = cls;
-  const size_t smem = fused_cluster_smem(net->h, net->w);
+  A.trace = g_trace_layer == 2 ? g_trace : nullptr;
+  // bulk copies need 16-byte rows: raw image rows (W C bytes) and FC1 weight rows (H/4 W/4 words)
+  if ((net->w * net->c) % 16 != 0 || ((net->h / 4) * (net->w / 4)) % 4 != 0) return BNN_OK;
+  const size_t smem = (size_t)FusedClusterLayout(net->h, net->w, net->c, a.k, 8, d1.l, d2.l, d3.l).total * 4;
   if (smem > 200 * 1024) return BNN_OK;
   auto go = [&](auto kfn) -> bnn_status {
     const int cs = fused_cluster_size(kfn, smem);
@@ -1430,9 +1435,18 @@ bnn_status forward_chunk(bnn_net* net, const void* images, int nb, int32_t* logi
     {
       ProfScope ps(net, 0, s);
       const int64_t npix = (int64_t)nb * net->h * net->w;
-      luma_u8img4_kernel<<<grid_for(npix / 4, 256), 256, 0, s>>>((const uint8_t*)images, nb, net->h, net->w, net->mode,
-                                                                 net->T, reinterpret_cast<uint8_t*>(net->packed_in));
-      bnn_status st = check_launch("luma_u8img4_kernel");
+      const size_t lsm = luma_band_smem(net->w);
+      bnn_status st = BNN_OK;
+      const int64_t nblk = (int64_t)nb * ((net->h + kLumaBand - 1) / kLumaBand);
+      if (g_opt_luma_band && lsm <= 48 * 1024 && nblk < (1ll << 31)) {  // one CTA per band of rows (luma computed once)
+        luma_band_kernel<<<(unsigned)nblk, 256, lsm, s>>>((const uint8_t*)images, nb, net->h, net->w, net->mode, net->T,
+                                                         reinterpret_cast<uint8_t*>(net->packed_in));
+        st = check_launch("luma_band_kernel");
+      } else {
+        luma_u8img4_kernel<<<grid_for(npix / 4, 256), 256, 0, s>>>((const uint8_t*)images, nb, net->h, net->w, net->mode,
+                                                                   net->T, reinterpret_cast<uint8_t*>(net->packed_in));
+        st = check_launch("luma_u8img4_kernel");
+      }
       if (st != BNN_OK) return st;
     }
     const LayerPlan& P = net->L[0];

@@ -95,6 +95,13 @@ struct Conv1Fp4Cfg {
   static constexpr int NB = (GROUPS + 31) / 32;    // builder warps per group (2 groups: tile parity)
   static constexpr int NE = NACC;                  // epilogue groups of 4 warps (group = accumulator set)
   static constexpr int THREADS = 32 * (2 + NBG * NB + 4 * NE);
+#ifndef BNN_C1_TMA_W
+#define BNN_C1_TMA_W 1
+#endif
+  // warp of the TMA producer (the builders take warps 1 .. 1 + NBG NB except it): 4 puts it on the MMA warp's SM
+  // sub-partition (warp % 4 == 0) so that no ALU-heavy builder warp competes with the MMA thread for issue slots
+  static constexpr int TMA_W = BNN_C1_TMA_W;
+  static_assert(TMA_W >= 1 && TMA_W < 2 + NBG * NB, "TMA warp among the first 2 + NBG NB warps");
   static constexpr bool LDS64 = WB % 8 == 0 && (6 * SPI) % 8 == 0;  // item words 8-byte aligned: LDS.64
   static constexpr uint32_t SMEM = NRAW * RAW_STRIDE + NA * A_BYTES + B_BYTES + CONST_BYTES + LBP_BYTES + 1024;
   static_assert(KS % 2 == 0 && GROUPS <= NB * 32, "config");
@@ -370,7 +377,7 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
         cb = (cb + 1 == NACC) ? 0 : cb + 1;
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == C::TMA_W) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint32_t raw_full0 = tc::smem_addr(&raw_full[0]), raw_empty0 = tc::smem_addr(&raw_empty[0]);
@@ -398,9 +405,10 @@ conv1_fp4_pool_kernel(const ConvArgs A, const __grid_constant__ CUtensorMap xmap
       }
     }
     __syncwarp();
-  } else if (warp <= 1 + C::NBG * NB) {
+  } else if (warp < 2 + C::NBG * NB) {
     // ------------------------------------------------------------ builders (group = tile parity)
-    const int grp = (warp - 2) / NB, bt = tid - 64 - grp * NB * 32;
+    const int bw = C::TMA_W == 1 ? warp - 2 : (warp < C::TMA_W ? warp - 1 : warp - 2);  // builder warp index
+    const int grp = bw / NB, bt = (bw - grp * NB) * 32 + lane;
     int t[CIN];
     bool zero_ok = true;  // an all-zero (out-of-image) byte thresholds to b = 0 (-1) for every channel
 #pragma unroll

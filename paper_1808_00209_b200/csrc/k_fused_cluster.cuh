@@ -4,52 +4,109 @@
 //
 // One cluster of up to 16 CTAs (one per SM, 16 warps each) runs every layer of one image after the other.
 // There is no global-memory activation and no software grid barrier: each CTA keeps a FULL copy of the
-// conv1 map (48 x 48 words) and of the conv2 map (24 x 24 words) in its shared memory, the producer of a
-// word stores it into every CTA's copy through distributed shared memory (lanes 0..15 of the producing
-// warp each write one CTA), and the hardware cluster barrier (barrier.cluster arrive.release /
-// wait.acquire) separates the phases:
-//   phase 1  conv1 (+ SIGN / THRESH_RGB input binarization, 2x2 OR-pool): warp = pooled pixel, lane =
-//            output channel; the K x K x c patch bits of the 4 window pixels come from ballots of the
-//            thresholded input bytes (Eq. 1, R14), acc = K^2 c - 2 popc(patch ^ w) (Eq. 4);
-//   phase 2  conv2 (+ pool): warp = pooled pixel (all 4 window pixels), lane = output channel, the
-//            (K2 x K2) 32-channel input words are warp-broadcast reads of the local conv1 copy;
-//   phase 3  FC1: warp = output (cluster-wide), lanes stride the local conv2 copy; the bit goes to CTA 0
-//            with one DSMEM atomicOr;
-//   phase 4  CTA 0: FC2 -> FC3 integer logits -> argmax (first maximum, R19).
+// conv1 map (48 x 48 words) and of the conv2 map (24 x 24 words) in its shared memory, producers write
+// every CTA's copy through distributed shared memory (lanes 0..15 of the producing warp each address one
+// CTA), and the hardware cluster barrier (barrier.cluster arrive.release / wait.acquire) separates the
+// phases.  Everything a phase reads is on chip before the phase starts:
+//   prologue  one thread per CTA issues the bulk copy (mbarrier complete_tx) of the CTA's block of FC1 weight
+//             rows (outputs [rank m1, rank m1 + m1)); CTA 0's threads issue 4-byte cp.async copies of the FC2 /
+//             FC3 weights -- they land while conv1 / conv2 run;
+//   phase 0   bulk copy of the raw image rows this CTA's conv1 rows need (pooled rows [rank RP, +RP) and the
+//             K1 - 1 halo rows), clamped to the image; rows outside it are never read (R4 padding);
+//   phase 1   conv1 (+ SIGN / THRESH_RGB input binarization, 2x2 OR-pool) over this CTA's pooled rows: warp =
+//             pooled pixel, lane = output channel; the K x K x c patch bits of the 4 window pixels come from
+//             ballots of the thresholded staged bytes (Eq. 1, R14), acc = K^2 c - 2 popc(patch ^ w) (Eq. 4);
+//   phase 2   conv2 (+ pool): unit = (pooled pixel, pool offset q), 2304 units spread evenly over all warps of
+//             the cluster (warp = unit, lane = output channel); the (K2 x K2) 32-channel input words are warp-
+//             broadcast reads of the local conv1 copy; a unit's sign word is OR-ed into every CTA's conv2
+//             copy with DSMEM atomics (the 2x2 OR-pool, R9);
+//   phase 3   FC1: warp = one of the CTA's m1 outputs (weights in shared memory), lanes stride the local conv2
+//             copy; the bit goes to CTA 0 with one DSMEM atomicOr;
+//   phase 4   CTA 0: FC2 -> FC3 integer logits (weights in shared memory) -> argmax (first maximum, R19).
 // All integer; results equal the layer-by-layer path.  Same topology checks as fused_small_kernel.
 #pragma once
 #include <cooperative_groups.h>
 
 #include "k_fused_small.cuh"
+#include "tc.cuh"
 
 namespace bnn {
 
 constexpr int kClusterMax = 16;
 
-// dynamic shared memory of fused_cluster_kernel for an H x W image
-__host__ __device__ constexpr size_t fused_cluster_smem(int H, int W) {
-  return (size_t)((H / 2) * (W / 2) + (H / 4) * (W / 4) + 2 * (kFusedMaxL / 32) + 32) * 4;
-}
+// shared-memory layout of fused_cluster_kernel (32-bit words; every block 16-byte aligned), for a cluster of
+// `ncta` CTAs -- the host sizes it for the smallest cluster it may get (8)
+struct FusedClusterLayout {
+  int y1, y2, h1, h2, logit, raw, f1w, f2w, f3w, total;  // word offsets, total words
+  int rp, raw_rows, m1;                                    // pooled rows per CTA, staged raw rows, FC1 rows per CTA
+  __host__ __device__ FusedClusterLayout(int H, int W, int C, int K1, int ncta, int l1, int l2, int l3) {
+    auto up4 = [](int v) { return (v + 3) & ~3; };
+    const int H1 = H / 2, W1 = W / 2, H2 = H1 / 2, W2 = W1 / 2;
+    rp = (H1 + ncta - 1) / ncta;
+    raw_rows = 2 * rp + K1 - 1;
+    m1 = (l1 + ncta - 1) / ncta;
+    const int dw1 = H2 * W2, dw2 = (l1 + 31) / 32, dw3 = (l2 + 31) / 32;
+    y1 = 0;
+    y2 = y1 + up4(H1 * W1);
+    h1 = y2 + up4(H2 * W2);
+    h2 = h1 + kFusedMaxL / 32;
+    logit = h2 + kFusedMaxL / 32;
+    raw = logit + 32;
+    f1w = raw + up4((raw_rows * W * C + 3) / 4);
+    f2w = f1w + up4(m1 * dw1);
+    f3w = f2w + up4(l2 * dw2);
+    total = f3w + up4(l3 * dw3);
+  }
+};
 
 template <int K2>
 __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(const FusedSmallArgs A) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint32_t cl_smem[];
+  __shared__ uint64_t w_bar, raw_bar;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = rank * kFusedWarps + warp, nw = ncta * kFusedWarps;
   const int H1 = A.H >> 1, W1 = A.W >> 1, H2 = H1 >> 1, W2 = W1 >> 1;
-  const int lw1 = (A.l1 + 31) / 32;
-  uint32_t* y1 = cl_smem;                          // [H1 * W1] conv1 map (full copy)
-  uint32_t* y2 = y1 + H1 * W1;                     // [H2 * W2] conv2 map (full copy)
-  uint32_t* h1 = y2 + H2 * W2;                     // FC1 bits (CTA 0's copy is the target)
-  uint32_t* h2 = h1 + kFusedMaxL / 32;             // FC2 bits (CTA 0)
-  int32_t* s_logit = reinterpret_cast<int32_t*>(h2 + kFusedMaxL / 32);
+  const int C = A.C, K = A.K1, R = (K - 1) / 2;
+  const FusedClusterLayout Lo(A.H, A.W, C, K, ncta, A.l1, A.l2, A.l3);
+  const int dw1 = H2 * W2, dw2 = (A.l1 + 31) / 32, dw3 = (A.l2 + 31) / 32;
+  uint32_t* y1 = cl_smem + Lo.y1;  // [H1 * W1] conv1 map (full copy)
+  uint32_t* y2 = cl_smem + Lo.y2;  // [H2 * W2] conv2 map (full copy; OR-accumulated)
+  uint32_t* h1 = cl_smem + Lo.h1;  // FC1 bits (CTA 0's copy is the target)
+  uint32_t* h2 = cl_smem + Lo.h2;  // FC2 bits (CTA 0)
+  int32_t* s_logit = reinterpret_cast<int32_t*>(cl_smem + Lo.logit);
+  const uint8_t* raw = reinterpret_cast<const uint8_t*>(cl_smem + Lo.raw);
+  const uint32_t* f1w = cl_smem + Lo.f1w;  // FC1 rows [rank m1, rank m1 + m1)
+  const uint32_t* f2w = cl_smem + Lo.f2w;  // (CTA 0)
+  const uint32_t* f3w = cl_smem + Lo.f3w;  // (CTA 0)
   // lane l < ncta addresses CTA l's copies (DSMEM); every lane addresses CTA 0's FC1 bits
   uint32_t* y1_l = cl.map_shared_rank(y1, lane < ncta ? lane : 0);
   uint32_t* y2_l = cl.map_shared_rank(y2, lane < ncta ? lane : 0);
   uint32_t* h1_0 = cl.map_shared_rank(h1, 0);
+  const int o1 = rank * Lo.m1, n1 = max(0, min(Lo.m1, A.l1 - o1));  // this CTA's FC1 outputs
+
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&w_bar, 1);
+    tc::mbar_init(&raw_bar, 1);
+    tc::fence_mbar_init();
+  }
+  __syncthreads();
+  // weights land while conv1 / conv2 run: this CTA's FC1 rows by bulk copy (waited before phase 3), CTA 0's FC2 /
+  // FC3 weights by 4-byte asynchronous copies (waited before phase 4)
+  if (threadIdx.x == 0) {
+    const uint32_t b1 = (uint32_t)n1 * dw1 * 4;  // dw1 % 4 == 0 (host check)
+    tc::mbar_arrive_expect_tx(&w_bar, b1);
+    if (b1) tc::stage_chunks(cl_smem + Lo.f1w, A.f1 + (int64_t)o1 * dw1, b1, &w_bar);
+  }
+  if (rank == 0) {
+    for (int j = threadIdx.x; j < A.l2 * dw2; j += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_addr(cl_smem + Lo.f2w + j)), "l"(A.f2 + j) : "memory");
+    for (int j = threadIdx.x; j < A.l3 * dw3; j += blockDim.x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_addr(cl_smem + Lo.f3w + j)), "l"(A.f3 + j) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
 
   // conv2 weights of this lane's output channel, in registers for the whole kernel
   constexpr int KK2 = K2 * K2;
@@ -59,7 +116,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   const int th2 = A.thr2 != nullptr ? A.thr2[lane] : 0;
   const bool fl2 = A.flip2 != nullptr && A.flip2[lane] != 0;
   // conv1: patch bit b = 32 w + lane <-> (ky, kx, c), b = (ky K + kx) C + c (MSB-first)
-  const int K = A.K1, R = (K - 1) / 2, C = A.C, nb = K * K * C, S1 = nb;
+  const int nb = K * K * C, S1 = nb;
   int t[4] = {0, 0, 0, 0};
   for (int c = 0; c < C; ++c) t[c] = A.T != nullptr ? u8_threshold(-A.T[c]) : 0;
   int dy_[3], dx_[3], ch_[3], tw_[3];
@@ -78,14 +135,25 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   }
   const int th1 = A.thr1 != nullptr ? A.thr1[lane] : 0;
   const bool fl1 = A.flip1 != nullptr && A.flip1[lane] != 0;
-  if (rank == 0)
-    for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h1[j] = 0u;
-  cl.sync();  // h1 zeroed before any DSMEM atomic reaches it; every CTA of the cluster is running
+  for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h1[j] = 0u;
+  for (int j = threadIdx.x; j < H2 * W2; j += blockDim.x) y2[j] = 0u;
+  const int py0 = rank * Lo.rp, py1 = min(H1, py0 + Lo.rp);  // this CTA's pooled conv1 rows
+  const int gy0 = 2 * py0 - R;                                 // image row of staged raw row 0
+  const int rlo = max(0, gy0), rhi = min(A.H, 2 * py1 + K - 1 - R);  // staged image rows [rlo, rhi)
+  const int rowb = A.W * C;
+  cl.sync();  // h1 / y2 zeroed before any DSMEM atomic reaches them; every CTA of the cluster is running
 
   for (int img = 0; img < A.n; ++img) {
-    // ---- phase 1: conv1 + input binarization + pool -> every CTA's y1
-    const uint8_t* xi = A.x + (int64_t)img * A.H * A.W * C;
-    for (int u = gw; u < H1 * W1; u += nw) {
+    if (rank == 0) fused_trace(A, img, 0);
+    // ---- phase 0: raw rows of this CTA's conv1 rows
+    if (threadIdx.x == 0 && rhi > rlo) {
+      const uint32_t bytes = (uint32_t)((rhi - rlo) * rowb);
+      tc::mbar_arrive_expect_tx(&raw_bar, bytes);
+      tc::stage_chunks(cl_smem + Lo.raw + ((rlo - gy0) * rowb) / 4, A.x + ((int64_t)img * A.H + rlo) * rowb, bytes, &raw_bar);
+    }
+    if (rhi > rlo) tc::mbar_wait(&raw_bar, (uint32_t)(img & 1));
+    // ---- phase 1: conv1 + input binarization + pool over pooled rows [py0, py1) -> every CTA's y1
+    for (int u = py0 * W1 + warp; u < py1 * W1; u += kFusedWarps) {
       const int py = u / W1, px = u - py * W1;
       bool any = false;
 #pragma unroll
@@ -96,7 +164,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         for (int w = 0; w < 3; ++w) {
           const int gy = oy + dy_[w], gx = ox + dx_[w];
           bool bit = false;
-          if (use_[w] && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) bit = (int)__ldg(xi + ((int64_t)gy * A.W + gx) * C + ch_[w]) > tw_[w];
+          if (use_[w] && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) bit = (int)raw[(gy - gy0) * rowb + gx * C + ch_[w]] > tw_[w];
           pc += popc(ballot_pack(bit) ^ wreg[w]);
         }
         any |= (S1 - 2 * pc > th1) != fl1;
@@ -105,56 +173,57 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       if (lane < ncta) y1_l[u] = word;
     }
     cl.sync();
-    // ---- phase 2: conv2 + pool from the local y1 -> every CTA's y2
+    if (rank == 0) fused_trace(A, img, 1);
+    // ---- phase 2: conv2 units (pooled pixel, offset q) from the local y1 -> OR into every CTA's y2
     {
       constexpr int RR = (K2 - 1) / 2;
       const int S2 = KK2 * 32;
-      for (int u = gw; u < H2 * W2; u += nw) {
-        const int py = u / W2, px = u - py * W2;
-        bool any = false;
+      for (int v = gw; v < 4 * H2 * W2; v += nw) {
+        const int u = v >> 2, q = v & 3, py = u / W2, px = u - py * W2;
+        const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+        int acc = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
-          int acc = 0;
+        for (int ky = 0; ky < K2; ++ky)
 #pragma unroll
-          for (int ky = 0; ky < K2; ++ky)
-#pragma unroll
-            for (int kx = 0; kx < K2; ++kx) {
-              const int gy = oy + ky - RR, gx = ox + kx - RR;
-              const uint32_t v = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;
-              acc += popc(v ^ w2[ky * K2 + kx]);
-            }
-          any |= (S2 - 2 * acc > th2) != fl2;
-        }
-        const uint32_t word = ballot_pack(any);
-        if (lane < ncta) y2_l[u] = word;
+          for (int kx = 0; kx < K2; ++kx) {
+            const int gy = oy + ky - RR, gx = ox + kx - RR;
+            const uint32_t x = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;
+            acc += popc(x ^ w2[ky * K2 + kx]);
+          }
+        const uint32_t word = ballot_pack((S2 - 2 * acc > th2) != fl2);
+        if (lane < ncta && word != 0u) atomicOr(y2_l + u, word);
       }
     }
     cl.sync();
-    // ---- phase 3: FC1 from the local y2, one warp per output, bits into CTA 0's h1
+    if (rank == 0) fused_trace(A, img, 2);
+    // ---- phase 3: FC1 outputs [o1, o1 + n1) from the local y2 (weights in shared memory), bits into CTA 0's h1
+    if (img == 0) tc::mbar_wait(&w_bar, 0);
     {
-      const int64_t d1 = (int64_t)H2 * W2 * 32;
-      const int dw1 = H2 * W2;
-      for (int o = gw; o < A.l1; o += nw) {
-        const uint32_t* wr = A.f1 + (int64_t)o * dw1;
+      const int64_t d1 = (int64_t)dw1 * 32;
+      for (int k = warp; k < n1; k += kFusedWarps) {
+        const uint32_t* wr = f1w + (int64_t)k * dw1;
         int s = 0;
 #pragma unroll 6
-        for (int j = lane; j < dw1; j += 32) s += popc(y2[j] ^ __ldg(wr + j));
+        for (int j = lane; j < dw1; j += 32) s += popc(y2[j] ^ wr[j]);
         s = __reduce_add_sync(BNN_FULL_MASK, s);
-        const int acc = (int)d1 - 2 * s;  // Eq. (4)
+        const int o = o1 + k, acc = (int)d1 - 2 * s;  // Eq. (4)
         const int tt = A.thr_f1 != nullptr ? A.thr_f1[o] : 0;
         const bool f = A.flip_f1 != nullptr && A.flip_f1[o] != 0;
         if (lane == 0 && ((acc > tt) != f)) atomicOr(h1_0 + (o >> 5), 1u << (31 - (o & 31)));
       }
     }
+    __syncthreads();  // this CTA's FC1 reads of y2 are done: clear it for the next image's atomics
+    for (int j = threadIdx.x; j < H2 * W2; j += blockDim.x) y2[j] = 0u;
     cl.sync();
+    if (rank == 0) fused_trace(A, img, 3);
     // ---- phase 4 (CTA 0): FC2 -> FC3 integer logits -> argmax
     if (rank == 0) {
+      if (img == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's FC2 / FC3 weight copies
       for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h2[j] = 0u;
       __syncthreads();
-      fused_dense(h1, A.l1, A.f2, A.l2, A.thr_f2, A.flip_f2, h2, nullptr);
+      fused_dense_smem(h1, A.l1, f2w, A.l2, A.thr_f2, A.flip_f2, h2, nullptr);
       __syncthreads();
-      fused_dense(h2, A.l2, A.f3, A.l3, nullptr, nullptr, nullptr, s_logit);
+      fused_dense_smem(h2, A.l2, f3w, A.l3, nullptr, nullptr, nullptr, s_logit);
       __syncthreads();
       if (warp == 0) {
         const bool ok = lane < A.l3;
@@ -169,8 +238,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         }
         if (lane == 0 && A.cls != nullptr) A.cls[img] = bi;  // first maximum wins (R19)
       }
-      for (int j = threadIdx.x; j < lw1; j += blockDim.x) h1[j] = 0u;  // next image's FC1 bits
+      for (int j = threadIdx.x; j < dw2; j += blockDim.x) h1[j] = 0u;  // next image's FC1 bits
       __syncthreads();
+      fused_trace(A, img, 4);
     }
   }
   cl.sync();  // no CTA exits while another may still address its shared memory

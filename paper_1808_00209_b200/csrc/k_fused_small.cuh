@@ -42,7 +42,21 @@ struct FusedSmallArgs {
   int32_t* logits;  // [n, l3] or null
   int32_t* cls;     // [n] or null
   unsigned* barrier;  // [2]: grid-barrier count, FC1-done count (zero at launch; the tail CTA re-arms them)
+  unsigned long long* trace;  // diagnostics build (bnn_set_trace, trace_layer 2): CTA 0's phase globaltimer stamps
 };
+
+// phase timestamp (ns, %globaltimer) ev of image img into A.trace[img * 8 + ev] (diagnostics build only)
+BNN_DEV void fused_trace(const FusedSmallArgs& A, int img, int ev) {
+#ifdef BNN_TRACE
+  if (A.trace != nullptr && threadIdx.x == 0 && img < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.trace[img * 8 + ev] = t;
+  }
+#else
+  (void)A, (void)img, (void)ev;
+#endif
+}
 
 constexpr int kFusedWarps = 16;
 constexpr int kFusedMaxL = 1024;  // l1, l2 <= this (shared-memory bit buffers)
@@ -69,6 +83,29 @@ BNN_DEV void grid_barrier(unsigned* ctr, unsigned target) {
 // One dense layer for one image inside a CTA: x = packed [dw] in shared memory, out bits -> s_out
 // (packed, zero-initialised by the caller) or logits.  Warp w takes outputs w, w + 16, ...; the
 // weight loads of up to 8 of its outputs are issued together (the batch-1 chain is latency-bound).
+// The same for weights already in shared memory (fused_cluster_kernel's FC2 / FC3): warp = output, lanes
+// stride the input words, one reduction per output.
+BNN_DEV void fused_dense_smem(const uint32_t* xs, int64_t d, const uint32_t* w, int l, const int32_t* thr,
+                              const uint8_t* flip, uint32_t* s_out, int32_t* s_logit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int dw = (int)((d + 31) / 32);
+  for (int o = warp; o < l; o += kFusedWarps) {
+    int s = 0;
+    for (int j = lane; j < dw; j += 32) s += popc(xs[j] ^ w[(int64_t)o * dw + j]);
+    s = __reduce_add_sync(BNN_FULL_MASK, s);
+    if (lane == 0) {
+      const int acc = (int)d - 2 * s;  // Eq. (4)
+      if (s_logit != nullptr) {
+        s_logit[o] = acc;
+      } else {
+        const int t = thr != nullptr ? thr[o] : 0;
+        const bool f = flip != nullptr && flip[o] != 0;
+        if ((acc > t) != f) atomicOr(&s_out[o >> 5], 1u << (31 - (o & 31)));
+      }
+    }
+  }
+}
+
 BNN_DEV void fused_dense(const uint32_t* xs, int64_t d, const uint32_t* __restrict__ w, int l, const int32_t* thr,
                          const uint8_t* flip, uint32_t* s_out, int32_t* s_logit) {
   constexpr int OB = 8;

@@ -153,4 +153,102 @@ __global__ void luma_u8img4_kernel(const uint8_t* __restrict__ x, int n, int h, 
   }
 }
 
+// The same output, one CTA per band of kLumaBand image rows: the band's rows and the rows above / below
+// (replicated at the image border) are staged in shared memory with coalesced word loads, every luma value is
+// computed ONCE (four pixels per lane from three aligned words) into a row of bytes whose border columns
+// replicate the edge columns, and the LBP neighbour bits (R16: TL, R, BL, strict >, replicate border) of four
+// pixels are three SIMD byte compares (vcmpgtu4) of shifted words; 12 output bytes per lane, three word
+// stores.  Warp = row, lane = 4-pixel group: no divisions.  The grid-stride kernel above re-reads every row
+// three times with dependent 4-byte loads (config 2: 0.118 ms per 4096 images, ~1 TB/s).
+constexpr int kLumaBand = 32;
+
+__host__ __device__ constexpr size_t luma_band_smem(int w) {
+  return (size_t)(kLumaBand + 2) * (size_t)w * 3 + (size_t)(kLumaBand + 2) * (size_t)(w + 8);
+}
+
+__global__ void __launch_bounds__(256) luma_band_kernel(const uint8_t* __restrict__ x, int n, int h, int w, int mode,
+                                                        const float* __restrict__ Tt, uint8_t* __restrict__ y) {
+  extern __shared__ __align__(16) uint8_t lb_smem[];
+  constexpr int BH = kLumaBand, NWARP = 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bands = (h + BH - 1) / BH;
+  const int64_t img = blockIdx.x / bands;
+  const int y0 = (int)(blockIdx.x - img * bands) * BH, nrows = min(BH, h - y0);
+  const int rw = w * 3 / 4, wg = w >> 2;  // words per image row, 4-pixel groups per row (w % 4 == 0)
+  const int lw = w + 8;                   // luma row pitch: column c at byte c + 4 (c = -1 .. w)
+  uint32_t* raw = reinterpret_cast<uint32_t*>(lb_smem);      // staged row r = image row y0 - 1 + r (clamped)
+  uint8_t* lum = lb_smem + (size_t)(BH + 2) * w * 3;          // [BH + 2][lw]
+  const uint8_t* base = x + img * (int64_t)h * w * 3;
+  // asynchronous copies (LDGSTS): every load of the band is in flight at once (a load -> shared store loop
+  // serialises on the load latency)
+  const bool v16 = (rw % 4) == 0;  // 16-byte chunks (rows and images 16-byte aligned)
+  for (int r = warp; r < nrows + 2; r += NWARP) {
+    const int gy = min(max(y0 - 1 + r, 0), h - 1);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(base + (int64_t)gy * w * 3);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(raw + r * rw);
+    if (v16) {
+      for (int c = lane; c < rw / 4; c += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * c), "l"(src + 4 * c) : "memory");
+    } else {
+      for (int c = lane; c < rw; c += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * c), "l"(src + c) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  for (int r = warp; r < nrows + 2; r += NWARP) {
+    uint8_t* lr = lum + r * lw;
+    for (int g = lane; g < wg; g += 32) {
+      const uint32_t v[4] = {raw[r * rw + 3 * g], raw[r * rw + 3 * g + 1], raw[r * rw + 3 * g + 2], 0u};
+      // R15: Y = (299 R + 587 G + 114 B + 500) div 1000; the sum as two DP2A (bytes of the word pairs), the division
+      // as a multiply-high by ceil(2^32 / 1000) (exact for numerators < 2^22)
+      uint32_t yw = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t rgb = __byte_perm(v[(3 * i) >> 2], v[((3 * i) >> 2) + 1], (uint32_t)(((3 * i) & 3) | ((((3 * i) & 3) + 1) << 4) | ((((3 * i) & 3) + 2) << 8)));
+        const uint32_t sy = __dp2a_hi(114u, rgb, __dp2a_lo((587u << 16) | 299u, rgb, 500u));
+        yw |= __umulhi(sy, 4294968u) << (8 * i);
+      }
+      *reinterpret_cast<uint32_t*>(lr + 4 + 4 * g) = yw;
+      if (g == 0) lr[3] = (uint8_t)yw;                        // column -1 = column 0
+      if (g == wg - 1) lr[w + 4] = (uint8_t)(yw >> 24);       // column w = column w - 1
+    }
+  }
+  __syncthreads();
+  const int tg = (mode == kThreshGray) ? u8_threshold(-Tt[0]) : 0;  // Y > -T <=> Y > tg (R14), tg in [-1, 255]
+  const uint32_t t4 = (uint32_t)(tg < 0 ? 0 : tg) * 0x01010101u;
+  for (int r = warp; r < nrows; r += NWARP) {
+    const uint8_t* lc = lum + (r + 1) * lw;
+    for (int g = lane; g < wg; g += 32) {
+      const int b = 4 + 4 * g;  // byte of pixel 4 g in its luma row
+      const uint32_t C = *reinterpret_cast<const uint32_t*>(lc + b);
+      uint32_t m0, m1, m2;
+      if (mode == kThreshGray) {
+        m0 = tg < 0 ? 0xFFFFFFFFu : __vcmpgtu4(C, t4);
+        m1 = m2 = 0u;
+      } else {  // clockwise from top-left: n0 = (-1,-1), n3 = (0,+1), n6 = (+1,-1)   (R16)
+        const uint32_t* up = reinterpret_cast<const uint32_t*>(lc - lw + b - 4);
+        const uint32_t* dn = reinterpret_cast<const uint32_t*>(lc + lw + b - 4);
+        const uint32_t* ce = reinterpret_cast<const uint32_t*>(lc + b);
+        const uint32_t TL = __funnelshift_r(up[0], up[1], 24), BL = __funnelshift_r(dn[0], dn[1], 24);
+        const uint32_t Rn = __funnelshift_r(ce[0], ce[1], 8);
+        m0 = __vcmpgtu4(TL, C);
+        m1 = __vcmpgtu4(Rn, C);
+        m2 = __vcmpgtu4(BL, C);
+      }
+      m0 &= 0x01010101u;
+      m1 &= 0x01010101u;
+      m2 &= 0x01010101u;
+      // output byte 3 i + j = bit j of pixel i
+      const uint32_t o0 = (m0 & 0xFFu) | ((m1 & 0xFFu) << 8) | ((m2 & 0xFFu) << 16) | ((m0 & 0xFF00u) << 16);
+      const uint32_t o1 = ((m1 >> 8) & 0xFFu) | ((m2 & 0xFF00u)) | ((m0 & 0xFF0000u)) | ((m1 & 0xFF0000u) << 8);
+      const uint32_t o2 = ((m2 >> 16) & 0xFFu) | ((m0 >> 16) & 0xFF00u) | ((m1 >> 8) & 0xFF0000u) | (m2 & 0xFF000000u);
+      uint32_t* yo = reinterpret_cast<uint32_t*>(y + ((img * h + y0 + r) * (int64_t)w + 4 * g) * 3);
+      yo[0] = o0;
+      yo[1] = o1;
+      yo[2] = o2;
+    }
+  }
+}
+
 }  // namespace bnn

@@ -93,6 +93,14 @@ BNN_DEV void stage_image(void* dst, const uint8_t* src, uint32_t bytes, uint64_t
   for (uint32_t o = 0; o < bytes; o += CH) bulk_g2s(static_cast<uint8_t*>(dst) + o, src + o, bytes - o < CH ? bytes - o : CH, bar);
 }
 
+// Bulk copies of `bytes` (16-byte aligned, multiple of 16) in <= 16 KB pieces onto `bar` (the caller arms the
+// barrier with the total expect_tx)
+BNN_DEV void stage_chunks(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  constexpr uint32_t CH = 16384;
+  for (uint32_t o = 0; o < bytes; o += CH)
+    bulk_g2s(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o, bytes - o < CH ? bytes - o : CH, bar);
+}
+
 BNN_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }

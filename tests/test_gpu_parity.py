@@ -654,14 +654,14 @@ def test_forward_scores_vehicle(cuda, orc, mode):
 
 
 # ------------------------------------------------------------------------------------ GRAY / LBP first layer
-@pytest.mark.parametrize("tma", [2, 1, 0])
+@pytest.mark.parametrize("tma", [2, 1, 3, 0])
 @pytest.mark.parametrize("h,w,k,cout,T", [(32, 48, 5, 32, -100.0), (18, 16, 3, 40, -100.0), (34, 64, 5, 64, -100.0),
                                           (32, 48, 5, 32, 5.0), (32, 16, 3, 32, -255.5)])
 @pytest.mark.parametrize("mode", [2, 3])
 def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, T, tma):
     """THRESH_GRAY (c_in = 1: zero weights on the two dummy channels) and LBP: luma (and the LBP neighbour
-    bits, replicate border) computed inside the TMA-fed first layer (tma = 2), luma_u8img4_kernel + the
-    TMA-fed first layer (tma = 1) or the
+    bits, replicate border) computed inside the TMA-fed first layer (tma = 2), the row-band pre-pass
+    luma_band_kernel (tma = 1; ragged last band) or luma_u8img4_kernel (tma = 3) + the TMA-fed first layer, or the
     packed-bit path (tma = 0), with BN thresholds / flips on the first layer, ragged tiles and channel
     groups, against the oracle.  GRAY T = -100 (Y + T = 0 ties), 5 (every pixel +1: the out-of-image
     bytes must still be -1), -255.5 (every pixel -1)."""
@@ -683,6 +683,7 @@ def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, T, tma):
     try:
         cuda.set_option("first_tma", 1 if tma else 0)
         cuda.set_option("luma_fused", 2 if tma == 2 else 0)
+        cuda.set_option("luma_band", 0 if tma == 3 else 1)
         net = cuda.Net(h, w, 3, cuda.U8, mode, None if T is None else dev(T), dl, max_batch=8)
         if tma:
             assert net.layer_kernel(0, 5) == "conv1_fp4_pool_kernel"
@@ -693,6 +694,7 @@ def test_first_layer_luma_tma(cuda, orc, mode, h, w, k, cout, T, tma):
     finally:
         cuda.set_option("first_tma", 1)
         cuda.set_option("luma_fused", 1)
+        cuda.set_option("luma_band", 1)
     ref_l, ref_c = oracle_net(orc, spec, mode, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
 
