@@ -13,13 +13,13 @@
 //             FC3 weights -- they land while conv1 / conv2 run;
 //   phase 0   bulk copy of the raw image rows this CTA's conv1 rows need (pooled rows [rank RP, +RP) and the
 //             K1 - 1 halo rows), clamped to the image; rows outside it are never read (R4 padding);
-//   phase 1   conv1 (+ SIGN / THRESH_RGB input binarization, 2x2 OR-pool) over this CTA's pooled rows: warp =
-//             pooled pixel, lane = output channel; the K x K x c patch bits of the 4 window pixels come from
-//             ballots of the thresholded staged bytes (Eq. 1, R14), acc = K^2 c - 2 popc(patch ^ w) (Eq. 4);
-//   phase 2   conv2 (+ pool): unit = (pooled pixel, pool offset q), 2304 units spread evenly over all warps of
-//             the cluster (warp = unit, lane = output channel); the (K2 x K2) 32-channel input words are warp-
-//             broadcast reads of the local conv1 copy; a unit's sign word is OR-ed into every CTA's conv2
-//             copy with DSMEM atomics (the 2x2 OR-pool, R9);
+//   phase 1   the staged rows are thresholded (SIGN / THRESH_RGB, Eq. 1, R14) into a 0/1 byte image with zero
+//             rows / columns around the image (the -1 padding, R4), then conv1 (+ 2x2 OR-pool) over this CTA's
+//             pooled rows: warp = pooled pixel, lane = output channel; the K x K x c patch bits of the 4 window
+//             pixels are branch-free byte reads + ballots, acc = K^2 c - 2 popc(patch ^ w) (Eq. 4); the word is
+//             stored into every CTA's map (st.shared::cluster, lane l -> CTA l);
+//   phase 2   conv2 (+ pool) from the local conv1 copy: warp = pooled pixel (all 4 window pixels), lane = output
+//             channel, the (K2 x K2) 32-channel input words are warp-broadcast reads; stored like phase 1;
 //   phase 3   FC1: warp = one of the CTA's m1 outputs (weights in shared memory), lanes stride the local conv2
 //             copy; the bit goes to CTA 0 with one DSMEM atomicOr;
 //   phase 4   CTA 0: FC2 -> FC3 integer logits (weights in shared memory) -> argmax (first maximum, R19).
@@ -37,8 +37,8 @@ constexpr int kClusterMax = 16;
 // shared-memory layout of fused_cluster_kernel (32-bit words; every block 16-byte aligned), for a cluster of
 // `ncta` CTAs -- the host sizes it for the smallest cluster it may get (8)
 struct FusedClusterLayout {
-  int y1, y2, h1, h2, logit, raw, f1w, f2w, f3w, total;  // word offsets, total words
-  int rp, raw_rows, m1;                                    // pooled rows per CTA, staged raw rows, FC1 rows per CTA
+  int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, total;  // word offsets, total words
+  int rp, raw_rows, m1, pb;  // pooled rows per CTA, staged raw rows, FC1 rows per CTA, bit-image row pitch (bytes)
   __host__ __device__ FusedClusterLayout(int H, int W, int C, int K1, int ncta, int l1, int l2, int l3) {
     auto up4 = [](int v) { return (v + 3) & ~3; };
     const int H1 = H / 2, W1 = W / 2, H2 = H1 / 2, W2 = W1 / 2;
@@ -52,10 +52,13 @@ struct FusedClusterLayout {
     h2 = h1 + kFusedMaxL / 32;
     logit = h2 + kFusedMaxL / 32;
     raw = logit + 32;
-    f1w = raw + up4((raw_rows * W * C + 3) / 4);
+    pb = (W + K1 - 1) * C;
+    bim = raw + up4((raw_rows * W * C + 3) / 4);
+    f1w = bim + up4((raw_rows * pb + 3) / 4);
     f2w = f1w + up4(m1 * dw1);
     f3w = f2w + up4(l2 * dw2);
-    total = f3w + up4(l3 * dw3);
+    tf = f3w + up4(l3 * dw3);                 // FC1 thr [m1], flip [m1]; FC2 thr [l2], flip [l2] (int)
+    total = tf + up4(2 * (m1 + l2));
   }
 };
 
@@ -78,24 +81,38 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   uint32_t* h2 = cl_smem + Lo.h2;  // FC2 bits (CTA 0)
   int32_t* s_logit = reinterpret_cast<int32_t*>(cl_smem + Lo.logit);
   const uint8_t* raw = reinterpret_cast<const uint8_t*>(cl_smem + Lo.raw);
+  uint8_t* bim = reinterpret_cast<uint8_t*>(cl_smem + Lo.bim);  // [raw_rows][pb] 0/1 bytes, zero outside the image
   const uint32_t* f1w = cl_smem + Lo.f1w;  // FC1 rows [rank m1, rank m1 + m1)
   const uint32_t* f2w = cl_smem + Lo.f2w;  // (CTA 0)
   const uint32_t* f3w = cl_smem + Lo.f3w;  // (CTA 0)
   // lane l < ncta addresses CTA l's copies (DSMEM); every lane addresses CTA 0's FC1 bits
-  uint32_t* y1_l = cl.map_shared_rank(y1, lane < ncta ? lane : 0);
-  uint32_t* y2_l = cl.map_shared_rank(y2, lane < ncta ? lane : 0);
+  const uint32_t y1_c = tc::mapa(tc::smem_addr(y1), lane < ncta ? lane : 0);  // CTA lane's maps (shared::cluster)
+  const uint32_t y2_c = tc::mapa(tc::smem_addr(y2), lane < ncta ? lane : 0);
   uint32_t* h1_0 = cl.map_shared_rank(h1, 0);
   const int o1 = rank * Lo.m1, n1 = max(0, min(Lo.m1, A.l1 - o1));  // this CTA's FC1 outputs
+  int32_t* s_t1 = reinterpret_cast<int32_t*>(cl_smem + Lo.tf);  // FC1 thresholds / flips of this CTA's outputs,
+  int32_t* s_f1 = s_t1 + Lo.m1;                                 // FC2's (CTA 0): read per output by one lane,
+  int32_t* s_t2 = s_f1 + Lo.m1;                                 // so they are loaded once, up front
+  int32_t* s_f2 = s_t2 + A.l2;
+  const int py0 = rank * Lo.rp, py1 = min(H1, py0 + Lo.rp);  // this CTA's pooled conv1 rows
+  const int gy0 = 2 * py0 - R;                                 // image row of staged raw row 0
+  const int rlo = max(0, gy0), rhi = min(A.H, 2 * py1 + K - 1 - R);  // staged image rows [rlo, rhi)
+  const int rowb = A.W * C;
+  auto stage_raw = [&](int img) {  // phase 0: the raw rows of this CTA's conv1 rows (one thread)
+    const uint32_t bytes = (uint32_t)((rhi - rlo) * rowb);
+    tc::mbar_arrive_expect_tx(&raw_bar, bytes);
+    tc::stage_chunks(cl_smem + Lo.raw + ((rlo - gy0) * rowb) / 4, A.x + ((int64_t)img * A.H + rlo) * rowb, bytes, &raw_bar);
+  };
 
+  // Prologue: one batch of independent loads and asynchronous copies, then one relaxed cluster barrier (no
+  // memory fence: nothing written here is read remotely before the phase barriers).  Thread 0 starts the first
+  // image's raw rows and this CTA's FC1 weight rows (bulk copies); CTA 0 starts the FC2 / FC3 weights (cp.async).
+  if (rank == 0) fused_trace(A, 64, 0);  // kernel entry
   if (threadIdx.x == 0) {
     tc::mbar_init(&w_bar, 1);
     tc::mbar_init(&raw_bar, 1);
     tc::fence_mbar_init();
-  }
-  __syncthreads();
-  // weights land while conv1 / conv2 run: this CTA's FC1 rows by bulk copy (waited before phase 3), CTA 0's FC2 /
-  // FC3 weights by 4-byte asynchronous copies (waited before phase 4)
-  if (threadIdx.x == 0) {
+    if (A.n > 0 && rhi > rlo) stage_raw(0);
     const uint32_t b1 = (uint32_t)n1 * dw1 * 4;  // dw1 % 4 == 0 (host check)
     tc::mbar_arrive_expect_tx(&w_bar, b1);
     if (b1) tc::stage_chunks(cl_smem + Lo.f1w, A.f1 + (int64_t)o1 * dw1, b1, &w_bar);
@@ -107,7 +124,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tc::smem_addr(cl_smem + Lo.f3w + j)), "l"(A.f3 + j) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-
   // conv2 weights of this lane's output channel, in registers for the whole kernel
   constexpr int KK2 = K2 * K2;
   uint32_t w2[KK2];
@@ -118,80 +134,104 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   // conv1: patch bit b = 32 w + lane <-> (ky, kx, c), b = (ky K + kx) C + c (MSB-first)
   const int nb = K * K * C, S1 = nb;
   int t[4] = {0, 0, 0, 0};
-  for (int c = 0; c < C; ++c) t[c] = A.T != nullptr ? u8_threshold(-A.T[c]) : 0;
-  int dy_[3], dx_[3], ch_[3], tw_[3];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (c < C) t[c] = A.T != nullptr ? u8_threshold(-A.T[c]) : 0;
+  int off_[3];  // patch bit 32 w + lane: byte offset in the bit image from the window's top-left corner
   bool use_[3];
   uint32_t wreg[3];
 #pragma unroll
   for (int w = 0; w < 3; ++w) {
     const int b = 32 * w + lane;
     use_[w] = b < nb;
-    const int tap = b / C, c = b - tap * C;
-    dy_[w] = tap / K - R;
-    dx_[w] = tap % K - R;
-    ch_[w] = c;
-    tw_[w] = c == 0 ? t[0] : (c == 1 ? t[1] : (c == 2 ? t[2] : t[3]));
+    const int tap = use_[w] ? b / C : 0, c = use_[w] ? b - tap * C : 0;
+    off_[w] = (tap / K) * Lo.pb + (tap % K) * C + c;
     wreg[w] = __ldg(A.w1p + lane * 3 + w);
   }
   const int th1 = A.thr1 != nullptr ? A.thr1[lane] : 0;
   const bool fl1 = A.flip1 != nullptr && A.flip1[lane] != 0;
+  for (int j = threadIdx.x; j < n1; j += blockDim.x) {  // read per output by one lane in phase 3 / 4: staged once
+    s_t1[j] = A.thr_f1 != nullptr ? A.thr_f1[o1 + j] : 0;
+    s_f1[j] = A.flip_f1 != nullptr ? A.flip_f1[o1 + j] : 0;
+  }
+  if (rank == 0)
+    for (int j = threadIdx.x; j < A.l2; j += blockDim.x) {
+      s_t2[j] = A.thr_f2 != nullptr ? A.thr_f2[j] : 0;
+      s_f2[j] = A.flip_f2 != nullptr ? A.flip_f2[j] : 0;
+    }
   for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h1[j] = 0u;
-  for (int j = threadIdx.x; j < H2 * W2; j += blockDim.x) y2[j] = 0u;
-  const int py0 = rank * Lo.rp, py1 = min(H1, py0 + Lo.rp);  // this CTA's pooled conv1 rows
-  const int gy0 = 2 * py0 - R;                                 // image row of staged raw row 0
-  const int rlo = max(0, gy0), rhi = min(A.H, 2 * py1 + K - 1 - R);  // staged image rows [rlo, rhi)
-  const int rowb = A.W * C;
-  cl.sync();  // h1 / y2 zeroed before any DSMEM atomic reaches them; every CTA of the cluster is running
+  if (rank == 0) fused_trace(A, 64, 1);
+  // every CTA of the cluster is running and has zeroed h1 (the first DSMEM atomics into it follow two phase
+  // barriers later); the barrier's wait side synchronises the CTA (mbarrier initialisation, staged values)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 
   for (int img = 0; img < A.n; ++img) {
     if (rank == 0) fused_trace(A, img, 0);
     // ---- phase 0: raw rows of this CTA's conv1 rows
-    if (threadIdx.x == 0 && rhi > rlo) {
-      const uint32_t bytes = (uint32_t)((rhi - rlo) * rowb);
-      tc::mbar_arrive_expect_tx(&raw_bar, bytes);
-      tc::stage_chunks(cl_smem + Lo.raw + ((rlo - gy0) * rowb) / 4, A.x + ((int64_t)img * A.H + rlo) * rowb, bytes, &raw_bar);
-    }
+    if (threadIdx.x == 0 && rhi > rlo && img > 0) stage_raw(img);
     if (rhi > rlo) tc::mbar_wait(&raw_bar, (uint32_t)(img & 1));
-    // ---- phase 1: conv1 + input binarization + pool over pooled rows [py0, py1) -> every CTA's y1
+    if (rank == 0) fused_trace(A, img, 5);
+    // ---- phase 1a: the 0/1 byte image of the staged rows (zero outside the image: the -1 padding, R4)
+    for (int r = warp; r < Lo.raw_rows; r += kFusedWarps) {  // warp = row, lane = bit-image column (pixel)
+      const int gy = gy0 + r;
+      const bool row_in = gy >= 0 && gy < A.H;
+      for (int xx = lane; xx < A.W + K - 1; xx += 32) {
+        const int gx = xx - R;
+        const bool in = row_in && gx >= 0 && gx < A.W;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)  // (t[] stays in registers: compile-time indices)
+          if (c < C) bim[r * Lo.pb + xx * C + c] = (in && (int)raw[(gy - gy0) * rowb + gx * C + c] > t[c]) ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    if (rank == 0) fused_trace(A, img, 6);
+    // ---- phase 1b: conv1 + pool over pooled rows [py0, py1) -> every CTA's y1
+#pragma unroll 2
     for (int u = py0 * W1 + warp; u < py1 * W1; u += kFusedWarps) {
       const int py = u / W1, px = u - py * W1;
+      const uint8_t* win = bim + (2 * py - R - gy0) * Lo.pb + 2 * px * C;  // window corner of offset q = 0
+      uint32_t v[12];  // all 12 patch bytes of the 4 offsets first (independent loads), then the ballots
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 3; ++w) v[3 * q + w] = win[(q >> 1) * Lo.pb + (q & 1) * C + off_[w]];
       bool any = false;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
         int pc = 0;
 #pragma unroll
-        for (int w = 0; w < 3; ++w) {
-          const int gy = oy + dy_[w], gx = ox + dx_[w];
-          bool bit = false;
-          if (use_[w] && gy >= 0 && gy < A.H && gx >= 0 && gx < A.W) bit = (int)raw[(gy - gy0) * rowb + gx * C + ch_[w]] > tw_[w];
-          pc += popc(ballot_pack(bit) ^ wreg[w]);
-        }
+        for (int w = 0; w < 3; ++w) pc += popc(ballot_pack(use_[w] && v[3 * q + w] != 0) ^ wreg[w]);
         any |= (S1 - 2 * pc > th1) != fl1;
       }
       const uint32_t word = ballot_pack(any);
-      if (lane < ncta) y1_l[u] = word;
+      // (no "memory" clobber: the next pixel's loads may move above the store; the cluster barrier orders it)
+      if (lane < ncta) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(y1_c + 4 * u), "r"(word));
     }
     cl.sync();
     if (rank == 0) fused_trace(A, img, 1);
-    // ---- phase 2: conv2 units (pooled pixel, offset q) from the local y1 -> OR into every CTA's y2
+    // ---- phase 2: conv2 + pool from the local y1 -> every CTA's y2
     {
       constexpr int RR = (K2 - 1) / 2;
       const int S2 = KK2 * 32;
-      for (int v = gw; v < 4 * H2 * W2; v += nw) {
-        const int u = v >> 2, q = v & 3, py = u / W2, px = u - py * W2;
-        const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
-        int acc = 0;
+      for (int u = gw; u < H2 * W2; u += nw) {
+        const int py = u / W2, px = u - py * W2;
+        bool any = false;
 #pragma unroll
-        for (int ky = 0; ky < K2; ++ky)
+        for (int q = 0; q < 4; ++q) {
+          const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
+          int acc = 0;
 #pragma unroll
-          for (int kx = 0; kx < K2; ++kx) {
-            const int gy = oy + ky - RR, gx = ox + kx - RR;
-            const uint32_t x = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;
-            acc += popc(x ^ w2[ky * K2 + kx]);
-          }
-        const uint32_t word = ballot_pack((S2 - 2 * acc > th2) != fl2);
-        if (lane < ncta && word != 0u) atomicOr(y2_l + u, word);
+          for (int ky = 0; ky < K2; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < K2; ++kx) {
+              const int gy = oy + ky - RR, gx = ox + kx - RR;
+              const uint32_t x = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;
+              acc += popc(x ^ w2[ky * K2 + kx]);
+            }
+          any |= (S2 - 2 * acc > th2) != fl2;
+        }
+        const uint32_t word = ballot_pack(any);
+        if (lane < ncta) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(y2_c + 4 * u), "r"(word));
       }
     }
     cl.sync();
@@ -207,22 +247,19 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         for (int j = lane; j < dw1; j += 32) s += popc(y2[j] ^ wr[j]);
         s = __reduce_add_sync(BNN_FULL_MASK, s);
         const int o = o1 + k, acc = (int)d1 - 2 * s;  // Eq. (4)
-        const int tt = A.thr_f1 != nullptr ? A.thr_f1[o] : 0;
-        const bool f = A.flip_f1 != nullptr && A.flip_f1[o] != 0;
+        const int tt = s_t1[k];
+        const bool f = s_f1[k] != 0;
         if (lane == 0 && ((acc > tt) != f)) atomicOr(h1_0 + (o >> 5), 1u << (31 - (o & 31)));
       }
     }
-    __syncthreads();  // this CTA's FC1 reads of y2 are done: clear it for the next image's atomics
-    for (int j = threadIdx.x; j < H2 * W2; j += blockDim.x) y2[j] = 0u;
     cl.sync();
     if (rank == 0) fused_trace(A, img, 3);
     // ---- phase 4 (CTA 0): FC2 -> FC3 integer logits -> argmax
     if (rank == 0) {
       if (img == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's FC2 / FC3 weight copies
-      for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h2[j] = 0u;
+      fused_dense_smem(h1, A.l1, f2w, A.l2, s_t2, s_f2, h2, nullptr);
       __syncthreads();
-      fused_dense_smem(h1, A.l1, f2w, A.l2, A.thr_f2, A.flip_f2, h2, nullptr);
-      __syncthreads();
+      fused_trace(A, img, 7);
       fused_dense_smem(h2, A.l2, f3w, A.l3, nullptr, nullptr, nullptr, s_logit);
       __syncthreads();
       if (warp == 0) {
@@ -243,7 +280,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       fused_trace(A, img, 4);
     }
   }
+  if (rank == 0) fused_trace(A, 64, 2);
   cl.sync();  // no CTA exits while another may still address its shared memory
+  if (rank == 0) fused_trace(A, 64, 3);
 }
 
 }  // namespace bnn

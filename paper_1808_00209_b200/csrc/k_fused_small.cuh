@@ -48,7 +48,7 @@ struct FusedSmallArgs {
 // phase timestamp (ns, %globaltimer) ev of image img into A.trace[img * 8 + ev] (diagnostics build only)
 BNN_DEV void fused_trace(const FusedSmallArgs& A, int img, int ev) {
 #ifdef BNN_TRACE
-  if (A.trace != nullptr && threadIdx.x == 0 && img < 64) {
+  if (A.trace != nullptr && threadIdx.x == 0 && img <= 64) {  // (img 64: kernel-level stamps)
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     A.trace[img * 8 + ev] = t;
@@ -83,25 +83,25 @@ BNN_DEV void grid_barrier(unsigned* ctr, unsigned target) {
 // One dense layer for one image inside a CTA: x = packed [dw] in shared memory, out bits -> s_out
 // (packed, zero-initialised by the caller) or logits.  Warp w takes outputs w, w + 16, ...; the
 // weight loads of up to 8 of its outputs are issued together (the batch-1 chain is latency-bound).
-// The same for weights already in shared memory (fused_cluster_kernel's FC2 / FC3): warp = output, lanes
-// stride the input words, one reduction per output.
+// The same for weights, thresholds and flips already in shared memory (fused_cluster_kernel's FC2 / FC3):
+// lane = output (a warp covers 32 outputs), each lane loops over the dw input words, and the warp's 32 sign
+// bits are one ballot stored as one word (Eq. 2, MSB-first) -- no cross-lane reductions, no atomics.
 BNN_DEV void fused_dense_smem(const uint32_t* xs, int64_t d, const uint32_t* w, int l, const int32_t* thr,
-                              const uint8_t* flip, uint32_t* s_out, int32_t* s_logit) {
+                              const int32_t* flip, uint32_t* s_out, int32_t* s_logit) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dw = (int)((d + 31) / 32);
-  for (int o = warp; o < l; o += kFusedWarps) {
+  for (int o0 = warp * 32; o0 < l; o0 += kFusedWarps * 32) {
+    const int o = o0 + lane;
+    const bool ok = o < l;
     int s = 0;
-    for (int j = lane; j < dw; j += 32) s += popc(xs[j] ^ w[(int64_t)o * dw + j]);
-    s = __reduce_add_sync(BNN_FULL_MASK, s);
-    if (lane == 0) {
-      const int acc = (int)d - 2 * s;  // Eq. (4)
-      if (s_logit != nullptr) {
-        s_logit[o] = acc;
-      } else {
-        const int t = thr != nullptr ? thr[o] : 0;
-        const bool f = flip != nullptr && flip[o] != 0;
-        if ((acc > t) != f) atomicOr(&s_out[o >> 5], 1u << (31 - (o & 31)));
-      }
+    if (ok)
+      for (int j = 0; j < dw; ++j) s += popc(xs[j] ^ w[(int64_t)o * dw + j]);
+    const int acc = (int)d - 2 * s;  // Eq. (4)
+    if (s_logit != nullptr) {
+      if (ok) s_logit[o] = acc;
+    } else {
+      const uint32_t word = ballot_pack(ok && ((acc > (thr != nullptr ? thr[o] : 0)) != (flip != nullptr && flip[o] != 0)));
+      if (lane == 0) s_out[o0 >> 5] = word;
     }
   }
 }
