@@ -19,7 +19,8 @@
 //             pixels are branch-free byte reads + ballots, acc = K^2 c - 2 popc(patch ^ w) (Eq. 4); the word is
 //             stored into every CTA's map (st.shared::cluster, lane l -> CTA l);
 //   phase 2   conv2 (+ pool) from the local conv1 copy: warp = pooled pixel (all 4 window pixels), lane = output
-//             channel, the (K2 x K2) 32-channel input words are warp-broadcast reads; stored like phase 1;
+//             channel, the (K2 x K2) 32-channel input words are warp-broadcast reads, each kernel row's K2 XOR
+//             words go through the carry-save popcount (3 POPC instead of 5 for K2 = 5); stored like phase 1;
 //   phase 3   FC1: warp = one of the CTA's m1 outputs (weights in shared memory), lanes stride the local conv2
 //             copy; the bit goes to CTA 0 with one DSMEM atomicOr;
 //   phase 4   CTA 0: FC2 -> FC3 integer logits (weights in shared memory) -> argmax (first maximum, R19).
@@ -27,6 +28,7 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include "k_conv.cuh"  // csa_popc
 #include "k_fused_small.cuh"
 #include "tc.cuh"
 
@@ -221,13 +223,16 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
           const int oy = 2 * py + (q >> 1), ox = 2 * px + (q & 1);
           int acc = 0;
 #pragma unroll
-          for (int ky = 0; ky < K2; ++ky)
+          for (int ky = 0; ky < K2; ++ky) {  // one kernel row's K2 XOR words through the carry-save popcount (f3)
+            uint32_t xr[K2];
 #pragma unroll
             for (int kx = 0; kx < K2; ++kx) {
               const int gy = oy + ky - RR, gx = ox + kx - RR;
               const uint32_t x = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;
-              acc += popc(x ^ w2[ky * K2 + kx]);
+              xr[kx] = x ^ w2[ky * K2 + kx];
             }
+            acc += csa_popc<K2>(xr);
+          }
           any |= (S2 - 2 * acc > th2) != fl2;
         }
         const uint32_t word = ballot_pack(any);
