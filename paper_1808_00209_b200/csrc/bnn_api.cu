@@ -850,7 +850,7 @@ const char* conv_kernel_name(bnn_dtype x_dt, int c_in, int k, int pool) {
   if (c_in >= 32 && tc_supported(k, (c_in + 31) / 32)) {
     const int cw = (c_in + 31) / 32;
     if (!g_opt_conv_tc_fp4) return "conv_tc_kernel";
-    if (use_conv_pool_tc(k, cw, pool)) return "conv_tc4_pool_kernel";
+    if (use_conv_pool_tc(k, cw, pool)) return g_opt_conv_pool3 ? "conv_tc4_pool3_kernel" : "conv_tc4_pool_kernel";
     const bool small = (k == 5 && cw <= 2) || (k == 3 && (cw <= 2 || cw == 4)) || (k == 7 && cw == 1);
     return small ? "conv_tc4_kernel" : "conv_tc4_big_kernel";
   }

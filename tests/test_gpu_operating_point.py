@@ -53,7 +53,7 @@ def test_forward_operating_point(cuda, orc, op_images, mode, thr, fp4):
 def _operating_point(cuda, orc, op_images, mode, thr, fp4):
     net, layers, T = build_net(cuda, synth.VEHICLE, mode, 7100 + mode, max_batch=CHUNK, thr=thr)
     assert net.layer_kernel(0, CHUNK) == ("conv1_fp4_pool_kernel" if fp4 and mode != -1 else "conv_first_tma_pool_kernel")
-    assert net.layer_kernel(1, CHUNK) == "conv_tc4_pool_kernel"
+    assert net.layer_kernel(1, CHUNK) == "conv_tc4_pool3_kernel"
     logits, cls = net.forward(op_images)
     torch.cuda.synchronize()
     idx = _sample_idx(N_OP, CHUNK, 12, 7200 + mode)

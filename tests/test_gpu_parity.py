@@ -498,7 +498,7 @@ def test_forward_pooled_layers_weight_images(cuda, orc, pair, k2, h, w, n):
     spec = dict(h=h, w=w, c=3, layers=[dict(kind="conv", k=5, c_out=32, pool=2), dict(kind="conv", k=k2, c_out=64, pool=2),
                                        dict(kind="dense", l=8)])
     net, layers, T = build_net(cuda, spec, 1, 3100 + k2, max_batch=4, thr=True)
-    assert net.layer_kernel(0, 4) == "conv1_fp4_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool_kernel"
+    assert net.layer_kernel(0, 4) == "conv1_fp4_pool_kernel" and net.layer_kernel(1, 4) == "conv_tc4_pool3_kernel"
     imgs = synth.images(n, h, w, 3, 3101 + h)  # several chunks, the last one ragged
     cuda.set_option("conv_pair", pair)
     try:

@@ -25,7 +25,7 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "launch__
 LAYER_OF = {"conv_first_lp_kernel": "layer0", "conv_strip_kernel": "layer0", "conv_patch_kernel": "layer0",
             "conv_first_tc_kernel": "layer0", "conv_first_tc_pool_kernel": "layer0",
             "conv_first_tma_pool_kernel": "layer0", "conv1_fp4_pool_kernel": "layer0", "conv_bin_kernel": "layer1", "conv_tc_kernel": "layer1",
-            "conv_tc4_kernel": "layer1", "conv_tc4_pool_kernel": "layer1", "dense_kernel": "layer2",
+            "conv_tc4_kernel": "layer1", "conv_tc4_pool_kernel": "layer1", "conv_tc4_pool3_kernel": "layer1", "dense_kernel": "layer2",
             "dense_tc4_kernel": "layer2"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
