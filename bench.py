@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--check", type=int, default=8, help="sampled images checked against the oracle after timing")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=V",
+                    help="bnn_set_option before the run (A/B of kernel variants; results are identical for every setting)")
     ap.add_argument("--config", default="vehicle", choices=["vehicle", "latency", "modes", "cifar", "sweep", "alg1"],
                     help="vehicle = the headline (default); latency = BASELINE config 1 (batch 1, 1000 images); "
                          "modes = config 2 (batch 4096, every input binarization); cifar = config 4; "
@@ -344,6 +346,11 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         return run_reference(a, rank, world)
+    if a.opt:
+        import paper_1808_00209_b200 as bnn
+        for kv in a.opt:
+            k, v = kv.split("=")
+            bnn.set_option(k, int(v))
     if a.config != "vehicle":
         return {"latency": run_latency, "modes": run_modes, "cifar": run_cifar, "sweep": run_sweep,
                 "alg1": run_alg1}[a.config](a)
@@ -509,6 +516,8 @@ def main():
             "binary_mac_per_s": tot_mac / (ms * 1e-3), "stage_ms_per_step": stages,
             "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
             "parity": parity, "multi_gpu_check": multi}
+    if a.opt:
+        line["config"]["options"] = a.opt
     if rank == 0:
         print(json.dumps(line), flush=True)
     net.close()

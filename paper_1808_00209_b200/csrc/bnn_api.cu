@@ -654,7 +654,7 @@ bnn_status launch_conv_tc4_pool_t(ConvArgs A, cudaStream_t s) {
     if (g_opt_conv_pair && A.bimg != nullptr) return launch_conv_tc4_pool3_t<K, true>(A, s);
     return launch_conv_tc4_pool3_t<K, false>(A, s);
   }
-  if (g_opt_conv_pair && A.bimg != nullptr) {  // CTA pairs (cta_group::2): each SM reads half of B per MMA
+  if (g_opt_conv_pair == 2 && A.bimg != nullptr) {  // CTA pairs (cta_group::2): each SM reads half of B per MMA
     using CP = ConvTc4PoolCfg<K, true>;
     auto kp = conv_tc4_pool_kernel<K, true>;
     const int occ = tc_occupancy(kp, CP::SMEM, CP::TMEM_COLS, kTc4PoolThreads);
@@ -913,7 +913,7 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     if (tmax) {
       const cuuint64_t dims[2] = {(cuuint64_t)A.dw, (cuuint64_t)n};
       const cuuint64_t strides[1] = {(cuuint64_t)A.dw * 4};
-      const cuuint32_t box[2] = {(cuuint32_t)DenseTc4Cfg<128>::KC, 128};
+      const cuuint32_t box[2] = {(cuuint32_t)(wide ? DenseTc4Cfg<256>::KC : DenseTc4Cfg<128>::KC), 128};
       const cuuint32_t estr[2] = {1, 1};
       tmax = tma_encoder()(&xmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(x), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1607,7 +1607,8 @@ bnn_status bnn_net_create(int h, int w, int c, bnn_dtype in_dt, int mode, const 
       D.wt = P.wt; D.l = P.l; D.d = P.d; D.dw = dw;
       const bool wide = P.l > 128;
       const int nt = wide ? 256 : 128, groups = (P.l + nt - 1) / nt;
-      const int nstage = (int)((dw + DenseTc4Cfg<128>::KC - 1) / DenseTc4Cfg<128>::KC);
+      const int kc = wide ? DenseTc4Cfg<256>::KC : DenseTc4Cfg<128>::KC;
+      const int nstage = (int)((dw + kc - 1) / kc);
       const size_t bb = wide ? DenseTc4Cfg<256>::B_BYTES : DenseTc4Cfg<128>::B_BYTES;
       if ((e = cudaMalloc(&P.bimg, (size_t)groups * nstage * bb)) != cudaSuccess) break;
       if (wide) prep_dense_tc4_kernel<256><<<dim3((unsigned)nstage, (unsigned)groups), 256>>>(D, P.bimg);

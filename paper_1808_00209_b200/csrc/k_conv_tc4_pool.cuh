@@ -229,8 +229,6 @@ conv_tc4_pool_kernel(const ConvArgs A) {
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = tc::idesc_mxf4(PAIR ? 256 : 128, N);
       constexpr uint32_t NB16 = (PAIR ? N / 2 : N) * 16;  // B: the CTA's N columns x 16 B per K chunk
-      const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA), C::ROWB, 2 * C::ROWB);
-      const uint64_t bdesc0 = tc::desc_kmajor(tc::smem_addr(sB), NB16, 128);
       if (!PAIR && A.bimg != nullptr) tc::mbar_wait(&w_bar, 0);  // weight image landed
       int it = 0;
       for (int tile = first; tile < tile_end; tile += stride, ++it) {
@@ -247,14 +245,16 @@ conv_tc4_pool_kernel(const ConvArgs A) {
         }
         trace_ev(A, it, 2);
         tc::fence_after();
-        // base descriptor + constant start-address offsets (see k_conv_tc4_pool3.cuh / tools/probes/issue_probe.cu)
-        const uint64_t abuf = adesc0 + (uint64_t)(buf * (C::A_BYTES >> 4));
+        // (descriptors rebuilt per MMA: the base + constant-offset form that runs the issue probe and the other kernels
+        // at the 64-clk floor made this 2-CTA/SM kernel slower in the bench step, 0.54 -> 0.79 ms per 16384 images)
+        const uint32_t a0 = tc::smem_addr(sA + buf * C::A_BYTES), b0 = tc::smem_addr(sB);
 #pragma unroll
         for (int sp = 0; sp < C::SP; ++sp)
 #pragma unroll
           for (int t = 0; t < KS; ++t) {
-            const uint64_t ad = abuf + (uint64_t)(((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16) >> 4);
-            const uint64_t bd = bdesc0 + (uint64_t)(((sp * KS + t) * 2 * NB16) >> 4);
+            const uint32_t off = (uint32_t)((t & 1) * C::PLANE + (2 * sp) * C::ROWB + (t >> 1) * 16);
+            const uint64_t ad = tc::desc_kmajor(a0 + off, C::ROWB, 2 * C::ROWB);
+            const uint64_t bd = tc::desc_kmajor(b0 + (uint32_t)((sp * KS + t) * 2) * NB16, NB16, 128);
             if constexpr (PAIR) tc::mma_mxf4_pair(tmem, ad, bd, idesc, sfa, sfb, 1u);
             else tc::mma_mxf4(tmem, ad, bd, idesc, sfa, sfb, 1u);
           }
