@@ -17,14 +17,20 @@ namespace bnn {
 template <int NT>
 struct DenseTc4Cfg {
   static constexpr int KC = 16;                         // words per stage (8 MMAs)
+#ifndef BNN_DENSE_NBR
+#define BNN_DENSE_NBR 3
+#endif
+  // weight-image ring: stage use u + NBR - 2 is bulk-copied while use u is expanded (its slot was read by MMA(u - 2));
+  // with 2 slots every stage's 32 KB copy was issued only when its own expansion began
+  static constexpr int NBR = NT > 128 ? 2 : BNN_DENSE_NBR;
   static constexpr uint32_t A_BYTES = KC * 128 * 16;    // 32 KB
   static constexpr uint32_t B_BYTES = KC * NT * 16;
   static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
   static constexpr int LUTC = 8;                        // LUT copies (lane & 7): fewer bank conflicts
   static constexpr int RING = NT > 128 ? 2 : 4;         // TMA ring of raw activation stages (TMAX variant)
   static constexpr uint32_t RAWB = 128 * KC * 4;        // one raw stage: 128 images x KC words
-  static constexpr uint32_t RAW_OFF = (2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 * LUTC + 127) / 128 * 128;
-  static constexpr uint32_t SMEM = 2 * (A_BYTES + B_BYTES) + NT * 4 + 256 * 4 * LUTC + 16;
+  static constexpr uint32_t RAW_OFF = (2 * A_BYTES + NBR * B_BYTES + NT * 4 + 256 * 4 * LUTC + 127) / 128 * 128;
+  static constexpr uint32_t SMEM = 2 * A_BYTES + NBR * B_BYTES + NT * 4 + 256 * 4 * LUTC + 16;
   static constexpr uint32_t SMEM_TMAX = RAW_OFF + RING * RAWB + 16;
 };
 
@@ -75,10 +81,10 @@ dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
   constexpr int KC = C::KC;
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sA = dsm;                                  // 2 x [kw][128][16]
-  uint8_t* sB = dsm + 2 * C::A_BYTES;                 // 2 x [kw][NT][16]
-  float* s_thr = reinterpret_cast<float*>(sB + 2 * C::B_BYTES);
+  uint8_t* sB = dsm + 2 * C::A_BYTES;                 // NBR x [kw][NT][16]
+  float* s_thr = reinterpret_cast<float*>(sB + C::NBR * C::B_BYTES);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(s_thr + NT);  // LUTC interleaved copies: entry i, copy c at LUTC i + c
-  __shared__ uint64_t bar_stage[2], bar_acc, bar_b[2], bar_raw[C::RING];
+  __shared__ uint64_t bar_stage[2], bar_acc, bar_b[C::NBR], bar_raw[C::RING];
   uint8_t* sRaw = dsm + C::RAW_OFF;  // TMAX: RING x [128 images][KC words]
   __shared__ uint32_t tmem_base_s;
 
@@ -103,8 +109,8 @@ dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
     tc::mbar_init(&bar_stage[0], 1);
     tc::mbar_init(&bar_stage[1], 1);
     tc::mbar_init(&bar_acc, 1);
-    tc::mbar_init(&bar_b[0], 1);
-    tc::mbar_init(&bar_b[1], 1);
+#pragma unroll
+    for (int i = 0; i < C::NBR; ++i) tc::mbar_init(&bar_b[i], 1);
 #pragma unroll
     for (int i = 0; i < C::RING; ++i) tc::mbar_init(&bar_raw[i], 1);
     tc::fence_mbar_init();
@@ -193,6 +199,15 @@ dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
         "l"(reinterpret_cast<uint64_t>(&xmap)), "r"(st * KC), "r"(t * 128), "r"(tc::smem_addr(bar))
         : "memory");
   };
+  // weight image of stage use u into ring slot u % NBR (a per-net image: independent of the predecessor layer)
+  auto issue_b = [&](uint32_t u) {
+    const int t = (int)blockIdx.x + (int)(u / nst) * (int)gridDim.x, st = st0 + (int)(u % nst);
+    if (t >= ntiles) return;
+    tc::stage_image(sB + (u % C::NBR) * C::B_BYTES, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES,
+                    &bar_b[u % C::NBR]);
+  };
+  if (b_img && tid == 0)
+    for (uint32_t u = 0; u < (uint32_t)(C::NBR - 2); ++u) issue_b(u);
   griddep_wait();  // activations of the predecessor layer
   if constexpr (TMAX) {
     if (tid == 0)
@@ -205,10 +220,10 @@ dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
       const int s = stage_uses & 1;
       if (stage_uses >= 2) tc::mbar_wait(&bar_stage[s], ((stage_uses - 2) >> 1) & 1);
       uint8_t* a = sA + s * C::A_BYTES;
-      uint8_t* b = sB + s * C::B_BYTES;
+      uint8_t* b = sB + (stage_uses % C::NBR) * C::B_BYTES;
       const int w0 = st * KC;
-      if (b_img && tid == 0)  // the stage's weight operand: one bulk copy of the pre-expanded image (L2-resident)
-        tc::stage_image(b, A.bimg + ((size_t)g * nstage + st) * C::B_BYTES, C::B_BYTES, &bar_b[s]);
+      // the weight operand of stage use u + NBR - 2 (pre-expanded image, L2-resident); its slot was read by MMA(u - 2)
+      if (b_img && tid == 0) issue_b(stage_uses + C::NBR - 2);
       if constexpr (TMAX) {
         const uint32_t slot = stage_uses % C::RING;
         tc::mbar_wait(&bar_raw[slot], (stage_uses / C::RING) & 1);
@@ -240,7 +255,7 @@ dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
       tc::fence_after();
       if (tid == 0) {
         if constexpr (TMAX) issue_raw(stage_uses + C::RING);  // the slot was read by every thread (barrier above)
-        if (b_img) tc::mbar_wait(&bar_b[s], (stage_uses >> 1) & 1);  // weight stage landed
+        if (b_img) tc::mbar_wait(&bar_b[stage_uses % C::NBR], (stage_uses / C::NBR) & 1);  // weight stage landed
         const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(a), 128 * 16, 128);
         const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(b), NT * 16, 128);
 #pragma unroll
