@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--total-batch", type=int, default=262144,
                     help="images per step over all GPUs (BASELINE config 5; strong scaling, contiguous shards)")
     ap.add_argument("--batch", type=int, default=0, help="if set: fixed images per GPU per step (weak scaling)")
-    ap.add_argument("--chunk", type=int, default=16384, help="bnn_net max_batch (images per internal chunk; 16384 measured best: 2 chunks per step on two streams)")
+    ap.add_argument("--chunk", type=int, default=65536, help="bnn_net max_batch (images per internal chunk; 65536 measured best at 262144 images per step: 14.2-14.4 vs 14.2 M img/s for 16384, tools/ab_chunks.sh)")
     ap.add_argument("--mode", default="rgb", choices=sorted(MODES))
     ap.add_argument("--seed", type=int, default=2018)
     ap.add_argument("--no-e2e", action="store_true")

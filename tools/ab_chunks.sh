@@ -1,4 +1,4 @@
-for rep in 1 2; do for c in 8192 16384 32768 65536; do
+for rep in 1 2; do for c in ${CHUNKS:-8192 16384 32768 65536}; do
 echo -n "chunk $c: "; timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --check 0 --chunk $c 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['stage_ms_per_step']

@@ -13,4 +13,4 @@ done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/${T}_launches.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"^(conv1_fp4_pool|conv_tc4_pool3|dense_tc4_kernel)" -c 3 -o /tmp/${T}_full python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > gpurun_out/${T}_full.log 2>&1; echo "full rc=$?"
 ncu -i /tmp/${T}_full.ncu-rep --page raw --csv > gpurun_out/${T}_full_raw.csv 2>&1
-python tools/ncu_summary.py /tmp/${T}_full.ncu-rep 16384 gpurun_out/${T}_ncu > gpurun_out/${T}_ncu_summary.log 2>&1; cp profiles/ncu_traffic.json gpurun_out/${T}_ncu_traffic.json
+python tools/ncu_summary.py /tmp/${T}_full.ncu-rep 65536 gpurun_out/${T}_ncu > gpurun_out/${T}_ncu_summary.log 2>&1; cp profiles/ncu_traffic.json gpurun_out/${T}_ncu_traffic.json
