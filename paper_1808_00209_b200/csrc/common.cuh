@@ -25,11 +25,12 @@ BNN_DEV int dp4a_us(uint32_t a, uint32_t b, int c) {
 
 // Division by a runtime-invariant divisor d (1 <= d < 2^31) for numerators n < 2^31, as a
 // multiply-high + add + shift (Granlund-Montgomery): l = ceil(log2 d),
-// m = floor(2^32 (2^l - d) / d) + 1, q = (umulhi(m, n) + n) >> l.  Built on the host.
+// m = floor(2^32 (2^l - d) / d) + 1, q = (umulhi(m, n) + n) >> l.  Built on the host (launch arguments) or once
+// per thread (luma_band_kernel).
 struct FastDiv {
   uint32_t d, m, l;
   __host__ __device__ FastDiv() : d(1), m(1), l(0) {}
-  __host__ explicit FastDiv(uint32_t div) : d(div) {
+  __host__ __device__ explicit FastDiv(uint32_t div) : d(div) {
     l = 0;
     while ((1ull << l) < div) ++l;
     m = (uint32_t)((((1ull << l) - div) << 32) / div + 1);

@@ -196,9 +196,13 @@ __global__ void __launch_bounds__(256) luma_band_kernel(const uint8_t* __restric
   }
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
   __syncthreads();
-  for (int r = warp; r < nrows + 2; r += NWARP) {
+  // (row, 4-pixel group) units flattened over the block: every lane busy (w / 4 = 24 groups per row would leave
+  // a quarter of a row-per-warp mapping idle); the row by a multiply-high division
+  const FastDiv fdg((uint32_t)wg);
+  for (int k = threadIdx.x; k < (nrows + 2) * wg; k += blockDim.x) {
+    const int r = (int)fdg.div((uint32_t)k), g = k - r * wg;
     uint8_t* lr = lum + r * lw;
-    for (int g = lane; g < wg; g += 32) {
+    {
       const uint32_t v[4] = {raw[r * rw + 3 * g], raw[r * rw + 3 * g + 1], raw[r * rw + 3 * g + 2], 0u};
       // R15: Y = (299 R + 587 G + 114 B + 500) div 1000; the sum as two DP2A (bytes of the word pairs), the division
       // as a multiply-high by ceil(2^32 / 1000) (exact for numerators < 2^22)
@@ -217,9 +221,10 @@ __global__ void __launch_bounds__(256) luma_band_kernel(const uint8_t* __restric
   __syncthreads();
   const int tg = (mode == kThreshGray) ? u8_threshold(-Tt[0]) : 0;  // Y > -T <=> Y > tg (R14), tg in [-1, 255]
   const uint32_t t4 = (uint32_t)(tg < 0 ? 0 : tg) * 0x01010101u;
-  for (int r = warp; r < nrows; r += NWARP) {
+  for (int k = threadIdx.x; k < nrows * wg; k += blockDim.x) {
+    const int r = (int)fdg.div((uint32_t)k), g = k - r * wg;
     const uint8_t* lc = lum + (r + 1) * lw;
-    for (int g = lane; g < wg; g += 32) {
+    {
       const int b = 4 + 4 * g;  // byte of pixel 4 g in its luma row
       const uint32_t C = *reinterpret_cast<const uint32_t*>(lc + b);
       uint32_t m0, m1, m2;
