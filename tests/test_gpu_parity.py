@@ -401,6 +401,28 @@ def forward_vehicle_case(cuda, orc, mode, fused):
     assert np.array_equal(cls.cpu().numpy(), ref_cls)
 
 
+@pytest.mark.parametrize("k1,k2,hw", [(3, 5, 64), (5, 3, 48), (5, 5, 96)])
+def test_forward_fused_cluster_shapes(cuda, orc, k1, k2, hw):
+    """The whole-network cluster kernel (f1) on vehicle-shaped nets other than the vehicle: conv1 k = 3 / 5, conv2
+    k = 3 / 5, 64 / 48 / 96-pixel images (1 .. 3 pooled conv1 rows per CTA), thresholds and flips on every hidden
+    layer; batches of 1 and 5 images against the oracle."""
+    spec = dict(h=hw, w=hw, c=3, layers=[dict(kind="conv", k=k1, c_out=32, pool=2), dict(kind="conv", k=k2, c_out=32, pool=2),
+                                         dict(kind="dense", l=100), dict(kind="dense", l=100), dict(kind="dense", l=4)])
+    net, layers, T = build_net(cuda, spec, 1, 4400 + 10 * k1 + k2, max_batch=8, thr=True)
+    imgs = synth.images(5, hw, hw, 3, 4401 + hw)
+    try:
+        cuda.set_option("fused_max_n", 8)
+        assert cuda.forward_launches(net, 1) == 1, "the whole-network kernel must take this net"
+        outs = [net.forward(dev(imgs[:1])), net.forward(dev(imgs))]
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("fused_max_n", 0)
+    onet = oracle_net(orc, spec, 1, layers, T)
+    for (lg, cls), x in zip(outs, (imgs[:1], imgs)):
+        ref_l, ref_c = onet.forward(x.numpy(), threads=5)
+        assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)
+
+
 @pytest.mark.parametrize("algo", [1, 2, 3, 4])
 @pytest.mark.parametrize("mode", [1, 0])
 def test_forward_vehicle_unfused_first_layer(cuda, orc, mode, algo):
