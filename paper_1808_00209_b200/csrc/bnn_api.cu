@@ -149,6 +149,7 @@ int g_opt_dense_ksplit = 1;   // 1: dense_tc4 splits K over grid.z when its tile
 int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run on tcgen05 (kind::mxf4)
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
 
+int g_opt_fused_tc = 1;       // 1: the cluster kernel runs conv2 on the tensor cores (pool-in-N mxf4, one tile per CTA)
 int g_opt_fused_cluster = 1;  // 1: the fused small-batch path is the thread-block-cluster kernel (DSMEM, cluster barriers); 0: cooperative
 int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
@@ -1000,6 +1001,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "first_real_tma") == 0) { g_opt_first_real_tma = value; return BNN_OK; }
   if (strcmp(key, "luma_band") == 0) { g_opt_luma_band = value; return BNN_OK; }
   if (strcmp(key, "fused_max_n") == 0) { g_opt_fused_max_n = value; return BNN_OK; }
+  if (strcmp(key, "fused_tc") == 0) { g_opt_fused_tc = value; return BNN_OK; }
   if (strcmp(key, "alg1") == 0) { g_opt_alg1 = value; return BNN_OK; }
   if (strcmp(key, "csa") == 0) { g_opt_csa = value; return BNN_OK; }
   if (strcmp(key, "big_img") == 0) { g_opt_big_img = value; return BNN_OK; }
@@ -1369,7 +1371,11 @@ bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_
     *launched = true;
     return check_launch("fused_cluster_kernel");
   };
-  if (b.k == 5) return go(fused_cluster_kernel<5>);
+  // conv2 on the tensor cores inside the cluster when its pool-in-N weight image exists (k = 5, 32 -> 32 channels)
+  const bool tc2 = g_opt_fused_tc && b.k == 5 && b.bimg != nullptr && b.c_in == 32 && b.c_out == 32 && b.pool == 2 &&
+                   net->w % 32 == 0;  // (conv2 tiles' 8-word pooled rows stay inside the W/4-word map rows)
+  A.w2img = tc2 ? b.bimg : nullptr;
+  if (b.k == 5) return tc2 ? go(fused_cluster_kernel<5, true>) : go(fused_cluster_kernel<5>);
   if (b.k == 3) return go(fused_cluster_kernel<3>);
   return go(fused_cluster_kernel<1>);
 }

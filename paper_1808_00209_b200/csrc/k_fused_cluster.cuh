@@ -29,6 +29,7 @@
 #include <cooperative_groups.h>
 
 #include "k_conv.cuh"  // csa_popc
+#include "k_conv_tc4_pool.cuh"  // the pool-in-N conv2 operand layout, weight image and epilogue
 #include "k_fused_small.cuh"
 #include "tc.cuh"
 
@@ -39,7 +40,7 @@ constexpr int kClusterMax = 16;
 // shared-memory layout of fused_cluster_kernel (32-bit words; every block 16-byte aligned), for a cluster of
 // `ncta` CTAs -- the host sizes it for the smallest cluster it may get (8)
 struct FusedClusterLayout {
-  int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, total;  // word offsets, total words
+  int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, tcb, tca, tcl, total;  // word offsets, total words
   int rp, raw_rows, m1, pb;  // pooled rows per CTA, staged raw rows, FC1 rows per CTA, bit-image row pitch (bytes)
   __host__ __device__ FusedClusterLayout(int H, int W, int C, int K1, int ncta, int l1, int l2, int l3) {
     auto up4 = [](int v) { return (v + 3) & ~3; };
@@ -60,15 +61,24 @@ struct FusedClusterLayout {
     f2w = f1w + up4(m1 * dw1);
     f3w = f2w + up4(l2 * dw2);
     tf = f3w + up4(l3 * dw3);                 // FC1 thr [m1], flip [m1]; FC2 thr [l2], flip [l2] (int)
-    total = tf + up4(2 * (m1 + l2));
+    // tensor-core conv2 (K2 = 5, 32 channels): weight image, A operand (both 1024-byte aligned), LUT + start values
+    tcb = (tf + up4(2 * (m1 + l2)) + 255) & ~255;
+    tca = tcb + (int)(ConvTc4PoolCfg<5>::B_BYTES / 4);
+    tcl = tca + ((int)(ConvTc4PoolCfg<5>::A_BYTES / 4) + 255) / 256 * 256;
+    total = tcl + 256 * (1 + ConvTc4PoolCfg<5>::LUTC) + 32;
   }
 };
 
-template <int K2>
+// TC2: conv2 (K2 = 5, 32 -> 32 channels, pool 2) on the tensor cores -- one 16 x 8 pooled-pixel tile per CTA, the
+// pool window folded into N exactly as conv_tc4_pool_kernel (18 mxf4 MMAs of M128 N128 K64 into TMEM), the A operand
+// expanded from the CTA's local conv1 copy, the start values C0 - (thr' + 1) and the s16 sign gather of that
+// kernel; each pooled word is stored into every CTA's conv2 map
+template <int K2, bool TC2 = false>
 __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(const FusedSmallArgs A) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint32_t cl_smem[];
-  __shared__ uint64_t w_bar, raw_bar;
+  __shared__ uint64_t w_bar, raw_bar, tc_wbar, tc_mma;
+  __shared__ uint32_t tmem_s;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -115,6 +125,12 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     tc::mbar_init(&raw_bar, 1);
     tc::fence_mbar_init();
     if (A.n > 0 && rhi > rlo) stage_raw(0);
+    if constexpr (TC2) {
+      tc::mbar_init(&tc_wbar, 1);
+      tc::mbar_init(&tc_mma, 1);
+      tc::fence_mbar_init();
+      tc::stage_image(cl_smem + Lo.tcb, A.w2img, ConvTc4PoolCfg<5>::B_BYTES, &tc_wbar);  // waited before the first MMA
+    }
     const uint32_t b1 = (uint32_t)n1 * dw1 * 4;  // dw1 % 4 == 0 (host check)
     tc::mbar_arrive_expect_tx(&w_bar, b1);
     if (b1) tc::stage_chunks(cl_smem + Lo.f1w, A.f1 + (int64_t)o1 * dw1, b1, &w_bar);
@@ -162,6 +178,32 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       s_f2[j] = A.flip_f2 != nullptr ? A.flip_f2[j] : 0;
     }
   for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h1[j] = 0u;
+  using TP = ConvTc4PoolCfg<5>;
+  const int tiles2_x = (W1 + TP::TW - 1) / TP::TW, tiles2 = ((H1 + TP::TH - 1) / TP::TH) * tiles2_x;
+  const bool has_tile2 = TC2 && rank < tiles2;
+  uint32_t* s_lut2 = cl_smem + Lo.tcl;            // LUTC interleaved copies of the bits -> e2m1 table
+  float* s_init2 = reinterpret_cast<float*>(s_lut2 + 256 * TP::LUTC);  // C0 - (thr' + 1) per TMEM column
+  if constexpr (TC2) {
+    if (warp == 0) {
+      tc::tmem_alloc<256>(&tmem_s);
+      tc::fence_before();  // (the address is read after the cluster barrier below)
+    }
+    if (threadIdx.x < 256) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v |= (((threadIdx.x >> (7 - k)) & 1) ? 0x2u : 0xAu) << (4 * k);
+#pragma unroll
+      for (int c = 0; c < TP::LUTC; ++c) s_lut2[TP::LUTC * threadIdx.x + c] = v;
+    }
+    if (threadIdx.x < 32) {  // (as conv_tc4_pool_kernel: 32 valid channels)
+      const int o = tc4_col_channel(threadIdx.x), S_TOT = 25 * 32;
+      const bool f = A.flip2 != nullptr && A.flip2[o] != 0;
+      int tt = A.thr2 != nullptr ? A.thr2[o] : 0;
+      tt = max(-S_TOT - 1, min(S_TOT, tt));
+      if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
+      s_init2[threadIdx.x] = 12582912.0f - (float)(tt + 1);
+    }
+  }
   if (rank == 0) fused_trace(A, 64, 1);
   // every CTA of the cluster is running and has zeroed h1 (the first DSMEM atomics into it follow two phase
   // barriers later); the barrier's wait side synchronises the CTA (mbarrier initialisation, staged values)
@@ -186,7 +228,6 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       }
     }
     __syncthreads();
-    if (rank == 0) fused_trace(A, img, 6);
     // ---- phase 1b: conv1 + pool over pooled rows [py0, py1) -> every CTA's y1
 #pragma unroll 2
     for (int u = py0 * W1 + warp; u < py1 * W1; u += kFusedWarps) {
@@ -206,13 +247,95 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         any |= (S1 - 2 * pc > th1) != fl1;
       }
       const uint32_t word = ballot_pack(any);
-      // (no "memory" clobber: the next pixel's loads may move above the store; the cluster barrier orders it)
+      // (no "memory" clobber: the next pixel's loads may move above the store; the cluster barrier orders it.
+      // Writing the own copy first and broadcasting 16-byte pieces after the loop measured the same.)
       if (lane < ncta) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(y1_c + 4 * u), "r"(word));
     }
+    if (rank == 0) fused_trace(A, img, 6);  // (thread 0: its own warp's pixels done)
     cl.sync();
     if (rank == 0) fused_trace(A, img, 1);
     // ---- phase 2: conv2 + pool from the local y1 -> every CTA's y2
-    {
+    if constexpr (TC2) {
+      tc::fence_after();
+      const uint32_t tmem = tmem_s;
+      if (has_tile2) {
+        const int ty = rank / tiles2_x, tx = rank - ty * tiles2_x, oy0 = ty * TP::TH, ox0 = tx * TP::TW;
+        uint8_t* sA2 = reinterpret_cast<uint8_t*>(cl_smem + Lo.tca);
+        // start values of the 4 x 32 accumulator columns (warps 0-3: TMEM lane quarters); block scales 1.0
+        if (warp < 4) {
+          const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+          uint32_t iv[16];
+#pragma unroll
+          for (int cb = 0; cb < 32; cb += 16) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) iv[k] = __float_as_uint(s_init2[cb + k]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tmem_st16(lb + (uint32_t)(q * 32 + cb), iv);
+          }
+          if (img == 0) {
+            tc::tmem_st8_same(lb + 128, 0x7F7F7F7Fu);
+            tc::tmem_st8_same(lb + 136, 0x7F7F7F7Fu);
+          }
+          tc::tmem_st_wait();
+        }
+        // A operand: the tile's halo pixels (IR x IC) as e2m1 in two column-parity planes (k_conv_tc4_pool.cuh)
+        const uint32_t* my_lut = s_lut2 + (lane & (TP::LUTC - 1));
+        for (int p = threadIdx.x; p < TP::NPIX; p += blockDim.x) {
+          const int r = p / TP::IC, c = p - r * TP::IC;
+          const int gy = oy0 - TP::R + r, gx = ox0 - TP::R + c;
+          const uint32_t w = (gy >= 0 && gy < H1 && gx >= 0 && gx < W1) ? y1[gy * W1 + gx] : 0u;  // outside: -1 (R4)
+          uint32_t o4[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o4[k] = my_lut[TP::LUTC * ((w >> (24 - 8 * k)) & 0xFFu)];
+          *reinterpret_cast<uint4*>(sA2 + (c & 1) * TP::PLANE + r * TP::ROWB + (c >> 1) * 16) = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (threadIdx.x == 0) {
+          if (img == 0) tc::mbar_wait(&tc_wbar, 0);  // the weight image landed
+          constexpr uint32_t idesc = tc::idesc_mxf4(128, 128);
+          const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA2), TP::ROWB, 2 * TP::ROWB);
+          const uint64_t bdesc0 = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.tcb), 128 * 16, 128);
+#pragma unroll
+          for (int sp = 0; sp < TP::SP; ++sp)
+#pragma unroll
+            for (int t = 0; t < TP::KS; ++t)
+              tc::mma_mxf4(tmem, adesc0 + (uint64_t)(((t & 1) * TP::PLANE + (2 * sp) * TP::ROWB + (t >> 1) * 16) >> 4),
+                           bdesc0 + (uint64_t)(((sp * TP::KS + t) * 2 * 128 * 16) >> 4), idesc, tmem + 128, tmem + 136, 1u);
+          tc::commit(&tc_mma);
+        }
+        // epilogue (warps 0-3, thread = pooled pixel of the tile): pooled bit = NOT(all four acc'_q < 0)
+        if (warp < 4) {
+          tc::mbar_wait(&tc_mma, (uint32_t)(img & 1));
+          __syncwarp();
+          tc::fence_after();
+          const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+          uint32_t a[16], b[16], c[16], d[16];
+          tc::tmem_ld16_p16(lb + 0 * 32, a);
+          tc::tmem_ld16_p16(lb + 1 * 32, b);
+          tc::tmem_ld16_p16(lb + 2 * 32, c);
+          tc::tmem_ld16_p16(lb + 3 * 32, d);
+          tc::tmem_ld_wait();
+          uint32_t neg = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            uint32_t x;
+            asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(x) : "r"(a[j]), "r"(b[j]), "r"(c[j]));
+            x = x & d[j] & 0x80008000u;
+            neg = __umulhi(neg, 0x80000000u) + x;
+          }
+          const int m = warp * 32 + lane, py = (oy0 >> 1) + m / TP::PW, px = (ox0 >> 1) + m % TP::PW;
+          if (py < H2 && px < W2) {
+            const uint32_t word = ~neg, addr = tc::smem_addr(y2 + py * W2 + px);
+            for (int r = 0; r < ncta; ++r)
+              asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(tc::mapa(addr, (uint32_t)r)), "r"(word));
+          }
+          tc::fence_before();  // (TMEM reads done before the next image's start values)
+        }
+      }
+    } else {
       constexpr int RR = (K2 - 1) / 2;
       const int S2 = KK2 * 32;
       for (int u = gw; u < H2 * W2; u += nw) {
@@ -288,6 +411,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   if (rank == 0) fused_trace(A, 64, 2);
   cl.sync();  // no CTA exits while another may still address its shared memory
   if (rank == 0) fused_trace(A, 64, 3);
+  if constexpr (TC2) {
+    if (warp == 0) tc::tmem_dealloc<256>(tmem_s);
+  }
 }
 
 }  // namespace bnn

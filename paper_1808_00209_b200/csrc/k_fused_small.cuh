@@ -43,6 +43,8 @@ struct FusedSmallArgs {
   int32_t* cls;     // [n] or null
   unsigned* barrier;  // [2]: grid-barrier count, FC1-done count (zero at launch; the tail CTA re-arms them)
   unsigned long long* trace;  // diagnostics build (bnn_set_trace, trace_layer 2): CTA 0's phase globaltimer stamps
+  const uint8_t* w2img;       // conv2's pool-in-N e2m1 weight image (prep_tc4_pool_kernel) for the cluster kernel's
+                              // tensor-core conv2 phase, or null
 };
 
 // phase timestamp (ns, %globaltimer) ev of image img into A.trace[img * 8 + ev] (diagnostics build only)

@@ -23,7 +23,7 @@ for n in (1, 1, 1, 4):
     t = tr.view(65, 8)[:n].cpu()
     for i in range(n):
         d = [int(t[i, k + 1] - t[i, k]) for k in range(4)]
-        print("n=%d img %d: conv1 %d ns (raw staged +%d, bit image +%d), conv2 %d ns, FC1 %d ns, FC2+FC3+argmax %d ns (FC2 +%d),"
+        print("n=%d img %d: conv1 %d ns (raw staged +%d, warp 0 pixels done +%d), conv2 %d ns, FC1 %d ns, FC2+FC3+argmax %d ns (FC2 +%d),"
               " total %d ns" % (n, i, d[0], int(t[i, 5] - t[i, 0]), int(t[i, 6] - t[i, 0]), d[1], d[2], d[3],
                                 int(t[i, 7] - t[i, 3]), sum(d)))
     k = tr.view(65, 8)[64].cpu()
