@@ -1375,7 +1375,10 @@ bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_
   const bool tc2 = g_opt_fused_tc && b.k == 5 && b.bimg != nullptr && b.c_in == 32 && b.c_out == 32 && b.pool == 2 &&
                    net->w % 32 == 0;  // (conv2 tiles' 8-word pooled rows stay inside the W/4-word map rows)
   A.w2img = tc2 ? b.bimg : nullptr;
-  if (b.k == 5) return tc2 ? go(fused_cluster_kernel<5, true>) : go(fused_cluster_kernel<5>);
+  // conv1 on the tensor cores (conv1_fp4's strips and weight image) for the vehicle geometry
+  const bool tc1 = tc2 && a.k == 5 && net->c == 3 && a.c_out == 32 && a.pool == 2 && a.bimg != nullptr && a.bimg_fp4 == 1;
+  A.w1img = tc1 ? a.bimg : nullptr;
+  if (b.k == 5) return tc1 ? go(fused_cluster_kernel<5, true, true>) : (tc2 ? go(fused_cluster_kernel<5, true>) : go(fused_cluster_kernel<5>));
   if (b.k == 3) return go(fused_cluster_kernel<3>);
   return go(fused_cluster_kernel<1>);
 }

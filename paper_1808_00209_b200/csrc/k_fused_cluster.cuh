@@ -30,6 +30,7 @@
 
 #include "k_conv.cuh"  // csa_popc
 #include "k_conv_tc4_pool.cuh"  // the pool-in-N conv2 operand layout, weight image and epilogue
+#include "k_conv1_fp4.cuh"     // the conv1 strip layout, threshold masks, e2m1 nibbles, weight image
 #include "k_fused_small.cuh"
 #include "tc.cuh"
 
@@ -40,7 +41,7 @@ constexpr int kClusterMax = 16;
 // shared-memory layout of fused_cluster_kernel (32-bit words; every block 16-byte aligned), for a cluster of
 // `ncta` CTAs -- the host sizes it for the smallest cluster it may get (8)
 struct FusedClusterLayout {
-  int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, tcb, tca, tcl, total;  // word offsets, total words
+  int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, tcb, tca, tcl, c1b, c1c, c1a, c1r, total;  // word offsets
   int rp, raw_rows, m1, pb;  // pooled rows per CTA, staged raw rows, FC1 rows per CTA, bit-image row pitch (bytes)
   __host__ __device__ FusedClusterLayout(int H, int W, int C, int K1, int ncta, int l1, int l2, int l3) {
     auto up4 = [](int v) { return (v + 3) & ~3; };
@@ -65,7 +66,12 @@ struct FusedClusterLayout {
     tcb = (tf + up4(2 * (m1 + l2)) + 255) & ~255;
     tca = tcb + (int)(ConvTc4PoolCfg<5>::B_BYTES / 4);
     tcl = tca + ((int)(ConvTc4PoolCfg<5>::A_BYTES / 4) + 255) / 256 * 256;
-    total = tcl + 256 * (1 + ConvTc4PoolCfg<5>::LUTC) + 32;
+    // tensor-core conv1 (K1 = 5, 3 channels): weight image, offset-MMA constants, A strips, raw box
+    c1b = (tcl + 256 * (1 + ConvTc4PoolCfg<5>::LUTC) + 32 + 255) & ~255;
+    c1c = c1b + (int)(Conv1Fp4Cfg<5>::B_BYTES / 4);
+    c1a = c1c + (int)(Conv1Fp4Cfg<5>::CONST_BYTES / 4);
+    c1r = c1a + (int)((Conv1Fp4Cfg<5>::A_BYTES / 4 + 31) & ~31u);
+    total = c1r + (int)(Conv1Fp4Cfg<5>::RAW_BYTES / 4) + 32;
   }
 };
 
@@ -73,7 +79,10 @@ struct FusedClusterLayout {
 // pool window folded into N exactly as conv_tc4_pool_kernel (18 mxf4 MMAs of M128 N128 K64 into TMEM), the A operand
 // expanded from the CTA's local conv1 copy, the start values C0 - (thr' + 1) and the s16 sign gather of that
 // kernel; each pooled word is stored into every CTA's conv2 map
-template <int K2, bool TC2 = false>
+// TC1: conv1 (K1 = 5, 3 input channels, SIGN / THRESH_RGB) on the tensor cores as conv1_fp4_pool_kernel computes it --
+// one 16 x 8 pooled-pixel tile per CTA and round (18 tiles for 96 x 96), the raw box staged by word loads, strips of
+// {0, 1} e2m1 built from the threshold masks, the offset MMA (C0) + 3 mxf4 MMAs, the s16 sign gather
+template <int K2, bool TC2 = false, bool TC1 = false>
 __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(const FusedSmallArgs A) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) uint32_t cl_smem[];
@@ -124,12 +133,15 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     tc::mbar_init(&w_bar, 1);
     tc::mbar_init(&raw_bar, 1);
     tc::fence_mbar_init();
-    if (A.n > 0 && rhi > rlo) stage_raw(0);
-    if constexpr (TC2) {
+    if (!TC1 && A.n > 0 && rhi > rlo) stage_raw(0);
+    if constexpr (TC2 || TC1) {
       tc::mbar_init(&tc_wbar, 1);
       tc::mbar_init(&tc_mma, 1);
       tc::fence_mbar_init();
-      tc::stage_image(cl_smem + Lo.tcb, A.w2img, ConvTc4PoolCfg<5>::B_BYTES, &tc_wbar);  // waited before the first MMA
+      // weight images, waited before the first MMA
+      tc::mbar_arrive_expect_tx(&tc_wbar, (TC2 ? ConvTc4PoolCfg<5>::B_BYTES : 0u) + (TC1 ? Conv1Fp4Cfg<5>::B_BYTES : 0u));
+      if (TC2) tc::stage_chunks(cl_smem + Lo.tcb, A.w2img, ConvTc4PoolCfg<5>::B_BYTES, &tc_wbar);
+      if (TC1) tc::stage_chunks(cl_smem + Lo.c1b, A.w1img, Conv1Fp4Cfg<5>::B_BYTES, &tc_wbar);
     }
     const uint32_t b1 = (uint32_t)n1 * dw1 * 4;  // dw1 % 4 == 0 (host check)
     tc::mbar_arrive_expect_tx(&w_bar, b1);
@@ -183,7 +195,14 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   const bool has_tile2 = TC2 && rank < tiles2;
   uint32_t* s_lut2 = cl_smem + Lo.tcl;            // LUTC interleaved copies of the bits -> e2m1 table
   float* s_init2 = reinterpret_cast<float*>(s_lut2 + 256 * TP::LUTC);  // C0 - (thr' + 1) per TMEM column
-  if constexpr (TC2) {
+  if constexpr (TC1) {  // the offset MMA's constant operands: A = 1.0 everywhere, B = 6.0 at element 0 of a chunk row
+    uint8_t* sC1 = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1c);
+    for (int i = threadIdx.x; i < (int)(Conv1Fp4Cfg<5>::CONST_BYTES / 16); i += blockDim.x)
+      *reinterpret_cast<uint4*>(sC1 + 16 * i) = i < (int)(Conv1Fp4Cfg<5>::CONST_BYTES / 32)
+                                                    ? make_uint4(0x22222222u, 0x22222222u, 0x22222222u, 0x22222222u)
+                                                    : make_uint4(0x7u, 0u, 0u, 0u);
+  }
+  if constexpr (TC2 || TC1) {
     if (warp == 0) {
       tc::tmem_alloc<256>(&tmem_s);
       tc::fence_before();  // (the address is read after the cluster barrier below)
@@ -209,8 +228,127 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   // barriers later); the barrier's wait side synchronises the CTA (mbarrier initialisation, staged values)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 
+  uint32_t mma_ph = 0;  // parity of the next tc_mma completion (conv1 tiles, then the conv2 tile, per image)
   for (int img = 0; img < A.n; ++img) {
     if (rank == 0) fused_trace(A, img, 0);
+    if constexpr (TC1) {
+      using C1 = Conv1Fp4Cfg<5>;
+      tc::fence_after();
+      const uint32_t tmem = tmem_s;
+      const int t1x = (W1 + C1::PW - 1) / C1::PW, ntile1 = ((H1 + C1::PH - 1) / C1::PH) * t1x;
+      uint8_t* box = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1r);
+      uint8_t* sA1 = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1a);
+      const uint8_t* xi = A.x + (int64_t)img * A.H * rowb;
+      // builder constants (k_conv1_fp4.cuh, kBinRgb): per-channel 16-bit-lane threshold terms
+      uint32_t Ev[3], Od[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        Ev[m] = (uint32_t)(0x7FFF - t[m]) | ((uint32_t)(0x7FFF - t[(m + 2) % 3]) << 16);
+        Od[m] = (uint32_t)(0x7FFF - t[(m + 1) % 3]) | ((uint32_t)(0x7FFF - t[m]) << 16);
+      }
+      const bool zero_ok = t[0] >= 0 && t[1] >= 0 && t[2] >= 0;  // an all-zero byte thresholds to b = 0 (-1)
+      for (int tile = rank; tile < ntile1; tile += ncta) {
+        const int ty = tile / t1x, tx = tile - ty * t1x, oy0 = ty * C1::TH, ox0 = tx * C1::TW;
+        // raw box: IR rows x RAW_W bytes from image row oy0 - R, byte ox0 C - XOFF (word loads; outside: 0)
+        for (int k = threadIdx.x; k < C1::IR * (C1::RAW_W / 4); k += blockDim.x) {
+          const int rr = k / (C1::RAW_W / 4), wd = k - rr * (C1::RAW_W / 4);
+          const int gy = oy0 - C1::R + rr, xb = ox0 * 3 - C1::XOFF + 4 * wd;
+          uint32_t v = 0u;
+          if (gy >= 0 && gy < A.H && xb >= 0 && xb + 4 <= rowb) v = __ldg(reinterpret_cast<const uint32_t*>(xi + (int64_t)gy * rowb + xb));
+          reinterpret_cast<uint32_t*>(box)[k] = v;
+        }
+        __syncthreads();
+        // strips: item = (strip row r, 4 pooled columns j)
+        if (threadIdx.x < C1::GROUPS) {
+          constexpr int IPR = C1::PW / C1::SPI;
+          const int r = threadIdx.x / IPR, j = threadIdx.x % IPR;
+          const uint8_t* src = box + r * C1::RAW_W + C1::WB + 6 * C1::SPI * j;
+          uint32_t M[C1::NWI];
+#pragma unroll
+          for (int w = 0; w < C1::NWI; ++w) M[w] = thresh_mask4(reinterpret_cast<const uint32_t*>(src)[w], Ev[(C1::C0 + w) % 3], Od[(C1::C0 + w) % 3]);
+          if (!zero_ok) {  // out-of-image bytes must be b = 0 whatever the threshold
+            const int gy = oy0 - C1::R + r;
+            const bool row_ok = gy >= 0 && gy < A.H;
+#pragma unroll
+            for (int w = 0; w < C1::NWI; ++w)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int xb = ox0 * 3 - C1::XOFF + C1::WB + 6 * C1::SPI * j + 4 * w + b;
+                if (!row_ok || xb < 0 || xb >= rowb) M[w] &= ~(0xFFu << (8 * b));
+              }
+          }
+          uint8_t* a = sA1 + r * C1::ROWP + C1::SPI * j * 16;
+#pragma unroll
+          for (int st = 0; st < C1::SPI; ++st) {
+            const int o = C1::E + 6 * st, qw = o >> 2, sh = 8 * (o & 3);
+            uint32_t m[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+              const int w = qw + k;
+              const uint32_t lo = w < C1::NWI ? M[w] : 0u, hi = w + 1 < C1::NWI ? M[w + 1] : 0u;
+              m[k] = (k < C1::NWS) ? (sh ? __funnelshift_r(lo, hi, sh) : lo) : 0u;
+            }
+            uint32_t v[4];
+            conv1_nibbles<C1::SB>(m, v);
+            *reinterpret_cast<uint4*>(a + st * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+          }
+        }
+        if (warp < 4 && img == 0 && tile == rank) {  // block scales (TMEM lane quarter = warp): 1.0, 1.0, 2^20
+          const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+          tc::tmem_st8_same(lb + 128, 0x7F7F7F7Fu);
+          tc::tmem_st8_same(lb + 136, 0x7F7F7F7Fu);
+          tc::tmem_st8_same(lb + 144, 0x93939393u);
+          tc::tmem_st_wait();
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        if (threadIdx.x == 0) {
+          if (img == 0 && tile == rank) tc::mbar_wait(&tc_wbar, 0);  // the weight images landed
+          constexpr uint32_t idesc = tc::idesc_mxf4(128, C1::N);
+          const uint64_t adc = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.c1c), 128 * 16, 128);
+          const uint64_t bdc = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.c1c) + C1::CONST_BYTES / 2, C1::N * 16, 128);
+          const uint64_t ad0 = tc::desc_kmajor(tc::smem_addr(sA1), C1::ROWP, 2 * C1::ROWP);
+          const uint64_t bd0 = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.c1b), C1::N * 16, 128);
+          tc::mma_mxf4(tmem, adc, bdc, idesc, tmem + 128, tmem + 144, 0u);  // D = C0
+#pragma unroll
+          for (int pp = 0; pp < C1::NMMA; ++pp)
+            tc::mma_mxf4(tmem, ad0 + (uint64_t)((pp * 2 * C1::ROWP) >> 4), bd0 + (uint64_t)((pp * 2 * C1::N * 16) >> 4), idesc,
+                         tmem + 128, tmem + 136, 1u);
+          tc::commit(&tc_mma);
+        }
+        if (warp < 4) {  // epilogue: pooled bit = max_q V_q >= 0 (k_conv1_fp4.cuh), thread = pooled pixel of the tile
+          tc::mbar_wait(&tc_mma, mma_ph);
+          __syncwarp();
+          tc::fence_after();
+          const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+          uint32_t a[16], b[16], c[16], d[16];
+          tc::tmem_ld16_p16(lb + 0 * 32, a);
+          tc::tmem_ld16_p16(lb + 1 * 32, b);
+          tc::tmem_ld16_p16(lb + 2 * 32, c);
+          tc::tmem_ld16_p16(lb + 3 * 32, d);
+          tc::tmem_ld_wait();
+          uint32_t neg = 0;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            uint32_t x;
+            asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(x) : "r"(a[jj]), "r"(b[jj]), "r"(c[jj]));
+            x = x & d[jj] & 0x80008000u;
+            neg = __umulhi(neg, 0x80000000u) + x;
+          }
+          const int m = warp * 32 + lane, py = (oy0 >> 1) + m / C1::PW, px = (ox0 >> 1) + m % C1::PW;
+          if (py < H1 && px < W1) {
+            const uint32_t word = ~neg, addr = tc::smem_addr(y1 + py * W1 + px);
+            for (int r = 0; r < ncta; ++r)
+              asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(tc::mapa(addr, (uint32_t)r)), "r"(word));
+          }
+          tc::fence_before();
+        }
+        mma_ph ^= 1u;
+        __syncthreads();  // (box, strips and the accumulator are reused by the next tile)
+      }
+    } else {
     // ---- phase 0: raw rows of this CTA's conv1 rows
     if (threadIdx.x == 0 && rhi > rlo && img > 0) stage_raw(img);
     if (rhi > rlo) tc::mbar_wait(&raw_bar, (uint32_t)(img & 1));
@@ -250,6 +388,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       // (no "memory" clobber: the next pixel's loads may move above the store; the cluster barrier orders it.
       // Writing the own copy first and broadcasting 16-byte pieces after the loop measured the same.)
       if (lane < ncta) asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(y1_c + 4 * u), "r"(word));
+    }
     }
     if (rank == 0) fused_trace(A, img, 6);  // (thread 0: its own warp's pixels done)
     cl.sync();
@@ -308,7 +447,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         }
         // epilogue (warps 0-3, thread = pooled pixel of the tile): pooled bit = NOT(all four acc'_q < 0)
         if (warp < 4) {
-          tc::mbar_wait(&tc_mma, (uint32_t)(img & 1));
+          tc::mbar_wait(&tc_mma, mma_ph);
           __syncwarp();
           tc::fence_after();
           const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
@@ -334,6 +473,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
           }
           tc::fence_before();  // (TMEM reads done before the next image's start values)
         }
+        mma_ph ^= 1u;
       }
     } else {
       constexpr int RR = (K2 - 1) / 2;
@@ -411,7 +551,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   if (rank == 0) fused_trace(A, 64, 2);
   cl.sync();  // no CTA exits while another may still address its shared memory
   if (rank == 0) fused_trace(A, 64, 3);
-  if constexpr (TC2) {
+  if constexpr (TC2 || TC1) {
     if (warp == 0) tc::tmem_dealloc<256>(tmem_s);
   }
 }

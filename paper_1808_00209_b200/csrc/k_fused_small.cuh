@@ -45,6 +45,7 @@ struct FusedSmallArgs {
   unsigned long long* trace;  // diagnostics build (bnn_set_trace, trace_layer 2): CTA 0's phase globaltimer stamps
   const uint8_t* w2img;       // conv2's pool-in-N e2m1 weight image (prep_tc4_pool_kernel) for the cluster kernel's
                               // tensor-core conv2 phase, or null
+  const uint8_t* w1img;       // conv1's e2m1 weight image (prep_conv1_fp4_kernel) for its tensor-core conv1 phase, or null
 };
 
 // phase timestamp (ns, %globaltimer) ev of image img into A.trace[img * 8 + ev] (diagnostics build only)
