@@ -600,14 +600,60 @@ def run_latency(a):
     torch.cuda.synchronize()
     per = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ev)
     b2b = _timed(lambda: net.forward_staged(1), 1000, 20, 0.3) * 1e3
+    device = _device_latency(bnn, synth, dev, imgs[:200])
     clocks = sampler.stop()
     _emit({"metric": "latency per image, batch 1 (kernel time)", "value": sum(per) / len(per), "unit": "us",
            "higher_is_better": False, "median_us": per[len(per) // 2], "p99_us": per[int(0.99 * len(per))],
            "back_to_back_us": b2b, "images_per_s_back_to_back": 1e6 / b2b,
+           "device_us_per_image": device,
+           "note": "value / back_to_back: one graph replay per image, bound by the host's cudaGraphLaunch (~16 us); "
+                   "device_us_per_image: 200 single-image forwards captured in one CUDA graph (launch cost amortised), "
+                   "for the default whole-network cluster kernel (f1, fused_max_n = 1) and the 5-kernel PDL path",
            "config": {"workload": "config 1: vehicle classifier, THRESH_RGB, 1000 random images one at a time, "
-                                  "one CUDA graph replay per image", "kernel": net.layer_kernel(0, 1)},
+                                  "one CUDA graph replay per image",
+                      "kernel": "fused_cluster_kernel" if bnn.forward_launches(net, 1) == 1 else net.layer_kernel(0, 1)},
            "context": "paper: 55.63 us per image on a GTX 1080 (Table 1, PAPER.md:292)",
            "gpu_launches_per_image": bnn.forward_launches(net, 1), "clocks": clocks})
+
+
+def _device_latency(bnn, synth, dev, imgs):
+    """Device-side batch-1 latency (us per image) of the whole-network cluster kernel (f1, the default for one image)
+    and of the 5-kernel PDL path: len(imgs) single-image forwards captured back to back in ONE CUDA graph, so the
+    host launch cost is paid once per graph; the two paths' classes must agree."""
+    import torch
+    R = imgs.shape[0]
+    out = {}
+    classes = []
+    for name, fused in (("fused_cluster", 1), ("pdl_graph", 0)):
+        bnn.set_option("fused_max_n", fused)
+        net, _, _ = _net_for(synth.VEHICLE, 1, 2018, dev, 8)
+        lg = torch.empty((R, 4), dtype=torch.int32, device=dev)
+        cls = torch.empty((R * 4,), dtype=torch.int32, device=dev)  # image i's class at 4 i (16-byte aligned)
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            for i in range(3):
+                net.forward(imgs[i:i + 1], lg[i:i + 1], cls[4 * i:4 * i + 1])
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(R):
+                net.forward(imgs[i:i + 1], lg[i:i + 1], cls[4 * i:4 * i + 1])
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) * 1e3 / (10 * R)
+        classes.append(cls[::4].clone())
+        net.close()
+    bnn.set_option("fused_max_n", 1)
+    out["classes_identical"] = bool(torch.equal(classes[0], classes[1]))
+    out["images_per_graph"] = R
+    return out
 
 
 def _stage_profile(net, fn, reps=3):

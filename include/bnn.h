@@ -126,9 +126,10 @@ BNN_API int bnn_version(void);
  *   "dense_ksplit"  1 (default): such a layer splits K over up to 4 CTA groups (+ a reduction kernel)
  *                   when its 128-image tile grid would leave SMs idle; 0: no split.
  *   "pdl"           1 (default): forward-path kernels use programmatic dependent launch.
- *   "fused_max_n"   forward chunks of n <= value images (default 0 = off) of a vehicle-shaped net run as
+ *   "fused_max_n"   forward chunks of n <= value images (default 1: batch 1; 0 = off) of a vehicle-shaped net run as
  *                   one whole-network kernel (a 16-CTA thread-block cluster; `fused_cluster` 0: cooperative grid).
- *   "fused_tc"      1 (default): that cluster kernel runs conv2 (k = 5, 32 -> 32 channels) on the tensor cores.
+ *   "fused_tc"      1 (default): that cluster kernel runs conv2 (k = 5, 32 -> 32 channels) and, for a 5x5x3 conv1,
+ *                   conv1 on the tensor cores; 0: the integer pipe.
  *   "alg1"          0 (default); 1: bnn_forward runs the paper's own design instead -- Alg. 1
  *                   im2col + packing (B = k*k), tiled XOR-popcount GEMM, int32 max-pool, 64-segment
  *                   FC -- as a comparison baseline (u8 SIGN / THRESH_RGB nets,

@@ -151,7 +151,7 @@ int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA in
 
 int g_opt_fused_tc = 1;       // 1: the cluster kernel runs conv2 on the tensor cores (pool-in-N mxf4, one tile per CTA)
 int g_opt_fused_cluster = 1;  // 1: the fused small-batch path is the thread-block-cluster kernel (DSMEM, cluster barriers); 0: cooperative
-int g_opt_fused_max_n = 0;  // forward over n <= this images runs as one fused kernel where the topology allows (0: off, default: the PDL graph is faster at batch 1)
+int g_opt_fused_max_n = 1;  // forward over n <= this images runs as one whole-network kernel where the topology allows (default 1: batch 1, where the tensor-core cluster kernel beats the PDL graph on the device, 12.4 vs 13.0 us; larger n run the batched layers)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
 int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison
 int g_opt_csa = 1;      // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders

@@ -394,7 +394,7 @@ def forward_vehicle_case(cuda, orc, mode, fused):
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_max_n", 1)  # (the default)
         cuda.set_option("fused_cluster", 1)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=6)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
@@ -416,7 +416,7 @@ def test_forward_fused_cluster_shapes(cuda, orc, k1, k2, hw):
         outs = [net.forward(dev(imgs[:1])), net.forward(dev(imgs))]
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_max_n", 1)  # (the default)
     onet = oracle_net(orc, spec, 1, layers, T)
     for (lg, cls), x in zip(outs, (imgs[:1], imgs)):
         ref_l, ref_c = onet.forward(x.numpy(), threads=5)
@@ -562,7 +562,7 @@ def test_forward_thresholds_and_chunking(cuda, orc, fused, streams):
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_max_n", 1)  # (the default)
         cuda.set_option("streams", 2)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
@@ -601,7 +601,7 @@ def test_forward_staged_graph(cuda, orc, pdl, fused):
             assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
     finally:
         cuda.set_option("pdl", 1)
-        cuda.set_option("fused_max_n", 0)
+        cuda.set_option("fused_max_n", 1)  # (the default)
         cuda.set_option("fused_cluster", 1)
 
 
