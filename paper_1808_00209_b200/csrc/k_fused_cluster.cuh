@@ -43,6 +43,7 @@ constexpr int kClusterMax = 16;
 struct FusedClusterLayout {
   int y1, y2, h1, h2, logit, raw, bim, f1w, f2w, f3w, tf, tcb, tca, tcl, c1b, c1c, c1a, c1r, total;  // word offsets
   int rp, raw_rows, m1, pb;  // pooled rows per CTA, staged raw rows, FC1 rows per CTA, bit-image row pitch (bytes)
+  int nbox;                  // conv1 raw boxes per CTA (tensor-core conv1)
   __host__ __device__ FusedClusterLayout(int H, int W, int C, int K1, int ncta, int l1, int l2, int l3) {
     auto up4 = [](int v) { return (v + 3) & ~3; };
     const int H1 = H / 2, W1 = W / 2, H2 = H1 / 2, W2 = W1 / 2;
@@ -71,7 +72,10 @@ struct FusedClusterLayout {
     c1c = c1b + (int)(Conv1Fp4Cfg<5>::B_BYTES / 4);
     c1a = c1c + (int)(Conv1Fp4Cfg<5>::CONST_BYTES / 4);
     c1r = c1a + (int)((Conv1Fp4Cfg<5>::A_BYTES / 4 + 31) & ~31u);
-    total = c1r + (int)(Conv1Fp4Cfg<5>::RAW_BYTES / 4) + 32;
+    // raw boxes of this CTA's conv1 tiles (ceil(tiles / ncta), prefetched one image ahead)
+    const int t1 = ((H1 + Conv1Fp4Cfg<5>::PH - 1) / Conv1Fp4Cfg<5>::PH) * ((W1 + Conv1Fp4Cfg<5>::PW - 1) / Conv1Fp4Cfg<5>::PW);
+    nbox = (t1 + ncta - 1) / ncta;
+    total = c1r + nbox * (int)(Conv1Fp4Cfg<5>::RAW_BYTES / 4) + 32;
   }
 };
 
@@ -119,6 +123,26 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   const int gy0 = 2 * py0 - R;                                 // image row of staged raw row 0
   const int rlo = max(0, gy0), rhi = min(A.H, 2 * py1 + K - 1 - R);  // staged image rows [rlo, rhi)
   const int rowb = A.W * C;
+  // tensor-core conv1: the raw boxes (IR rows x RAW_W bytes from image row oy0 - R, byte ox0 C - XOFF) of this
+  // CTA's tiles of image im, by 16-byte cp.async (zero fill outside the image; rows and boxes are 16-byte aligned)
+  auto prefetch_boxes = [&](int im) {
+    using C1 = Conv1Fp4Cfg<5>;
+    constexpr int CPR = C1::RAW_W / 16, CPB = C1::IR * CPR;  // 16-byte chunks per box row / box
+    const int t1x = (W1 + C1::PW - 1) / C1::PW, ntile1 = ((H1 + C1::PH - 1) / C1::PH) * t1x;
+    const uint8_t* xi = A.x + (int64_t)im * A.H * A.W * C;
+    uint8_t* boxes = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1r);
+    for (int k = threadIdx.x; k < Lo.nbox * CPB; k += blockDim.x) {
+      const int sel = k / CPB, kk = k - sel * CPB, tile = rank + sel * ncta;
+      if (tile >= ntile1) continue;
+      const int ty = tile / t1x, tx = tile - ty * t1x, rr = kk / CPR, ch = kk - rr * CPR;
+      const int gy = ty * C1::TH - C1::R + rr, xb = tx * C1::TW * 3 - C1::XOFF + 16 * ch;
+      const bool ok = gy >= 0 && gy < A.H && xb >= 0 && xb + 16 <= A.W * C;
+      const uint8_t* src = ok ? xi + (int64_t)gy * A.W * C + xb : A.x;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tc::smem_addr(boxes + sel * C1::RAW_BYTES + rr * C1::RAW_W + 16 * ch)),
+                   "l"(src), "r"(ok ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   auto stage_raw = [&](int img) {  // phase 0: the raw rows of this CTA's conv1 rows (one thread)
     const uint32_t bytes = (uint32_t)((rhi - rlo) * rowb);
     tc::mbar_arrive_expect_tx(&raw_bar, bytes);
@@ -146,6 +170,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     const uint32_t b1 = (uint32_t)n1 * dw1 * 4;  // dw1 % 4 == 0 (host check)
     tc::mbar_arrive_expect_tx(&w_bar, b1);
     if (b1) tc::stage_chunks(cl_smem + Lo.f1w, A.f1 + (int64_t)o1 * dw1, b1, &w_bar);
+  }
+  if constexpr (TC1) {
+    if (A.n > 0) prefetch_boxes(0);
   }
   if (rank == 0) {
     for (int j = threadIdx.x; j < A.l2 * dw2; j += blockDim.x)
@@ -236,9 +263,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
       tc::fence_after();
       const uint32_t tmem = tmem_s;
       const int t1x = (W1 + C1::PW - 1) / C1::PW, ntile1 = ((H1 + C1::PH - 1) / C1::PH) * t1x;
-      uint8_t* box = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1r);
       uint8_t* sA1 = reinterpret_cast<uint8_t*>(cl_smem + Lo.c1a);
-      const uint8_t* xi = A.x + (int64_t)img * A.H * rowb;
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this image's raw boxes (prefetched)
+      __syncthreads();
       // builder constants (k_conv1_fp4.cuh, kBinRgb): per-channel 16-bit-lane threshold terms
       uint32_t Ev[3], Od[3];
 #pragma unroll
@@ -247,17 +274,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         Od[m] = (uint32_t)(0x7FFF - t[(m + 1) % 3]) | ((uint32_t)(0x7FFF - t[m]) << 16);
       }
       const bool zero_ok = t[0] >= 0 && t[1] >= 0 && t[2] >= 0;  // an all-zero byte thresholds to b = 0 (-1)
-      for (int tile = rank; tile < ntile1; tile += ncta) {
+      for (int tile = rank, sel = 0; tile < ntile1; tile += ncta, ++sel) {
         const int ty = tile / t1x, tx = tile - ty * t1x, oy0 = ty * C1::TH, ox0 = tx * C1::TW;
-        // raw box: IR rows x RAW_W bytes from image row oy0 - R, byte ox0 C - XOFF (word loads; outside: 0)
-        for (int k = threadIdx.x; k < C1::IR * (C1::RAW_W / 4); k += blockDim.x) {
-          const int rr = k / (C1::RAW_W / 4), wd = k - rr * (C1::RAW_W / 4);
-          const int gy = oy0 - C1::R + rr, xb = ox0 * 3 - C1::XOFF + 4 * wd;
-          uint32_t v = 0u;
-          if (gy >= 0 && gy < A.H && xb >= 0 && xb + 4 <= rowb) v = __ldg(reinterpret_cast<const uint32_t*>(xi + (int64_t)gy * rowb + xb));
-          reinterpret_cast<uint32_t*>(box)[k] = v;
-        }
-        __syncthreads();
+        const uint8_t* box = reinterpret_cast<const uint8_t*>(cl_smem + Lo.c1r) + sel * C1::RAW_BYTES;
         // strips: item = (strip row r, 4 pooled columns j)
         if (threadIdx.x < C1::GROUPS) {
           constexpr int IPR = C1::PW / C1::SPI;
@@ -346,8 +365,9 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
           tc::fence_before();
         }
         mma_ph ^= 1u;
-        __syncthreads();  // (box, strips and the accumulator are reused by the next tile)
+        __syncthreads();  // (strips and the accumulator are reused by the next tile)
       }
+      if (img + 1 < A.n) prefetch_boxes(img + 1);  // lands during conv2 / FC
     } else {
     // ---- phase 0: raw rows of this CTA's conv1 rows
     if (threadIdx.x == 0 && rhi > rlo && img > 0) stage_raw(img);
