@@ -110,8 +110,8 @@ def conv_case(cuda, orc, n, h, w, cin, cout, k, pool, thr=False, flip=False, see
 ])
 @pytest.mark.parametrize("tc", [1, 0])
 def test_conv_binary(cuda, orc, n, h, w, cin, cout, k, pool, tc):
-    """tc = 1: layers with c_in >= 32 run on the tensor cores (tcgen05 kind::i8) where an
-    instantiation exists; tc = 0: everything on the XOR-popcount integer path."""
+    """tc = 1: layers with c_in >= 32 run on the tensor cores (tcgen05 kind::mxf4 by default, kind::i8 with
+    conv_tc_fp4 = 0) where an instantiation exists; tc = 0: everything on the XOR-popcount integer path."""
     try:
         cuda.set_option("conv_tc", tc)
         conv_case(cuda, orc, n, h, w, cin, cout, k, pool, seed=h + cin + k)
