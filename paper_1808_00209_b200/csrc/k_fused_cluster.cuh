@@ -190,10 +190,13 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   const bool fl2 = A.flip2 != nullptr && A.flip2[lane] != 0;
   // conv1: patch bit b = 32 w + lane <-> (ky, kx, c), b = (ky K + kx) C + c (MSB-first)
   const int nb = K * K * C, S1 = nb;
-  int t[4] = {0, 0, 0, 0};
+  // Small parameters are loaded into registers here and consumed (or stored to shared memory) at their first use,
+  // so no load -> use stall sits in the prologue of this latency-critical kernel.
+  float Tf[4] = {0.f, 0.f, 0.f, 0.f};  // input thresholds: t[c] = u8_threshold(-T[c]) at the image's conv1 phase
 #pragma unroll
   for (int c = 0; c < 4; ++c)
-    if (c < C) t[c] = A.T != nullptr ? u8_threshold(-A.T[c]) : 0;
+    if (c < C && A.T != nullptr) Tf[c] = A.T[c];
+  int t[4] = {0, 0, 0, 0};
   int off_[3];  // patch bit 32 w + lane: byte offset in the bit image from the window's top-left corner
   bool use_[3];
   uint32_t wreg[3];
@@ -207,15 +210,33 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   }
   const int th1 = A.thr1 != nullptr ? A.thr1[lane] : 0;
   const bool fl1 = A.flip1 != nullptr && A.flip1[lane] != 0;
-  for (int j = threadIdx.x; j < n1; j += blockDim.x) {  // read per output by one lane in phase 3 / 4: staged once
-    s_t1[j] = A.thr_f1 != nullptr ? A.thr_f1[o1 + j] : 0;
-    s_f1[j] = A.flip_f1 != nullptr ? A.flip_f1[o1 + j] : 0;
-  }
-  if (rank == 0)
-    for (int j = threadIdx.x; j < A.l2; j += blockDim.x) {
-      s_t2[j] = A.thr_f2 != nullptr ? A.thr_f2[j] : 0;
-      s_f2[j] = A.flip_f2 != nullptr ? A.flip_f2[j] : 0;
+  // FC1 / FC2 thresholds and flips (thread j < n1, CTA 0's threads j, j + 512 < l2 <= 1024): stored to shared memory
+  // after image 0's conv1 phase (read per output by one lane in phases 3 / 4)
+  const int pt1 = (threadIdx.x < n1 && A.thr_f1 != nullptr) ? A.thr_f1[o1 + threadIdx.x] : 0;
+  const int pf1 = (threadIdx.x < n1 && A.flip_f1 != nullptr) ? A.flip_f1[o1 + threadIdx.x] : 0;
+  int pt2[2] = {0, 0}, pf2[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = threadIdx.x + h * (int)blockDim.x;
+    if (rank == 0 && j < A.l2) {
+      pt2[h] = A.thr_f2 != nullptr ? A.thr_f2[j] : 0;
+      pf2[h] = A.flip_f2 != nullptr ? A.flip_f2[j] : 0;
     }
+  }
+  auto store_fc_params = [&]() {
+    if (threadIdx.x < n1) {
+      s_t1[threadIdx.x] = pt1;
+      s_f1[threadIdx.x] = pf1;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = threadIdx.x + h * (int)blockDim.x;
+      if (rank == 0 && j < A.l2) {
+        s_t2[j] = pt2[h];
+        s_f2[j] = pf2[h];
+      }
+    }
+  };
   for (int j = threadIdx.x; j < kFusedMaxL / 32; j += blockDim.x) h1[j] = 0u;
   using TP = ConvTc4PoolCfg<5>;
   const int tiles2_x = (W1 + TP::TW - 1) / TP::TW, tiles2 = ((H1 + TP::TH - 1) / TP::TH) * tiles2_x;
@@ -241,15 +262,19 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
 #pragma unroll
       for (int c = 0; c < TP::LUTC; ++c) s_lut2[TP::LUTC * threadIdx.x + c] = v;
     }
-    if (threadIdx.x < 32) {  // (as conv_tc4_pool_kernel: 32 valid channels)
-      const int o = tc4_col_channel(threadIdx.x), S_TOT = 25 * 32;
-      const bool f = A.flip2 != nullptr && A.flip2[o] != 0;
-      int tt = A.thr2 != nullptr ? A.thr2[o] : 0;
-      tt = max(-S_TOT - 1, min(S_TOT, tt));
-      if (f) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
+  }
+  // conv2 start values C0 - (thr' + 1) per TMEM column (as conv_tc4_pool_kernel: 32 valid channels): loaded here,
+  // stored with the FC parameters
+  const int pt_c2 = (TC2 && threadIdx.x < 32 && A.thr2 != nullptr) ? A.thr2[tc4_col_channel(threadIdx.x)] : 0;
+  const int pf_c2 = (TC2 && threadIdx.x < 32 && A.flip2 != nullptr) ? A.flip2[tc4_col_channel(threadIdx.x)] : 0;
+  auto store_c2_init = [&]() {
+    if (TC2 && threadIdx.x < 32) {
+      constexpr int S_TOT = 25 * 32;
+      int tt = max(-S_TOT - 1, min(S_TOT, pt_c2));
+      if (pf_c2 != 0) tt = max(-S_TOT - 1, min(S_TOT, -tt - 1));
       s_init2[threadIdx.x] = 12582912.0f - (float)(tt + 1);
     }
-  }
+  };
   if (rank == 0) fused_trace(A, 64, 1);
   // every CTA of the cluster is running and has zeroed h1 (the first DSMEM atomics into it follow two phase
   // barriers later); the barrier's wait side synchronises the CTA (mbarrier initialisation, staged values)
@@ -258,6 +283,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   uint32_t mma_ph = 0;  // parity of the next tc_mma completion (conv1 tiles, then the conv2 tile, per image)
   for (int img = 0; img < A.n; ++img) {
     if (rank == 0) fused_trace(A, img, 0);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) t[c] = (c < C && A.T != nullptr) ? u8_threshold(-Tf[c]) : 0;
     if constexpr (TC1) {
       using C1 = Conv1Fp4Cfg<5>;
       tc::fence_after();
@@ -411,6 +438,10 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     }
     }
     if (rank == 0) fused_trace(A, img, 6);  // (thread 0: its own warp's pixels done)
+    if (img == 0) {  // (the phase barrier below publishes them)
+      store_fc_params();
+      store_c2_init();
+    }
     cl.sync();
     if (rank == 0) fused_trace(A, img, 1);
     // ---- phase 2: conv2 + pool from the local y1 -> every CTA's y2
