@@ -922,7 +922,8 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     }
     auto launch = [&](auto kfn, uint32_t smem) {
       ensure_smem(kfn, smem);
-      dim3 grid((unsigned)std::min(ntiles, num_sms()), (unsigned)groups, (unsigned)A.ks);
+      const int cps = wide ? DenseTc4Cfg<256>::CPS : DenseTc4Cfg<128>::CPS;
+      dim3 grid((unsigned)std::min(ntiles, num_sms() * cps), (unsigned)groups, (unsigned)A.ks);
       launch_pdl(kfn, grid, dim3(256), smem, s, A, xmap);
     };
     if (wide) {

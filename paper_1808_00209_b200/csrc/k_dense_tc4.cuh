@@ -16,13 +16,23 @@ namespace bnn {
 
 template <int NT>
 struct DenseTc4Cfg {
-  static constexpr int KC = 16;                         // words per stage (8 MMAs)
+#ifndef BNN_DENSE_KC
+#define BNN_DENSE_KC 8
+#endif
+  // words per stage (KC / 2 MMAs).  NT <= 128: 8-word stages keep a CTA at ~89 KB of shared memory so TWO CTAs run
+  // per SM and one's per-stage block barrier overlaps the other's expansion / MMAs (ncu: 27% of FC1's warp samples
+  // waited at that barrier with one CTA per SM): FC1 0.248 -> 0.207 ms per 65536 images (tools/gpu_fc1_ab.sh)
+  static constexpr int KC = NT > 128 ? 16 : BNN_DENSE_KC;
 #ifndef BNN_DENSE_NBR
-#define BNN_DENSE_NBR 3
+#define BNN_DENSE_NBR 2
 #endif
   // weight-image ring: stage use u + NBR - 2 is bulk-copied while use u is expanded (its slot was read by MMA(u - 2));
   // with 2 slots every stage's 32 KB copy was issued only when its own expansion began
   static constexpr int NBR = NT > 128 ? 2 : BNN_DENSE_NBR;
+#ifndef BNN_DENSE_CPS
+#define BNN_DENSE_CPS 2
+#endif
+  static constexpr int CPS = NT > 128 ? 1 : BNN_DENSE_CPS;  // CTAs per SM the kernel is built for
   static constexpr uint32_t A_BYTES = KC * 128 * 16;    // 32 KB
   static constexpr uint32_t B_BYTES = KC * NT * 16;
   static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
@@ -74,7 +84,7 @@ __global__ void __launch_bounds__(256) prep_dense_tc4_kernel(const DenseArgs A, 
 // ring, issued RING stages ahead, instead of one-stage-ahead register prefetches (whose L2 latency
 // every stage waited for).
 template <int NT, bool TMAX = false>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, DenseTc4Cfg<NT>::CPS)
 dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
   griddep_launch();
   using C = DenseTc4Cfg<NT>;
