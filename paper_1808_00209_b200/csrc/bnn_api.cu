@@ -911,10 +911,11 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     CUtensorMap xmap;
     std::memset(&xmap, 0, sizeof(xmap));
     bool tmax = g_opt_dense_tma && aligned16(x) && tma_encoder() != nullptr;
+    const bool two = !wide && ntiles >= 2 * num_sms();  // two CTAs per SM (DenseTc4Cfg<128, true>) for large batches
     if (tmax) {
       const cuuint64_t dims[2] = {(cuuint64_t)A.dw, (cuuint64_t)n};
       const cuuint64_t strides[1] = {(cuuint64_t)A.dw * 4};
-      const cuuint32_t box[2] = {(cuuint32_t)(wide ? DenseTc4Cfg<256>::KC : DenseTc4Cfg<128>::KC), 128};
+      const cuuint32_t box[2] = {(cuuint32_t)(wide ? DenseTc4Cfg<256>::KC : (two ? DenseTc4Cfg<128, true>::KC : DenseTc4Cfg<128>::KC)), 128};
       const cuuint32_t estr[2] = {1, 1};
       tmax = tma_encoder()(&xmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(x), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -922,7 +923,7 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
     }
     auto launch = [&](auto kfn, uint32_t smem) {
       ensure_smem(kfn, smem);
-      const int cps = wide ? DenseTc4Cfg<256>::CPS : DenseTc4Cfg<128>::CPS;
+      const int cps = (!wide && two) ? DenseTc4Cfg<128, true>::CPS : 1;
       dim3 grid((unsigned)std::min(ntiles, num_sms() * cps), (unsigned)groups, (unsigned)A.ks);
       launch_pdl(kfn, grid, dim3(256), smem, s, A, xmap);
     };
@@ -930,8 +931,13 @@ bnn_status launch_dense(const uint32_t* x, int n, int64_t d, const uint32_t* wt,
       if (tmax) launch(dense_tc4_kernel<256, true>, DenseTc4Cfg<256>::SMEM_TMAX);
       else launch(dense_tc4_kernel<256>, DenseTc4Cfg<256>::SMEM);
     } else {
-      if (tmax) launch(dense_tc4_kernel<128, true>, DenseTc4Cfg<128>::SMEM_TMAX);
-      else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM);
+      if (two) {
+        if (tmax) launch(dense_tc4_kernel<128, true, true>, DenseTc4Cfg<128, true>::SMEM_TMAX);
+        else launch(dense_tc4_kernel<128, false, true>, DenseTc4Cfg<128, true>::SMEM);
+      } else {
+        if (tmax) launch(dense_tc4_kernel<128, true>, DenseTc4Cfg<128>::SMEM_TMAX);
+        else launch(dense_tc4_kernel<128>, DenseTc4Cfg<128>::SMEM);
+      }
     }
     st = check_launch("dense_tc4_kernel");
     if (st == BNN_OK && A.ks > 1) {

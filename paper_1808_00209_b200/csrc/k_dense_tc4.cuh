@@ -14,25 +14,17 @@
 
 namespace bnn {
 
-template <int NT>
+// TWO (NT <= 128, large batches): 8-word stages keep a CTA at ~89 KB of shared memory so TWO CTAs run per SM and one's
+// per-stage block barrier overlaps the other's expansion / MMAs (ncu: 27% of FC1's warp samples waited at that
+// barrier with one CTA per SM): FC1 0.248 -> 0.207 ms per 65536 images; with fewer tiles than 2 x SMs (config 2's
+// 4096 images) the 16-word, one-CTA-per-SM form is faster (0.033 vs 0.039 ms).  The per-net weight image is laid out
+// word by word ([word][NT][16 B]), so both forms read the same image.
+template <int NT, bool TWO = false>
 struct DenseTc4Cfg {
-#ifndef BNN_DENSE_KC
-#define BNN_DENSE_KC 8
-#endif
-  // words per stage (KC / 2 MMAs).  NT <= 128: 8-word stages keep a CTA at ~89 KB of shared memory so TWO CTAs run
-  // per SM and one's per-stage block barrier overlaps the other's expansion / MMAs (ncu: 27% of FC1's warp samples
-  // waited at that barrier with one CTA per SM): FC1 0.248 -> 0.207 ms per 65536 images (tools/gpu_fc1_ab.sh)
-  static constexpr int KC = NT > 128 ? 16 : BNN_DENSE_KC;
-#ifndef BNN_DENSE_NBR
-#define BNN_DENSE_NBR 2
-#endif
-  // weight-image ring: stage use u + NBR - 2 is bulk-copied while use u is expanded (its slot was read by MMA(u - 2));
-  // with 2 slots every stage's 32 KB copy was issued only when its own expansion began
-  static constexpr int NBR = NT > 128 ? 2 : BNN_DENSE_NBR;
-#ifndef BNN_DENSE_CPS
-#define BNN_DENSE_CPS 2
-#endif
-  static constexpr int CPS = NT > 128 ? 1 : BNN_DENSE_CPS;  // CTAs per SM the kernel is built for
+  static constexpr int KC = TWO ? 8 : 16;  // words per stage (KC / 2 MMAs)
+  // weight-image ring: stage use u + NBR - 2 is bulk-copied while use u is expanded (its slot was read by MMA(u - 2))
+  static constexpr int NBR = (TWO || NT > 128) ? 2 : 3;
+  static constexpr int CPS = TWO ? 2 : 1;  // CTAs per SM the kernel is built for
   static constexpr uint32_t A_BYTES = KC * 128 * 16;    // 32 KB
   static constexpr uint32_t B_BYTES = KC * NT * 16;
   static constexpr uint32_t TMEM_COLS = (NT + 16 <= 64) ? 64 : ((NT + 16 <= 128) ? 128 : ((NT + 16 <= 256) ? 256 : 512));
@@ -83,11 +75,11 @@ __global__ void __launch_bounds__(256) prep_dense_tc4_kernel(const DenseArgs A, 
 // TMAX: the activation stages arrive by TMA (2-D box of KC words x 128 images) in a RING-deep shared
 // ring, issued RING stages ahead, instead of one-stage-ahead register prefetches (whose L2 latency
 // every stage waited for).
-template <int NT, bool TMAX = false>
-__global__ void __launch_bounds__(256, DenseTc4Cfg<NT>::CPS)
+template <int NT, bool TMAX = false, bool TWO = false>
+__global__ void __launch_bounds__(256, DenseTc4Cfg<NT, TWO>::CPS)
 dense_tc4_kernel(const DenseArgs A, const __grid_constant__ CUtensorMap xmap) {
   griddep_launch();
-  using C = DenseTc4Cfg<NT>;
+  using C = DenseTc4Cfg<NT, TWO>;
   constexpr int KC = C::KC;
   extern __shared__ __align__(1024) uint8_t dsm[];
   uint8_t* sA = dsm;                                  // 2 x [kw][128][16]
