@@ -121,3 +121,26 @@ def test_dense_operating_point_sampled(cuda, orc):
         ra = orc.dense(xv, W)
         assert np.array_equal(acc_np[i], ra.astype(np.int32)), "acc mismatch image %d" % i
         assert np.array_equal(yw[i], orc.pack(orc.binarize(ra[None])[0])), "bits mismatch image %d" % i
+
+
+def test_forward_bench_chunk(cuda, orc):
+    """The vehicle net at bench.py's default chunk (65536 images: FC1 in the two-CTAs-per-SM form,
+    512 conv tiles per CTA pair wave) with a ragged second chunk on the other stream: sampled images
+    against the oracle, and every image against a 16384-image-chunk run of the same net (the one-CTA
+    FC1 form, other tile assignment)."""
+    big, n = 65536, 65536 + 1000
+    imgs = synth.images_chunked(0, n, 96, 96, 3, 7301, device="cuda")
+    net, layers, T = build_net(cuda, synth.VEHICLE, 1, 7302, max_batch=big)
+    logits, cls = net.forward(imgs)
+    torch.cuda.synchronize()
+    idx = _sample_idx(n, big, 8, 7303)
+    ref_l, ref_c = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs[idx].cpu().numpy(), threads=8)
+    got_l, got_c = logits[idx].cpu().numpy(), cls[idx].cpu().numpy()
+    bad = [i for j, i in enumerate(idx) if not (np.array_equal(got_l[j], ref_l[j]) and got_c[j] == ref_c[j])]
+    assert not bad, "images differing from the oracle: %s" % bad
+    net2, _, _ = build_net(cuda, synth.VEHICLE, 1, 7302, max_batch=CHUNK)
+    l2, c2 = net2.forward(imgs)
+    torch.cuda.synchronize()
+    assert torch.equal(l2, logits) and torch.equal(c2, cls)
+    net.close()
+    net2.close()

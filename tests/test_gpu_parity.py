@@ -797,3 +797,32 @@ def test_forward_staged_graph_modes(cuda, orc, mode):
         ref_l, ref_c = onet.forward(imgs.numpy(), threads=n)
         assert np.array_equal(st_lg[:n].cpu().numpy(), ref_l)
         assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
+
+
+@pytest.mark.parametrize("n,d,l,flip", [(40000, 4096, 100, True), (37889, 2040, 10, False)])
+@pytest.mark.parametrize("tma", [1, 0])
+def test_dense_tensor_core_two_cta_form(cuda, orc, n, d, l, flip, tma):
+    """Batches with at least 2 x 148 image tiles run dense_tc4_kernel's two-CTAs-per-SM form (8-word
+    stages, 2-slot weight ring; bnn_api.cu `two`): ragged last tile (37889 = 296 tiles + 1 image),
+    a partial last word (d = 2040), thresholds + flips, fused argmax; sampled images against
+    orc_dense including the first and last image of the batch."""
+    xs = synth.pm1((n, d), 195 + d)
+    ws = synth.pm1((l, d), 196 + l)
+    t = synth.int_thresholds(l, 197, -40, 41)
+    f = synth.flips(l, 198) if flip else None
+    xp = cuda.pack(dev(xs).view(n, 1, 1, d)).view(n, -1)
+    try:
+        cuda.set_option("dense_tma", tma)
+        y, acc, cls = cuda.dense(xp, d, cuda.pack_weights(dev(ws)), l, dev(t), None if f is None else dev(f),
+                                 want_acc=True, want_cls=True)
+        torch.cuda.synchronize()
+    finally:
+        cuda.set_option("dense_tma", 1)
+    acc, y, cls = acc.cpu().numpy(), u32(y), cls.cpu().numpy()
+    W = ws.numpy()
+    for i in sorted(set(list(range(0, n, 997)) + [127, 128, n - 2, n - 1])):
+        ra = orc.dense(xs[i].numpy(), W)
+        assert np.array_equal(acc[i], ra), "acc mismatch image %d" % i
+        b = orc.binarize(ra[None], t.numpy(), None if f is None else f.numpy())[0]
+        assert np.array_equal(y[i], orc.pack(b, 32)), "bits mismatch image %d" % i
+        assert cls[i] == orc.argmax(ra), "argmax mismatch image %d" % i
