@@ -128,7 +128,7 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
 
 int g_opt_conv_algo = 0;      // 0 auto, 1 force the generic one-word-per-tap conv
 int g_opt_tiles_per_cta = 0;  // 0 auto, else a fixed number of tiles per CTA
-int g_opt_gemv_max_n = 16;    // dense layers with n <= this use the GEMV kernel
+int g_opt_gemv_max_n = 255;   // dense layers with n <= this use the GEMV kernel (every n below the tensor path's 256: dense_kernel's 64-image CTAs leave the SMs idle there, FC1 ~0.2 ms at 17-255 images vs 0.005-0.03 ms)
 int g_opt_conv_tc = 1;        // 1: binary convs with c_in >= 32 run on tcgen05 (kind::i8) where supported
 int g_opt_first_pool_tc = 1;  // 1: pooled first layers use the pool-window-ordered tensor-core kernel
 int g_opt_conv_tc_fp4 = 1;    // 1: tensor-core binary convs use packed e2m1 (kind::mxf4), 0: int8 (kind::i8)
@@ -150,8 +150,9 @@ int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
 
 int g_opt_fused_tc = 1;       // 1: the cluster kernel runs conv2 on the tensor cores (pool-in-N mxf4, one tile per CTA)
+int g_opt_fused_multi = 1;    // 1: fused_cluster_kernel runs one cluster per image of a small batch; 0: one cluster
 int g_opt_fused_cluster = 1;  // 1: the fused small-batch path is the thread-block-cluster kernel (DSMEM, cluster barriers); 0: cooperative
-int g_opt_fused_max_n = 1;  // forward over n <= this images runs as one whole-network kernel where the topology allows (default 1: batch 1, where the tensor-core cluster kernel beats the PDL graph on the device, 12.4 vs 13.0 us; larger n run the batched layers)
+int g_opt_fused_max_n = 7;  // forward over n <= this images runs as one whole-network kernel where the topology allows (default 7: one 16-CTA cluster per image, 7 clusters fit at once: 11.3-11.7 us on the device for 1-7 images vs 13.0-15.7 us for the PDL layers; 8 images: 18.4 vs 16.0 us, so larger n run the batched layers)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
 int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison
 int g_opt_csa = 1;      // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
@@ -1020,6 +1021,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "dense_tma") == 0) { g_opt_dense_tma = value; return BNN_OK; }
   if (strcmp(key, "luma_fused") == 0) { g_opt_luma_fused = value; return BNN_OK; }
   if (strcmp(key, "fused_cluster") == 0) { g_opt_fused_cluster = value; return BNN_OK; }
+  if (strcmp(key, "fused_multi") == 0) { g_opt_fused_multi = value ? 1 : 0; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
 
@@ -1314,7 +1316,8 @@ bnn_status launch_fused_small(bnn_net* net, const void* images, int nb, int32_t*
 }
 
 // Cluster size of fused_cluster_kernel on the current device: 16 (non-portable) if the device runs a
-// 16-CTA cluster of it, else 8; 0 if neither (then the cooperative kernel serves)
+// 16-CTA cluster of it, else 8; 0 if neither (then the cooperative kernel serves).  Returned as
+// size + 256 x (clusters of that size the device holds at once)
 template <typename F>
 int fused_cluster_size(F kfn, size_t smem) {
   return dev_cached(reinterpret_cast<const char*>(kfn) + 2, [&] {
@@ -1335,7 +1338,7 @@ int fused_cluster_size(F kfn, size_t smem) {
       int nclusters = 0;
       if (cudaOccupancyMaxActiveClusters(&nclusters, kfn, &cfg) == cudaSuccess && nclusters >= 1) {
         (void)cudaGetLastError();
-        return cs;
+        return cs + 256 * nclusters;
       }
       (void)cudaGetLastError();
     }
@@ -1360,10 +1363,13 @@ bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_
   const size_t smem = (size_t)FusedClusterLayout(net->h, net->w, net->c, a.k, 8, d1.l, d2.l, d3.l).total * 4;
   if (smem > 200 * 1024) return BNN_OK;
   auto go = [&](auto kfn) -> bnn_status {
-    const int cs = fused_cluster_size(kfn, smem);
+    const int cv = fused_cluster_size(kfn, smem), cs = cv & 255;
     if (cs == 0) return BNN_OK;
+    // one cluster per image up to what the device holds at once (images are independent; a cluster
+    // serves images cid, cid + ncl, ... when the batch is larger)
+    const int ncl = std::max(1, std::min(nb, (cv >> 8) * g_opt_fused_multi + (1 - g_opt_fused_multi)));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)cs);
+    cfg.gridDim = dim3((unsigned)(cs * ncl));
     cfg.blockDim = dim3(kFusedWarps * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;

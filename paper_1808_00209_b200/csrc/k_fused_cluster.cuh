@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   __shared__ uint32_t tmem_s;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), ncta = (int)cl.num_blocks();
+  // several clusters (1-D grid of whole clusters): cluster cid serves images cid, cid + ncl, ... (no shared state)
+  const int cid = (int)(blockIdx.x / (unsigned)ncta), ncl = (int)(gridDim.x / (unsigned)ncta);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = rank * kFusedWarps + warp, nw = ncta * kFusedWarps;
   const int H1 = A.H >> 1, W1 = A.W >> 1, H2 = H1 >> 1, W2 = W1 >> 1;
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     tc::mbar_init(&w_bar, 1);
     tc::mbar_init(&raw_bar, 1);
     tc::fence_mbar_init();
-    if (!TC1 && A.n > 0 && rhi > rlo) stage_raw(0);
+    if (!TC1 && cid < A.n && rhi > rlo) stage_raw(cid);
     if constexpr (TC2 || TC1) {
       tc::mbar_init(&tc_wbar, 1);
       tc::mbar_init(&tc_mma, 1);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     if (b1) tc::stage_chunks(cl_smem + Lo.f1w, A.f1 + (int64_t)o1 * dw1, b1, &w_bar);
   }
   if constexpr (TC1) {
-    if (A.n > 0) prefetch_boxes(0);
+    if (cid < A.n) prefetch_boxes(cid);
   }
   if (rank == 0) {
     for (int j = threadIdx.x; j < A.l2 * dw2; j += blockDim.x)
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 
   uint32_t mma_ph = 0;  // parity of the next tc_mma completion (conv1 tiles, then the conv2 tile, per image)
-  for (int img = 0; img < A.n; ++img) {
+  for (int img = cid, it = 0; img < A.n; img += ncl, ++it) {  // it: this cluster's image count (phases, first use)
     if (rank == 0) fused_trace(A, img, 0);
 #pragma unroll
     for (int c = 0; c < 4; ++c) t[c] = (c < C && A.T != nullptr) ? u8_threshold(-Tf[c]) : 0;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
             *reinterpret_cast<uint4*>(a + st * 16) = make_uint4(v[0], v[1], v[2], v[3]);
           }
         }
-        if (warp < 4 && img == 0 && tile == rank) {  // block scales (TMEM lane quarter = warp): 1.0, 1.0, 2^20
+        if (warp < 4 && it == 0 && tile == rank) {  // block scales (TMEM lane quarter = warp): 1.0, 1.0, 2^20
           const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
           tc::tmem_st8_same(lb + 128, 0x7F7F7F7Fu);
           tc::tmem_st8_same(lb + 136, 0x7F7F7F7Fu);
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         __syncthreads();
         tc::fence_after();
         if (threadIdx.x == 0) {
-          if (img == 0 && tile == rank) tc::mbar_wait(&tc_wbar, 0);  // the weight images landed
+          if (it == 0 && tile == rank) tc::mbar_wait(&tc_wbar, 0);  // the weight images landed
           constexpr uint32_t idesc = tc::idesc_mxf4(128, C1::N);
           const uint64_t adc = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.c1c), 128 * 16, 128);
           const uint64_t bdc = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.c1c) + C1::CONST_BYTES / 2, C1::N * 16, 128);
@@ -394,11 +396,11 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         mma_ph ^= 1u;
         __syncthreads();  // (strips and the accumulator are reused by the next tile)
       }
-      if (img + 1 < A.n) prefetch_boxes(img + 1);  // lands during conv2 / FC
+      if (img + ncl < A.n) prefetch_boxes(img + ncl);  // lands during conv2 / FC
     } else {
     // ---- phase 0: raw rows of this CTA's conv1 rows
-    if (threadIdx.x == 0 && rhi > rlo && img > 0) stage_raw(img);
-    if (rhi > rlo) tc::mbar_wait(&raw_bar, (uint32_t)(img & 1));
+    if (threadIdx.x == 0 && rhi > rlo && it > 0) stage_raw(img);
+    if (rhi > rlo) tc::mbar_wait(&raw_bar, (uint32_t)(it & 1));
     if (rank == 0) fused_trace(A, img, 5);
     // ---- phase 1a: the 0/1 byte image of the staged rows (zero outside the image: the -1 padding, R4)
     for (int r = warp; r < Lo.raw_rows; r += kFusedWarps) {  // warp = row, lane = bit-image column (pixel)
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     }
     }
     if (rank == 0) fused_trace(A, img, 6);  // (thread 0: its own warp's pixels done)
-    if (img == 0) {  // (the phase barrier below publishes them)
+    if (it == 0) {  // (the phase barrier below publishes them)
       store_fc_params();
       store_c2_init();
     }
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
 #pragma unroll
             for (int q = 0; q < 4; ++q) tmem_st16(lb + (uint32_t)(q * 32 + cb), iv);
           }
-          if (img == 0) {
+          if (it == 0) {
             tc::tmem_st8_same(lb + 128, 0x7F7F7F7Fu);
             tc::tmem_st8_same(lb + 136, 0x7F7F7F7Fu);
           }
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
         __syncthreads();
         tc::fence_after();
         if (threadIdx.x == 0) {
-          if (img == 0) tc::mbar_wait(&tc_wbar, 0);  // the weight image landed
+          if (it == 0) tc::mbar_wait(&tc_wbar, 0);  // the weight image landed
           constexpr uint32_t idesc = tc::idesc_mxf4(128, 128);
           const uint64_t adesc0 = tc::desc_kmajor(tc::smem_addr(sA2), TP::ROWB, 2 * TP::ROWB);
           const uint64_t bdesc0 = tc::desc_kmajor(tc::smem_addr(cl_smem + Lo.tcb), 128 * 16, 128);
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     cl.sync();
     if (rank == 0) fused_trace(A, img, 2);
     // ---- phase 3: FC1 outputs [o1, o1 + n1) from the local y2 (weights in shared memory), bits into CTA 0's h1
-    if (img == 0) tc::mbar_wait(&w_bar, 0);
+    if (it == 0) tc::mbar_wait(&w_bar, 0);
     {
       const int64_t d1 = (int64_t)dw1 * 32;
       for (int k = warp; k < n1; k += kFusedWarps) {
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kFusedWarps * 32, 1) fused_cluster_kernel(cons
     if (rank == 0) fused_trace(A, img, 3);
     // ---- phase 4 (CTA 0): FC2 -> FC3 integer logits -> argmax
     if (rank == 0) {
-      if (img == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's FC2 / FC3 weight copies
+      if (it == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's FC2 / FC3 weight copies
       fused_dense_smem(h1, A.l1, f2w, A.l2, s_t2, s_f2, h2, nullptr);
       __syncthreads();
       fused_trace(A, img, 7);
