@@ -608,7 +608,7 @@ def run_latency(a):
            "device_us_per_image": device,
            "note": "value / back_to_back: one graph replay per image, bound by the host's cudaGraphLaunch (~16 us); "
                    "device_us_per_image: 200 single-image forwards captured in one CUDA graph (launch cost amortised), "
-                   "for the default whole-network cluster kernel (f1; the default for chunks of <= 7 images) and the 5-kernel PDL path",
+                   "for the default whole-network cluster kernel (f1; the default for chunks of <= 12 images) and the 5-kernel PDL path",
            "config": {"workload": "config 1: vehicle classifier, THRESH_RGB, 1000 random images one at a time, "
                                   "one CUDA graph replay per image",
                       "kernel": "fused_cluster_kernel" if bnn.forward_launches(net, 1) == 1 else net.layer_kernel(0, 1)},
@@ -650,7 +650,7 @@ def _device_latency(bnn, synth, dev, imgs):
         out[name] = e0.elapsed_time(e1) * 1e3 / (10 * R)
         classes.append(cls[::4].clone())
         net.close()
-    bnn.set_option("fused_max_n", 7)  # (the default)
+    bnn.set_option("fused_max_n", 12)  # (the default)
     out["classes_identical"] = bool(torch.equal(classes[0], classes[1]))
     out["images_per_graph"] = R
     return out

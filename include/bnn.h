@@ -126,10 +126,12 @@ BNN_API int bnn_version(void);
  *   "dense_ksplit"  1 (default): such a layer splits K over up to 4 CTA groups (+ a reduction kernel)
  *                   when its 128-image tile grid would leave SMs idle; 0: no split.
  *   "pdl"           1 (default): forward-path kernels use programmatic dependent launch.
- *   "fused_max_n"   forward chunks of n <= value images (default 7 = the 16-CTA clusters a B200 holds at once; 0 = off) of a vehicle-shaped net run as
+ *   "fused_max_n"   forward chunks of n <= value images (default 12; 0 = off) of a vehicle-shaped net run as
  *                   one whole-network kernel (a 16-CTA thread-block cluster; `fused_cluster` 0: cooperative grid).
  *   "fused_multi"   1 (default): that kernel runs one cluster per image of the chunk (up to the clusters the device
  *                   holds at once; a cluster serves images i, i + clusters, ...); 0: one cluster for the whole chunk.
+ *   "fused_cs"      0 (default): 16-CTA clusters while the chunk's images fit in one wave of them (7 on a B200), else
+ *                   8-CTA clusters; 8: always 8-CTA clusters.
  *   "fused_tc"      1 (default): that cluster kernel runs conv2 (k = 5, 32 -> 32 channels) and, for a 5x5x3 conv1,
  *                   conv1 on the tensor cores; 0: the integer pipe.
  *   "alg1"          0 (default); 1: bnn_forward runs the paper's own design instead -- Alg. 1

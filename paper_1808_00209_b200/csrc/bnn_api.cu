@@ -150,9 +150,10 @@ int g_opt_dense_tc = 1;       // 1: dense layers with n >= 256 and d >= 1024 run
 int g_opt_dense_tma = 1;      // 1: dense_tc4 activation stages arrive by TMA into a 4-deep ring
 
 int g_opt_fused_tc = 1;       // 1: the cluster kernel runs conv2 on the tensor cores (pool-in-N mxf4, one tile per CTA)
+int g_opt_fused_cs = 0;       // cluster size of fused_cluster_kernel: 0 = 16 where the device runs it and the chunk's images fit in one wave of 16-CTA clusters, else 8; 8 = always 8
 int g_opt_fused_multi = 1;    // 1: fused_cluster_kernel runs one cluster per image of a small batch; 0: one cluster
 int g_opt_fused_cluster = 1;  // 1: the fused small-batch path is the thread-block-cluster kernel (DSMEM, cluster barriers); 0: cooperative
-int g_opt_fused_max_n = 7;  // forward over n <= this images runs as one whole-network kernel where the topology allows (default 7: one 16-CTA cluster per image, 7 clusters fit at once: 11.3-11.7 us on the device for 1-7 images vs 13.0-15.7 us for the PDL layers; 8 images: 18.4 vs 16.0 us, so larger n run the batched layers)
+int g_opt_fused_max_n = 12;  // forward over n <= this images runs as one whole-network kernel where the topology allows (default 12: one cluster per image -- 16-CTA clusters for up to 7 images (what a B200 holds at once; 11.3-11.7 us on the device vs 13.0-15.7 us for the PDL layers), 8-CTA clusters beyond (12.5-12.7 us for 8-12 images vs 16.0-16.3 us; 16 images: 20.4 vs 16.8 us), larger n run the batched layers)
 int g_opt_pdl = 1;   // 1: forward-path kernels are launched with programmatic dependent launch
 int g_opt_alg1 = 0;  // 1: bnn_forward runs the paper's own design (Alg. 1 im2col + GEMM + pool + FC), for comparison
 int g_opt_csa = 1;      // 1: the XOR-popcount conv compresses each kernel row's K words with carry-save adders
@@ -1021,6 +1022,7 @@ int bnn_set_option(const char* key, int value) {
   if (strcmp(key, "dense_tma") == 0) { g_opt_dense_tma = value; return BNN_OK; }
   if (strcmp(key, "luma_fused") == 0) { g_opt_luma_fused = value; return BNN_OK; }
   if (strcmp(key, "fused_cluster") == 0) { g_opt_fused_cluster = value; return BNN_OK; }
+  if (strcmp(key, "fused_cs") == 0) { g_opt_fused_cs = value; return BNN_OK; }
   if (strcmp(key, "fused_multi") == 0) { g_opt_fused_multi = value ? 1 : 0; return BNN_OK; }
   return (int)fail(BNN_E_ARG, "bnn_set_option: unknown key '%s'", key);
 }
@@ -1319,11 +1321,12 @@ bnn_status launch_fused_small(bnn_net* net, const void* images, int nb, int32_t*
 // 16-CTA cluster of it, else 8; 0 if neither (then the cooperative kernel serves).  Returned as
 // size + 256 x (clusters of that size the device holds at once)
 template <typename F>
-int fused_cluster_size(F kfn, size_t smem) {
-  return dev_cached(reinterpret_cast<const char*>(kfn) + 2, [&] {
+int fused_cluster_size(F kfn, size_t smem, int only = 0) {
+  return dev_cached(reinterpret_cast<const char*>(kfn) + 2 + (only == 8), [&] {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     for (int cs : {kClusterMax, 8}) {
+      if (only != 0 && cs != only) continue;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)cs);
       cfg.blockDim = dim3(kFusedWarps * 32);
@@ -1363,7 +1366,13 @@ bnn_status launch_fused_cluster(bnn_net* net, const void* images, int nb, int32_
   const size_t smem = (size_t)FusedClusterLayout(net->h, net->w, net->c, a.k, 8, d1.l, d2.l, d3.l).total * 4;
   if (smem > 200 * 1024) return BNN_OK;
   auto go = [&](auto kfn) -> bnn_status {
-    const int cv = fused_cluster_size(kfn, smem), cs = cv & 255;
+    int cv = fused_cluster_size(kfn, smem, g_opt_fused_cs == 8 ? 8 : 0);
+    // more images than 16-CTA clusters fit at once: 8-CTA clusters (twice as many fit; ~1 us slower per image)
+    if (g_opt_fused_cs == 0 && g_opt_fused_multi && (cv & 255) == 16 && nb > (cv >> 8)) {
+      const int cv8 = fused_cluster_size(kfn, smem, 8);
+      if ((cv8 & 255) == 8) cv = cv8;
+    }
+    const int cs = cv & 255;
     if (cs == 0) return BNN_OK;
     // one cluster per image up to what the device holds at once (images are independent; a cluster
     // serves images cid, cid + ncl, ... when the batch is larger)

@@ -95,7 +95,7 @@ def test_validation_errors(L):
     doc = hdr[hdr.index("Process-wide tuning"):hdr.index("BNN_API int bnn_set_option")]
     keys = re.findall(r'\*\s+"(\w+)"', doc)
     assert {"conv_algo", "conv_tc", "conv_tc_fp4", "conv_pool_tc", "first_tma", "pdl"} <= set(keys)
-    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 255, "fused_max_n": 7, "alg1": 0, "first_fp4": 1, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1, "dense_ksplit": 1}
+    defaults = {"conv_algo": 0, "tiles_per_cta": 0, "gemv_max_n": 255, "fused_max_n": 12, "fused_cs": 0, "alg1": 0, "first_fp4": 1, "streams": 2, "csa": 1, "big_img": 1, "first_db": 1, "dense_ksplit": 1}
     for k in keys:
         if k == "first_exp":
             continue

@@ -394,7 +394,7 @@ def forward_vehicle_case(cuda, orc, mode, fused):
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 7)  # (the default)
+        cuda.set_option("fused_max_n", 12)  # (the default)
         cuda.set_option("fused_cluster", 1)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, mode, layers, T).forward(imgs.numpy(), threads=6)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
@@ -416,7 +416,7 @@ def test_forward_fused_cluster_shapes(cuda, orc, k1, k2, hw):
         outs = [net.forward(dev(imgs[:1])), net.forward(dev(imgs))]
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 7)  # (the default)
+        cuda.set_option("fused_max_n", 12)  # (the default)
     onet = oracle_net(orc, spec, 1, layers, T)
     for (lg, cls), x in zip(outs, (imgs[:1], imgs)):
         ref_l, ref_c = onet.forward(x.numpy(), threads=5)
@@ -562,7 +562,7 @@ def test_forward_thresholds_and_chunking(cuda, orc, fused, streams):
         logits, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 7)  # (the default)
+        cuda.set_option("fused_max_n", 12)  # (the default)
         cuda.set_option("streams", 2)
     ref_logits, ref_cls = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=5)
     assert np.array_equal(logits.cpu().numpy(), ref_logits)
@@ -601,7 +601,7 @@ def test_forward_staged_graph(cuda, orc, pdl, fused):
             assert np.array_equal(st_cls[:n].cpu().numpy(), ref_c)
     finally:
         cuda.set_option("pdl", 1)
-        cuda.set_option("fused_max_n", 7)  # (the default)
+        cuda.set_option("fused_max_n", 12)  # (the default)
         cuda.set_option("fused_cluster", 1)
 
 
@@ -828,12 +828,13 @@ def test_dense_tensor_core_two_cta_form(cuda, orc, n, d, l, flip, tma):
         assert cls[i] == orc.argmax(ra), "argmax mismatch image %d" % i
 
 
-@pytest.mark.parametrize("n", [2, 9, 20])
+@pytest.mark.parametrize("n", [2, 7, 9, 12, 20])
 @pytest.mark.parametrize("multi", [1, 0])
 def test_forward_fused_multi_cluster(cuda, orc, n, multi):
     """The whole-network cluster kernel (f1) over a small batch: multi = 1 launches one 16-CTA cluster per image up
-    to the clusters the device holds at once (n = 20: each cluster serves every ncl-th image, so the per-cluster
-    image count, barrier phases and box prefetch stride are exercised), multi = 0 one cluster for all images;
+    to the clusters the device holds at once -- 16-CTA clusters while the images fit in one wave of them (n = 2, 7),
+    8-CTA clusters beyond (n = 9, 12, 20; n = 20: each cluster serves every ncl-th image, so the per-cluster
+    image count, barrier phases and box prefetch stride are exercised) -- multi = 0 one cluster for all images;
     thresholds and flips, against the oracle."""
     net, layers, T = build_net(cuda, synth.VEHICLE, 1, 4600 + n, max_batch=32, thr=True)
     imgs = synth.images(n, 96, 96, 3, 4601 + n)
@@ -844,7 +845,7 @@ def test_forward_fused_multi_cluster(cuda, orc, n, multi):
         lg, cls = net.forward(dev(imgs))
         torch.cuda.synchronize()
     finally:
-        cuda.set_option("fused_max_n", 7)  # (the default)
+        cuda.set_option("fused_max_n", 12)  # (the default)
         cuda.set_option("fused_multi", 1)
     ref_l, ref_c = oracle_net(orc, synth.VEHICLE, 1, layers, T).forward(imgs.numpy(), threads=8)
     assert np.array_equal(lg.cpu().numpy(), ref_l) and np.array_equal(cls.cpu().numpy(), ref_c)

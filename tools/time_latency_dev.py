@@ -41,7 +41,7 @@ for name, fused in (("graph (5 kernels, PDL)", 0), ("cluster kernel (f1)", 8)):
     res[name] = e0.elapsed_time(e1) * 1e3 / (reps * R)
     res[name + " classes"] = cls[::4].clone()
     net.close()
-bnn.set_option("fused_max_n", 7)
+bnn.set_option("fused_max_n", 12)
 same = torch.equal(res["graph (5 kernels, PDL) classes"], res["cluster kernel (f1) classes"])
 for k, v in res.items():
     if not k.endswith("classes"):

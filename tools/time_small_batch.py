@@ -4,6 +4,7 @@ with one cluster for the batch (fused_multi = 0), and the layer-by-layer PDL pat
 usage: python tools/time_small_batch.py [R] [B,B,...]  The three
 must agree on every class."""
 import json
+import os
 import sys
 
 import torch
@@ -13,6 +14,7 @@ from paper_1808_00209_b200 import synth
 
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 layers = synth.make_weights(synth.VEHICLE, 1, 5)
+bnn.set_option("fused_cs", int(os.environ.get("BNN_FUSED_CS", "0")))  # 8: force 8-CTA clusters
 dl = [dict(L, wt=bnn.pack_weights(L["wt"].cuda())) for L in layers]
 out = []
 for B in [int(b) for b in (sys.argv[2].split(",") if len(sys.argv) > 2 else "1,2,4,8,9,16,32".split(","))]:
@@ -56,6 +58,7 @@ for B in [int(b) for b in (sys.argv[2].split(",") if len(sys.argv) > 2 else "1,2
     row["classes_identical"] = all(torch.equal(classes[0], c) for c in classes[1:])
     print(json.dumps(row), flush=True)
     out.append(row)
-bnn.set_option("fused_max_n", 7)
+bnn.set_option("fused_max_n", 12)
 bnn.set_option("fused_multi", 1)
 bnn.set_option("gemv_max_n", 255)
+bnn.set_option("fused_cs", 0)
